@@ -1,0 +1,132 @@
+/*
+ * treepipe_b200.h — C ABI of the B200-native SpecPipe step (arXiv 2504.04104).
+ *
+ * The reference (`/root/reference/pkg/src/treepipe`) is pure Python; its seam
+ * for this path is duck-typed module globals that `pipeline.py` binds at import
+ * (`pipeline.py:35`).  Each entry point below replaces one of those calls; the
+ * Python host mirror (`paper_2504_04104_b200/model.py`) binds them with ctypes
+ * under the reference names.  Plain pointers and sizes only: "host" arrays are
+ * CPU memory, "dev" pointers are CUDA device memory on the model's device.
+ *
+ * Status codes map onto the reference exception hierarchy (errors.py:4-49):
+ *   TP_ESHAPE -> ShapeError, TP_ECONTRACT -> ContractViolation,
+ *   TP_EINVARIANT / TP_ECUDA -> InvariantViolation, TP_ECONFIG -> ConfigError.
+ *
+ * Threading: calls on distinct stages may run concurrently (the reference's
+ * worker mode, pipeline.py:195-199,303-307); calls on one stage are serialised
+ * by the caller.  All kernels are deterministic (no float atomics) and
+ * batch-invariant: a node's result does not depend on which other nodes
+ * share the launch.
+ */
+#ifndef TREEPIPE_B200_H
+#define TREEPIPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TP_OK 0
+#define TP_ESHAPE 1
+#define TP_ECONTRACT 2
+#define TP_EINVARIANT 3
+#define TP_ECONFIG 4
+#define TP_ECUDA 5
+
+#define TP_ARCH_TOY 0   /* reference ToyModel: f64, LN, sinusoid, 1 head, ReLU FFN, tied head */
+#define TP_ARCH_LLAMA 1 /* Llama-shape: bf16 weights, RMSNorm, RoPE, GQA, SwiGLU, LM head */
+
+typedef struct tp_model tp_model; /* weights of a layer range on one device   */
+typedef struct tp_stage tp_stage; /* KV cache + workspace of one pipeline stage */
+
+typedef struct tp_model_config {
+  int32_t arch;
+  int32_t vocab, hidden, layers;             /* full-model shape                    */
+  int32_t heads, kv_heads, head_dim, ffn;    /* llama (toy: 1, 1, hidden, 2*hidden) */
+  int32_t layer_lo, layer_hi;                /* layers hosted by this object        */
+  int32_t with_embed, with_head;             /* embedding table / final norm + head */
+  int32_t device;
+  int32_t max_nodes;                         /* nodes per forward launch            */
+  float rope_theta, norm_eps;
+  int32_t weight_scale;                      /* llama: 1 = x sqrt(3/fan_in)/0.1     */
+} tp_model_config;
+
+/* One tree level (or prompt chunk) to push through a stage's layers.
+ * Node i attends cache rows [0, prefix_rows[i]) then, in increasing order,
+ * rows bits_base + b for every set bit b of anc_bits[i*words .. +words), then
+ * itself (self last) — the reference's `rows_for` + self
+ * (model.py:157-163, 265-271).  With append=1 node i's K/V become cache row
+ * rows()+i (KvCache.begin_row/append, model.py:136-152).                    */
+typedef struct tp_level {
+  int32_t n;
+  int32_t append;
+  const int32_t* tokens;      /* host [n]; read when hidden_in == NULL       */
+  const int32_t* positions;   /* host [n]                                     */
+  const int32_t* prefix_rows; /* host [n]                                     */
+  int32_t words;              /* u64 words per node mask (0 = none)          */
+  int32_t bits_base;          /* cache row addressed by bit 0                 */
+  const uint64_t* anc_bits;   /* host [n*words], self bit excluded           */
+  int32_t layer_lo, layer_hi; /* sub-range of the stage's layers (0,0 = all)  */
+} tp_level;
+
+const char* tp_last_error(void);
+int tp_device_count(int32_t* out);
+
+/* ---- model: replaces ToyModel(cfg) / init_model (model.py:207-236) ------- */
+int tp_model_create(const tp_model_config* cfg, tp_model** out);
+int tp_model_destroy(tp_model* m);
+/* LCG weight stream (model.py:28-44) generated on device, jump-ahead per thread. */
+int tp_model_init_lcg(tp_model* m, uint64_t seed, void* stream);
+/* The reference weight stream itself (lcg_uniform_stream, model.py:33-44): count
+ * f64 samples starting at stream index `start`, written to dev memory.          */
+int tp_lcg_uniform(int32_t device, uint64_t seed, int64_t start, int64_t count, void* out_dev, void* stream);
+/* Raw tensor I/O (checkpoint import/export, model.py:388-435; tests).
+ * which: 0 embedding, 1..6 toy Wq,Wk,Wv,Wo,W1,W2 ([in,out] row-major f64);
+ *        llama: 1 Wq 2 Wk 3 Wv 4 Wo 5 Wgate 6 Wup 7 Wdown ([out,in] bf16), 8 lm_head. */
+int tp_model_tensor_bytes(const tp_model* m, int32_t which, int32_t layer, int64_t* nbytes);
+int tp_model_write_tensor(tp_model* m, int32_t which, int32_t layer, const void* host, int64_t nbytes);
+int tp_model_read_tensor(const tp_model* m, int32_t which, int32_t layer, void* host, int64_t nbytes);
+
+/* ToyModel.embed (model.py:239-240) / Llama token embedding, n rows -> dev. */
+int tp_model_embed(tp_model* m, int32_t n, const int32_t* tokens, const int32_t* positions,
+                   void* out_dev, void* stream);
+/* ToyModel.head (model.py:242-244): final norm + head, n rows -> f32/f64 logits (dev). */
+int tp_model_logits(tp_model* m, tp_stage* ws, int32_t n, const void* hidden_dev, void* logits_dev,
+                    void* stream);
+/* Verify (model.py:247-248 + pipeline.py:328-339): greedy token of one hidden
+ * row (first argmax) and the first child whose token matches.  result_host =
+ * {token, child_index or -1}; synchronises the stream.                        */
+int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
+                    int32_t n_children, int32_t* result_host, void* stream);
+
+/* ---- stage: replaces KvCache (model.py:105-204) + forward_tree (:312-349) - */
+int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t capacity_rows,
+                    tp_stage** out);
+int tp_stage_destroy(tp_stage* s);
+int tp_stage_rows(const tp_stage* s, int32_t* rows);
+/* forward_tree / forward_position for the stage's layers.  hidden: [n, hidden]
+ * (f64 toy, f32 llama residual stream).  hidden_in == NULL embeds tokens.  */
+int tp_stage_forward(tp_stage* s, const tp_level* level, const void* hidden_in, void* hidden_out,
+                     void* stream);
+/* Pruning propagation (KvCache.promote/prune/_restrict/drop_speculative,
+ * model.py:169-194): rows < first_row stay; of rows [first_row, first_row+count)
+ * those with keep bit set are compacted stably to follow them; the rest and
+ * every row beyond are dropped.                                              */
+int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64_t* keep_bits,
+                     void* stream);
+int tp_stage_truncate(tp_stage* s, int32_t rows);
+/* Copy K (kind 0) or V (kind 1) of one layer, rows [lo,hi), as [rows][kv_heads][head_dim]. */
+int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo, int32_t hi, void* host);
+
+/* ---- transmit: in-flight embedding filter (pipeline.py:379-400) ---------- */
+/* dst[j] = src[i_j] for the set bits i_0 < i_1 < ... of keep_bits (n_src rows of row_bytes). */
+int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t row_bytes, int32_t n_src,
+                    const uint64_t* keep_bits, int32_t* n_out, void* stream);
+/* Grow the KV capacity (reference KvCache grow-by-doubling, model.py:141-148). */
+int tp_stage_reserve(tp_stage* s, int32_t capacity_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TREEPIPE_B200_H */

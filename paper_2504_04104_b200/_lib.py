@@ -1,0 +1,129 @@
+"""ctypes binding of ``libtreepipe_b200.so`` (the C ABI in include/treepipe_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, :func:`lib` raises.  ctypes releases the GIL for every call, so
+distinct stages can be driven from worker threads (reference worker mode,
+`pipeline.py:195-199`).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import ConfigError, ContractViolation, InvariantViolation, ShapeError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtreepipe_b200.so")
+
+TP_OK, TP_ESHAPE, TP_ECONTRACT, TP_EINVARIANT, TP_ECONFIG, TP_ECUDA = range(6)
+ARCH_TOY, ARCH_LLAMA = 0, 1
+
+_ERRORS = {
+    TP_ESHAPE: ShapeError,
+    TP_ECONTRACT: ContractViolation,
+    TP_EINVARIANT: InvariantViolation,
+    TP_ECONFIG: ConfigError,
+    TP_ECUDA: InvariantViolation,
+}
+
+
+class ModelConfig(C.Structure):
+    _fields_ = [
+        ("arch", C.c_int32), ("vocab", C.c_int32), ("hidden", C.c_int32), ("layers", C.c_int32),
+        ("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32),
+        ("layer_lo", C.c_int32), ("layer_hi", C.c_int32), ("with_embed", C.c_int32),
+        ("with_head", C.c_int32), ("device", C.c_int32), ("max_nodes", C.c_int32),
+        ("rope_theta", C.c_float), ("norm_eps", C.c_float), ("weight_scale", C.c_int32),
+    ]
+
+
+class Level(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("append", C.c_int32), ("tokens", C.c_void_p), ("positions", C.c_void_p),
+        ("prefix_rows", C.c_void_p), ("words", C.c_int32), ("bits_base", C.c_int32),
+        ("anc_bits", C.c_void_p), ("layer_lo", C.c_int32), ("layer_hi", C.c_int32),
+    ]
+
+
+_P = C.c_void_p
+_I = C.c_int32
+_SIGS = {
+    "tp_last_error": (C.c_char_p, []),
+    "tp_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
+    "tp_model_create": (C.c_int, [C.POINTER(ModelConfig), C.POINTER(_P)]),
+    "tp_model_destroy": (C.c_int, [_P]),
+    "tp_model_init_lcg": (C.c_int, [_P, C.c_uint64, _P]),
+    "tp_lcg_uniform": (C.c_int, [_I, C.c_uint64, C.c_int64, C.c_int64, _P, _P]),
+    "tp_model_tensor_bytes": (C.c_int, [_P, _I, _I, C.POINTER(C.c_int64)]),
+    "tp_model_write_tensor": (C.c_int, [_P, _I, _I, _P, C.c_int64]),
+    "tp_model_read_tensor": (C.c_int, [_P, _I, _I, _P, C.c_int64]),
+    "tp_model_embed": (C.c_int, [_P, _I, _P, _P, _P, _P]),
+    "tp_model_logits": (C.c_int, [_P, _P, _I, _P, _P, _P]),
+    "tp_model_verify": (C.c_int, [_P, _P, _P, _P, _I, _P, _P]),
+    "tp_stage_create": (C.c_int, [_P, _I, _I, _I, C.POINTER(_P)]),
+    "tp_stage_destroy": (C.c_int, [_P]),
+    "tp_stage_rows": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+    "tp_stage_reserve": (C.c_int, [_P, _I]),
+    "tp_stage_forward": (C.c_int, [_P, C.POINTER(Level), _P, _P, _P]),
+    "tp_stage_compact": (C.c_int, [_P, _I, _I, _P, _P]),
+    "tp_stage_truncate": (C.c_int, [_P, _I]),
+    "tp_stage_read_kv": (C.c_int, [_P, _I, _I, _I, _I, _P]),
+    "tp_rows_compact": (C.c_int, [_P, _P, _P, C.c_int64, _I, _P, C.POINTER(C.c_int32), _P]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib: C.CDLL | None = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load the shared library and declare every signature (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise InvariantViolation(
+                    f"{path} missing: build it with `python -m paper_2504_04104_b200.build` "
+                    "(there is no CPU fallback)")
+            cdll = C.CDLL(path)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(cdll, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = cdll
+    return _lib
+
+
+def lib() -> C.CDLL:
+    """The library, after checking a CUDA device is present."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise InvariantViolation("no CUDA device visible: the B200 path has no CPU fallback")
+    return load()
+
+
+def check(status: int) -> None:
+    if status == TP_OK:
+        return
+    msg = (load().tp_last_error() or b"").decode(errors="replace")
+    raise _ERRORS.get(status, InvariantViolation)(msg or f"treepipe_b200 status {status}")
+
+
+def ptr(arr) -> int | None:
+    """Address of a numpy array / torch tensor (None for None)."""
+    if arr is None:
+        return None
+    if hasattr(arr, "data_ptr"):
+        return arr.data_ptr()
+    return arr.ctypes.data
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,479 @@
+// C-ABI of libtreepipe_b200.so (see include/treepipe_b200.h for the contract and
+// the reference call each entry point replaces).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+
+namespace tp {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace tp
+
+using namespace tp;
+
+namespace {
+
+struct ToyTensorSpec {
+  int64_t rows, cols;
+};
+
+// toy per-layer tensors in generation order (model.py:224-233)
+ToyTensorSpec toy_spec(int d, int which) {
+  switch (which) {
+    case 1: case 2: case 3: case 4: return {d, d};
+    case 5: return {d, 2 * d};
+    case 6: return {2 * d, d};
+  }
+  return {0, 0};
+}
+
+size_t meta_capacity(const tp_model* m, int cap, int* words) {
+  *words = (cap + 64) / 64 + 1;
+  size_t n = (size_t)std::max(m->cfg.max_nodes, 64);
+  size_t bytes = n * 4 * 4                       // tokens, positions, prefix rows, children
+                 + n * (size_t)(*words) * 8      // anc bits
+                 + (size_t)(cap + 64) * 4        // compaction / gather index lists
+                 + 256;
+  return (bytes + 255) & ~(size_t)255;
+}
+
+int upload(tp_stage* s, const void* host, size_t bytes, size_t dev_off, cudaStream_t st) {
+  TP_CHECK(dev_off + bytes <= s->meta_bytes, TP_ESHAPE, "metadata exceeds stage staging buffer");
+  TP_CUDA(cudaEventSynchronize(s->meta_done));  // previous upload has left the pinned buffer
+  std::memcpy(s->host_meta + dev_off, host, bytes);
+  TP_CUDA(cudaMemcpyAsync(s->meta + dev_off, s->host_meta + dev_off, bytes, cudaMemcpyHostToDevice, st));
+  TP_CUDA(cudaEventRecord(s->meta_done, st));
+  return TP_OK;
+}
+
+int alloc_kv(tp_stage* s, int cap) {
+  int nl = s->hi - s->lo;
+  size_t plane = (size_t)s->kv_heads * cap * s->head_dim * s->esize;
+  std::vector<void*> k(nl), v(nl);
+  for (int l = 0; l < nl; ++l) {
+    TP_CUDA(cudaMalloc(&k[l], plane));
+    TP_CUDA(cudaMalloc(&v[l], plane));
+    TP_CUDA(cudaMemset(k[l], 0, plane));
+    TP_CUDA(cudaMemset(v[l], 0, plane));
+    if (!s->k.empty()) {  // reserve(): carry rows over, head plane by head plane
+      size_t row = (size_t)s->head_dim * s->esize;
+      for (int h = 0; h < s->kv_heads; ++h) {
+        TP_CUDA(cudaMemcpy((char*)k[l] + h * cap * row, (char*)s->k[l] + h * (size_t)s->cap * row,
+                           (size_t)s->rows * row, cudaMemcpyDeviceToDevice));
+        TP_CUDA(cudaMemcpy((char*)v[l] + h * cap * row, (char*)s->v[l] + h * (size_t)s->cap * row,
+                           (size_t)s->rows * row, cudaMemcpyDeviceToDevice));
+      }
+      cudaFree(s->k[l]);
+      cudaFree(s->v[l]);
+    }
+  }
+  s->k = k;
+  s->v = v;
+  s->cap = cap;
+  std::vector<void*> planes(2 * nl);
+  for (int l = 0; l < nl; ++l) {
+    planes[2 * l] = k[l];
+    planes[2 * l + 1] = v[l];
+  }
+  if (s->d_planes) cudaFree(s->d_planes);
+  TP_CUDA(cudaMalloc(&s->d_planes, sizeof(void*) * std::max(1, 2 * nl)));
+  if (nl) TP_CUDA(cudaMemcpy(s->d_planes, planes.data(), sizeof(void*) * 2 * nl, cudaMemcpyHostToDevice));
+  // metadata staging follows capacity
+  if (s->meta) cudaFree(s->meta);
+  if (s->host_meta) cudaFreeHost(s->host_meta);
+  s->meta_bytes = meta_capacity(s->m, cap, &s->max_words);
+  TP_CUDA(cudaMalloc((void**)&s->meta, s->meta_bytes));
+  TP_CUDA(cudaMallocHost((void**)&s->host_meta, s->meta_bytes));
+  return TP_OK;
+}
+
+bool is_toy(const tp_model* m) { return m->cfg.arch == TP_ARCH_TOY; }
+
+}  // namespace
+
+extern "C" {
+
+const char* tp_last_error(void) { return g_err.c_str(); }
+
+int tp_device_count(int32_t* out) {
+  int n = 0;
+  TP_CUDA(cudaGetDeviceCount(&n));
+  *out = n;
+  return TP_OK;
+}
+
+int tp_model_create(const tp_model_config* cfg, tp_model** out) {
+  TP_CHECK(cfg && out, TP_ECONFIG, "null argument");
+  const tp_model_config& c = *cfg;
+  TP_CHECK(c.arch == TP_ARCH_TOY || c.arch == TP_ARCH_LLAMA, TP_ECONFIG, "unknown arch");
+  TP_CHECK(c.vocab >= 16, TP_ESHAPE, "vocab must be at least 16");
+  TP_CHECK(c.hidden >= 2 && c.hidden % 2 == 0, TP_ESHAPE, "hidden dim must be even");
+  TP_CHECK(c.layers >= 1, TP_ESHAPE, "need at least one layer");
+  TP_CHECK(0 <= c.layer_lo && c.layer_lo <= c.layer_hi && c.layer_hi <= c.layers, TP_ECONFIG,
+           "hosted layer range outside the model");
+  TP_CHECK(c.max_nodes >= 1 && c.max_nodes <= 1024, TP_ECONFIG, "max_nodes must lie in [1, 1024]");
+  TP_CUDA(cudaSetDevice(c.device));
+  tp_model* m = new tp_model();
+  m->cfg = c;
+  int rc = TP_OK;
+  const int64_t d = c.hidden, V = c.vocab;
+  if (is_toy(m)) {
+    m->cfg.heads = m->cfg.kv_heads = 1;
+    m->cfg.head_dim = c.hidden;
+    m->cfg.ffn = 2 * c.hidden;
+    if (c.with_embed || c.with_head) {
+      m->embed_bytes = V * d * 8;
+      if (cudaMalloc(&m->embed, m->embed_bytes) != cudaSuccess) rc = TP_ECUDA;
+    }
+    for (int l = c.layer_lo; l < c.layer_hi && rc == TP_OK; ++l) {
+      tp_layer_weights w;
+      for (int t = 1; t <= 6; ++t) {
+        ToyTensorSpec sp = toy_spec((int)d, t);
+        w.bytes[t] = sp.rows * sp.cols * 8;
+        if (cudaMalloc(&w.w[t], w.bytes[t]) != cudaSuccess) rc = TP_ECUDA;
+      }
+      m->layers.push_back(w);
+    }
+  } else {
+    TP_CHECK(c.heads >= 1 && c.kv_heads >= 1 && c.heads % c.kv_heads == 0, TP_ESHAPE,
+             "heads must be a multiple of kv_heads");
+    TP_CHECK(c.head_dim == 128, TP_ESHAPE, "llama path supports head_dim 128");
+    TP_CHECK(c.hidden % 128 == 0 && c.ffn % 128 == 0, TP_ESHAPE, "hidden and ffn must be multiples of 128");
+    const int64_t q = (int64_t)c.heads * c.head_dim, kv = (int64_t)c.kv_heads * c.head_dim, f = c.ffn;
+    if (c.with_embed) {
+      m->embed_bytes = V * d * 2;
+      if (cudaMalloc(&m->embed, m->embed_bytes) != cudaSuccess) rc = TP_ECUDA;
+    }
+    if (c.with_head) {
+      m->head_bytes = V * d * 2;
+      if (cudaMalloc(&m->head, m->head_bytes) != cudaSuccess) rc = TP_ECUDA;
+    }
+    for (int l = c.layer_lo; l < c.layer_hi && rc == TP_OK; ++l) {
+      tp_layer_weights w;
+      w.bytes[1] = (q + 2 * kv) * d * 2;  // fused [Wq; Wk; Wv]  ([out, in])
+      w.bytes[4] = d * q * 2;             // Wo
+      w.bytes[5] = 2 * f * d * 2;         // fused gate/up, 64-row interleave
+      w.bytes[7] = d * f * 2;             // Wdown
+      for (int t : {1, 4, 5, 7})
+        if (cudaMalloc(&w.w[t], w.bytes[t]) != cudaSuccess) rc = TP_ECUDA;
+      m->layers.push_back(w);
+    }
+  }
+  if (rc != TP_OK) {
+    set_error("cudaMalloc failed while allocating weights");
+    tp_model_destroy(m);
+    return rc;
+  }
+  *out = m;
+  return TP_OK;
+}
+
+int tp_model_destroy(tp_model* m) {
+  if (!m) return TP_OK;
+  cudaSetDevice(m->cfg.device);
+  if (m->embed) cudaFree(m->embed);
+  if (m->head) cudaFree(m->head);
+  for (auto& w : m->layers)
+    for (void* p : w.w)
+      if (p) cudaFree(p);
+  if (m->tma_cache) free(m->tma_cache);
+  delete m;
+  return TP_OK;
+}
+
+int tp_model_init_lcg(tp_model* m, uint64_t seed, void* stream) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!is_toy(m)) {
+    TP_TRY(llama_init_weights(m, seed, st));
+    TP_CUDA(cudaStreamSynchronize(st));
+    return TP_OK;
+  }
+  const int64_t d = m->cfg.hidden, V = m->cfg.vocab;
+  const int64_t per_layer = 8 * d * d;
+  if (m->embed) TP_TRY(lcg_fill_f64((double*)m->embed, V * d, seed, 0, st));
+  for (int l = m->cfg.layer_lo; l < m->cfg.layer_hi; ++l) {
+    int64_t off = V * d + (int64_t)l * per_layer;
+    const tp_layer_weights& w = m->layers[l - m->cfg.layer_lo];
+    for (int t = 1; t <= 6; ++t) {
+      int64_t cnt = w.bytes[t] / 8;
+      TP_TRY(lcg_fill_f64((double*)w.w[t], cnt, seed, off, st));
+      off += cnt;
+    }
+  }
+  TP_CUDA(cudaStreamSynchronize(st));
+  return TP_OK;
+}
+
+int tp_lcg_uniform(int32_t device, uint64_t seed, int64_t start, int64_t count, void* out_dev, void* stream) {
+  TP_CUDA(cudaSetDevice(device));
+  TP_CHECK(count >= 0 && start >= 0, TP_ESHAPE, "negative range");
+  if (count == 0) return TP_OK;
+  return lcg_fill_f64((double*)out_dev, count, seed, start, (cudaStream_t)stream);
+}
+
+static int tensor_ptr(const tp_model* m, int which, int layer, void** p, int64_t* bytes) {
+  if (which == 0) {
+    *p = m->embed;
+    *bytes = m->embed_bytes;
+  } else if (which == 8 && !is_toy(m)) {
+    *p = m->head;
+    *bytes = m->head_bytes;
+  } else {
+    TP_CHECK(layer >= m->cfg.layer_lo && layer < m->cfg.layer_hi, TP_ESHAPE, "layer not hosted by model");
+    TP_CHECK(which >= 1 && which <= 7, TP_ESHAPE, "bad tensor id");
+    const tp_layer_weights& w = m->layers[layer - m->cfg.layer_lo];
+    *p = w.w[which];
+    *bytes = w.bytes[which];
+  }
+  TP_CHECK(*p != nullptr, TP_ESHAPE, "tensor not present (llama tensors are fused: ids 1,4,5,7)");
+  return TP_OK;
+}
+
+int tp_model_tensor_bytes(const tp_model* m, int32_t which, int32_t layer, int64_t* nbytes) {
+  void* p;
+  return tensor_ptr(m, which, layer, &p, nbytes);
+}
+
+int tp_model_write_tensor(tp_model* m, int32_t which, int32_t layer, const void* host, int64_t nbytes) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  void* p;
+  int64_t b;
+  TP_TRY(tensor_ptr(m, which, layer, &p, &b));
+  TP_CHECK(b == nbytes, TP_ESHAPE, "tensor size mismatch");
+  TP_CUDA(cudaMemcpy(p, host, b, cudaMemcpyHostToDevice));
+  return TP_OK;
+}
+
+int tp_model_read_tensor(const tp_model* m, int32_t which, int32_t layer, void* host, int64_t nbytes) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  void* p;
+  int64_t b;
+  TP_TRY(tensor_ptr(m, which, layer, &p, &b));
+  TP_CHECK(b == nbytes, TP_ESHAPE, "tensor size mismatch");
+  TP_CUDA(cudaMemcpy(host, p, b, cudaMemcpyDeviceToHost));
+  return TP_OK;
+}
+
+int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t capacity_rows, tp_stage** out) {
+  TP_CHECK(m && out, TP_ECONFIG, "null argument");
+  TP_CHECK(m->cfg.layer_lo <= layer_lo && layer_lo <= layer_hi && layer_hi <= m->cfg.layer_hi, TP_ECONFIG,
+           "stage layers must be hosted by the model");
+  TP_CHECK(capacity_rows >= 1, TP_ECONFIG, "capacity must be positive");
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  tp_stage* s = new tp_stage();
+  s->m = m;
+  s->lo = layer_lo;
+  s->hi = layer_hi;
+  if (is_toy(m)) {
+    s->kv_heads = 1;
+    s->head_dim = m->cfg.hidden;
+    s->esize = 8;
+    TP_TRY(toy_workspace_bytes(m, m->cfg.max_nodes, &s->ws_bytes));
+  } else {
+    s->kv_heads = m->cfg.kv_heads;
+    s->head_dim = m->cfg.head_dim;
+    s->esize = 2;
+    TP_TRY(llama_workspace_bytes(m, m->cfg.max_nodes, &s->ws_bytes));
+  }
+  int rc = alloc_kv(s, capacity_rows);
+  if (rc != TP_OK) {
+    tp_stage_destroy(s);
+    return rc;
+  }
+  TP_CUDA(cudaMalloc((void**)&s->ws, s->ws_bytes));
+  TP_CUDA(cudaMemset(s->ws, 0, s->ws_bytes));
+  TP_CUDA(cudaEventCreateWithFlags(&s->meta_done, cudaEventDisableTiming));
+  TP_CUDA(cudaEventRecord(s->meta_done, 0));
+  TP_CUDA(cudaMalloc((void**)&s->d_result, 16));
+  TP_CUDA(cudaMallocHost((void**)&s->h_result, 16));
+  TP_CUDA(cudaMalloc(&s->logits, (size_t)m->cfg.vocab * 8));
+  *out = s;
+  return TP_OK;
+}
+
+int tp_stage_destroy(tp_stage* s) {
+  if (!s) return TP_OK;
+  cudaSetDevice(s->m->cfg.device);
+  for (void* p : s->k) cudaFree(p);
+  for (void* p : s->v) cudaFree(p);
+  if (s->ws) cudaFree(s->ws);
+  if (s->meta) cudaFree(s->meta);
+  if (s->host_meta) cudaFreeHost(s->host_meta);
+  if (s->meta_done) cudaEventDestroy(s->meta_done);
+  if (s->d_result) cudaFree(s->d_result);
+  if (s->h_result) cudaFreeHost(s->h_result);
+  if (s->d_planes) cudaFree(s->d_planes);
+  if (s->logits) cudaFree(s->logits);
+  delete s;
+  return TP_OK;
+}
+
+int tp_stage_rows(const tp_stage* s, int32_t* rows) {
+  *rows = s->rows;
+  return TP_OK;
+}
+
+int tp_stage_reserve(tp_stage* s, int32_t capacity_rows) {
+  if (capacity_rows <= s->cap) return TP_OK;
+  TP_CUDA(cudaSetDevice(s->m->cfg.device));
+  TP_CUDA(cudaDeviceSynchronize());
+  return alloc_kv(s, capacity_rows);
+}
+
+int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, void* stream) {
+  TP_CHECK(s && L && hidden_out, TP_ECONFIG, "null argument");
+  tp_model* m = s->m;
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = L->n;
+  TP_CHECK(n >= 1 && n <= m->cfg.max_nodes, TP_ESHAPE, "level size outside [1, max_nodes]");
+  TP_CHECK(L->positions && L->prefix_rows, TP_ECONFIG, "positions and prefix_rows are required");
+  TP_CHECK(hidden_in || (L->tokens && m->embed), TP_ECONFIG, "need hidden_in or tokens + embedding");
+  TP_CHECK(L->words >= 0 && L->words <= s->max_words, TP_ESHAPE, "too many mask words for this stage");
+  TP_CHECK(!L->append || s->rows + n <= s->cap, TP_ESHAPE, "KV capacity exceeded (reserve first)");
+  const int visible = s->rows + (L->append ? n : 0);
+  for (int i = 0; i < n; ++i) {
+    TP_CHECK(L->prefix_rows[i] >= 0 && L->prefix_rows[i] <= visible, TP_ECONTRACT, "prefix rows beyond cache");
+    if (L->tokens && !hidden_in)
+      TP_CHECK(L->tokens[i] >= 0 && L->tokens[i] < m->cfg.vocab, TP_ESHAPE, "token outside vocabulary");
+    for (int w = 0; w < L->words; ++w) {
+      uint64_t bits = L->anc_bits[(int64_t)i * L->words + w];
+      if (!bits) continue;
+      int hi_bit = 63 - __builtin_clzll(bits), lo_bit = __builtin_ctzll(bits);
+      TP_CHECK(L->bits_base + w * 64 + lo_bit >= 0 && L->bits_base + w * 64 + hi_bit < visible, TP_ECONTRACT,
+               "ancestor row outside the cache");
+    }
+  }
+  // pack metadata: tokens | positions | prefix | anc (8-aligned)
+  size_t off_tok = 0, off_pos = 4 * (size_t)n, off_pre = 8 * (size_t)n;
+  size_t off_anc = ((12 * (size_t)n) + 7) & ~(size_t)7;
+  size_t total = off_anc + 8 * (size_t)n * L->words;
+  TP_CHECK(total <= s->meta_bytes, TP_ESHAPE, "metadata exceeds stage staging buffer");
+  TP_CUDA(cudaEventSynchronize(s->meta_done));
+  char* h = s->host_meta;
+  if (L->tokens) std::memcpy(h + off_tok, L->tokens, 4 * (size_t)n);
+  else std::memset(h + off_tok, 0, 4 * (size_t)n);
+  std::memcpy(h + off_pos, L->positions, 4 * (size_t)n);
+  std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
+  if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
+  TP_CUDA(cudaMemcpyAsync(s->meta, h, total, cudaMemcpyHostToDevice, st));
+  TP_CUDA(cudaEventRecord(s->meta_done, st));
+  LevelDev lv;
+  lv.n = n;
+  lv.append = L->append;
+  lv.row0 = s->rows;
+  lv.words = L->words;
+  lv.bits_base = L->bits_base;
+  const bool all_layers = L->layer_lo == 0 && L->layer_hi == 0;
+  const bool no_layers = L->layer_lo < 0;  // explicit empty range: embed/copy only
+  lv.layer_lo = all_layers ? s->lo : (no_layers ? s->lo : L->layer_lo);
+  lv.layer_hi = all_layers ? s->hi : (no_layers ? s->lo : L->layer_hi);
+  TP_CHECK(s->lo <= lv.layer_lo && lv.layer_lo <= lv.layer_hi && lv.layer_hi <= s->hi, TP_ESHAPE,
+           "layer range not hosted by this stage");
+  lv.tokens = (const int32_t*)(s->meta + off_tok);
+  lv.positions = (const int32_t*)(s->meta + off_pos);
+  lv.prefix_rows = (const int32_t*)(s->meta + off_pre);
+  lv.anc = (const uint64_t*)(s->meta + off_anc);
+  int rc = is_toy(m) ? toy_forward(s, lv, hidden_in, hidden_out, st) : llama_forward(s, lv, hidden_in, hidden_out, st);
+  if (rc != TP_OK) return rc;
+  if (L->append) s->rows += n;
+  return TP_OK;
+}
+
+int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64_t* keep_bits, void* stream) {
+  TP_CUDA(cudaSetDevice(s->m->cfg.device));
+  TP_CHECK(first_row >= 0 && count >= 0 && first_row + count <= s->rows, TP_ECONTRACT,
+           "compaction window outside the cache (prefix rows cannot be dropped)");
+  std::vector<int32_t> src;
+  src.reserve(count);
+  for (int j = 0; j < count; ++j)
+    if ((keep_bits[j >> 6] >> (j & 63)) & 1ull) src.push_back(first_row + j);
+  if (!src.empty()) {
+    cudaStream_t st = (cudaStream_t)stream;
+    TP_TRY(upload(s, src.data(), src.size() * 4, 0, st));
+    TP_TRY(kv_compact(s, (const int32_t*)s->meta, (int)src.size(), first_row, s->d_planes, st));
+  }
+  s->rows = first_row + (int)src.size();
+  return TP_OK;
+}
+
+int tp_stage_truncate(tp_stage* s, int32_t rows) {
+  TP_CHECK(rows >= 0 && rows <= s->rows, TP_ECONTRACT, "truncate beyond filled rows");
+  s->rows = rows;
+  return TP_OK;
+}
+
+int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo, int32_t hi, void* host) {
+  TP_CUDA(cudaSetDevice(s->m->cfg.device));
+  TP_CHECK(layer >= s->lo && layer < s->hi, TP_ESHAPE, "layer not hosted by stage");
+  TP_CHECK(0 <= lo && lo <= hi && hi <= s->cap, TP_ESHAPE, "row range outside capacity");
+  if (hi == lo) return TP_OK;
+  const char* plane = (const char*)(kind == 0 ? s->k : s->v)[layer - s->lo];
+  size_t row = (size_t)s->head_dim * s->esize;
+  TP_CUDA(cudaDeviceSynchronize());
+  for (int h = 0; h < s->kv_heads; ++h)
+    TP_CUDA(cudaMemcpy2D((char*)host + h * row, row * s->kv_heads, plane + (h * (size_t)s->cap + lo) * row, row,
+                         row, hi - lo, cudaMemcpyDeviceToHost));
+  return TP_OK;
+}
+
+int tp_model_embed(tp_model* m, int32_t n, const int32_t* tokens, const int32_t* positions, void* out_dev,
+                   void* stream) {
+  // uses a transient stage-free path: small synchronous upload
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
+  for (int i = 0; i < n; ++i) TP_CHECK(tokens[i] >= 0 && tokens[i] < m->cfg.vocab, TP_ESHAPE, "token outside vocabulary");
+  int32_t* d = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  TP_CUDA(cudaMallocAsync((void**)&d, 8 * (size_t)n, st));
+  TP_CUDA(cudaMemcpyAsync(d, tokens, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  TP_CUDA(cudaMemcpyAsync(d + n, positions, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  int rc = is_toy(m) ? toy_embed(m, n, d, d + n, (double*)out_dev, st) : llama_embed(m, n, d, (float*)out_dev, st);
+  cudaFreeAsync(d, st);
+  return rc;
+}
+
+int tp_model_logits(tp_model* m, tp_stage* ws, int32_t n, const void* hidden_dev, void* logits_dev, void* stream) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  TP_CHECK(ws && ws->m == m, TP_ECONFIG, "workspace stage must belong to the model");
+  TP_CHECK(n >= 1 && n <= m->cfg.max_nodes, TP_ESHAPE, "rows outside [1, max_nodes]");
+  cudaStream_t st = (cudaStream_t)stream;
+  return is_toy(m) ? toy_logits(m, ws, n, (const double*)hidden_dev, (double*)logits_dev, st)
+                   : llama_logits(m, ws, n, (const float*)hidden_dev, (float*)logits_dev, st);
+}
+
+int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
+                    int32_t n_children, int32_t* result_host, void* stream) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  TP_CHECK(ws && ws->m == m, TP_ECONFIG, "workspace stage must belong to the model");
+  TP_CHECK(n_children >= 0 && n_children <= m->cfg.max_nodes, TP_ESHAPE, "too many children");
+  cudaStream_t st = (cudaStream_t)stream;
+  TP_TRY(tp_model_logits(m, ws, 1, hidden_dev, ws->logits, stream));
+  if (n_children) TP_TRY(upload(ws, child_tokens, 4 * (size_t)n_children, 0, st));
+  TP_TRY(argmax_match(ws->logits, is_toy(m), m->cfg.vocab, (const int32_t*)ws->meta, n_children, ws->d_result, st));
+  TP_CUDA(cudaMemcpyAsync(ws->h_result, ws->d_result, 8, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaStreamSynchronize(st));
+  result_host[0] = ws->h_result[0];
+  result_host[1] = ws->h_result[1];
+  return TP_OK;
+}
+
+int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t row_bytes, int32_t n_src,
+                    const uint64_t* keep_bits, int32_t* n_out, void* stream) {
+  TP_CUDA(cudaSetDevice(ws->m->cfg.device));
+  std::vector<int32_t> idx;
+  for (int j = 0; j < n_src; ++j)
+    if ((keep_bits[j >> 6] >> (j & 63)) & 1ull) idx.push_back(j);
+  *n_out = (int32_t)idx.size();
+  if (idx.empty()) return TP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  TP_TRY(upload(ws, idx.data(), idx.size() * 4, 0, st));
+  return rows_compact(src_dev, dst_dev, row_bytes, (const int32_t*)ws->meta, (int)idx.size(), st);
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Internal object layout shared by the C-ABI (api.cu) and the kernel files.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+// Per-layer weights.  Toy: f64 [in,out] row-major as the reference stores
+// them (model.py:72-80).  Llama: bf16 [out,in] (K-major for the swap-AB
+// tcgen05 GEMM: weights are the MMA "A" operand, tree nodes the "B" operand).
+struct tp_layer_weights {
+  void* w[8] = {nullptr};
+  int64_t bytes[8] = {0};
+};
+
+struct tp_model {
+  tp_model_config cfg;
+  void* embed = nullptr;  // [V, d] (f64 toy / bf16 llama)
+  void* head = nullptr;   // llama lm_head [V, d] bf16 (toy: tied to embed)
+  int64_t embed_bytes = 0, head_bytes = 0;
+  std::vector<tp_layer_weights> layers;  // index layer - cfg.layer_lo
+  // llama: tensor maps for TMA live beside the weights (filled lazily)
+  void* tma_cache = nullptr;
+};
+
+struct tp_stage {
+  tp_model* m = nullptr;
+  int lo = 0, hi = 0;     // hosted layers
+  int cap = 0, rows = 0;  // KV capacity / filled rows
+  int kv_heads = 1, head_dim = 0, esize = 8;
+  std::vector<void*> k, v;  // per hosted layer [kv_heads][cap][head_dim]
+  // device workspace
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  // device metadata block (tokens, positions, prefix rows, anc bits, extras)
+  char* meta = nullptr;
+  size_t meta_bytes = 0;
+  int max_words = 0;
+  // pinned host staging for metadata uploads
+  char* host_meta = nullptr;
+  cudaEvent_t meta_done = nullptr;
+  // verify result staging
+  int32_t* d_result = nullptr;
+  int32_t* h_result = nullptr;
+  void** d_planes = nullptr;  // [2*layers] K/V plane bases for kv_compact
+  void* logits = nullptr;     // [vocab] verify scratch (f64 toy / f32 llama)
+};
+
+namespace tp {
+
+// Device view of one forward call's per-node metadata.
+struct LevelDev {
+  int n;
+  int append;
+  int row0;  // first appended row (== rows before the call)
+  int words;
+  int bits_base;
+  int layer_lo, layer_hi;  // layers to run
+  const int32_t* tokens;
+  const int32_t* positions;
+  const int32_t* prefix_rows;
+  const uint64_t* anc;  // [n][words]
+};
+
+int fill_lcg_jump_table();
+int lcg_fill_f64(double* out, int64_t count, uint64_t seed, int64_t start, cudaStream_t st);
+int lcg_fill_bf16_t(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, uint64_t seed,
+                    int64_t start, double scale, cudaStream_t st);
+
+// toy arch (toy.cu)
+int toy_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out,
+                cudaStream_t st);
+int toy_embed(tp_model* m, int n, const int32_t* d_tokens, const int32_t* d_pos, double* out,
+              cudaStream_t st);
+int toy_logits(tp_model* m, tp_stage* ws, int n, const double* x, double* logits, cudaStream_t st);
+int toy_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);
+
+// llama arch (llama.cu)
+int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out,
+                  cudaStream_t st);
+int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st);
+int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st);
+int llama_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);
+int llama_init_weights(tp_model* m, uint64_t seed, cudaStream_t st);
+
+// shared (kv.cu)
+int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_children, int n_children,
+                 int32_t* d_result, cudaStream_t st);
+int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, void** d_planes,
+               cudaStream_t st);
+int rows_compact(const void* src, void* dst, int64_t row_bytes, const int32_t* d_idx, int n_out,
+                 cudaStream_t st);
+
+}  // namespace tp

@@ -1,0 +1,147 @@
+// K3 (pruning propagation) and K4's argmax/child-match tail.
+//
+// kv_compact: stable in-place compaction of a stage's speculative KV rows
+// (reference KvCache.promote/prune/_restrict, model.py:169-194).  Kept rows
+// only ever move toward lower indices, so one CTA per (layer, K|V, kv-head)
+// walks the kept list in chunks: stage CH rows in shared memory, barrier,
+// store, barrier — a later chunk can never overwrite a row an earlier
+// chunk still has to read.  Rows already in place (the leading kept run)
+// are skipped, so a steady-state hit moves only the rows behind the first
+// pruned sibling.
+//
+// argmax_match: deterministic first-argmax over the vocabulary (np.argmax
+// semantics, lowest id wins ties, NaN ranks highest) followed by the
+// first-level-1-child match of pipeline.py:333-339.
+#include "internal.h"
+
+namespace tp {
+
+constexpr int kMoveThreads = 256;
+constexpr int kMoveChunkBytes = 32 * 1024;
+
+__global__ void __launch_bounds__(kMoveThreads) kv_move_kernel(void* const* __restrict__ planes,
+                                                               int64_t plane_stride_bytes, int row_bytes,
+                                                               const int32_t* __restrict__ src_rows,
+                                                               int n_keep, int first) {
+  __shared__ __align__(16) uint4 stage[kMoveChunkBytes / 16];
+  char* base = (char*)planes[blockIdx.x] + (int64_t)blockIdx.y * plane_stride_bytes;
+  // leading run already in place
+  int j0 = 0;
+  while (j0 < n_keep && src_rows[j0] == first + j0) ++j0;
+  const int vec_per_row = row_bytes / 16;
+  const int rows_per_chunk = max(1, kMoveChunkBytes / row_bytes);
+  for (int c = j0; c < n_keep; c += rows_per_chunk) {
+    int cnt = min(rows_per_chunk, n_keep - c);
+    int total = cnt * vec_per_row;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      int r = t / vec_per_row, e = t % vec_per_row;
+      stage[t] = reinterpret_cast<const uint4*>(base + (int64_t)src_rows[c + r] * row_bytes)[e];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      int r = t / vec_per_row, e = t % vec_per_row;
+      reinterpret_cast<uint4*>(base + (int64_t)(first + c + r) * row_bytes)[e] = stage[t];
+    }
+    __syncthreads();
+  }
+}
+
+int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, void** d_planes,
+               cudaStream_t st) {
+  int nl = s->hi - s->lo;
+  int row_bytes = s->head_dim * s->esize;
+  TP_CHECK(row_bytes % 16 == 0, TP_ESHAPE, "KV row bytes must be a multiple of 16");
+  TP_CHECK(row_bytes <= kMoveChunkBytes, TP_ESHAPE, "KV row too large for the compaction kernel");
+  if (n_keep == 0 || nl == 0) return TP_OK;
+  int64_t plane = (int64_t)s->cap * row_bytes;  // one kv-head plane
+  dim3 grid(2 * nl, s->kv_heads);
+  kv_move_kernel<<<grid, kMoveThreads, 0, st>>>(d_planes, plane, row_bytes, d_src_rows, n_keep, first);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+__global__ void rows_gather_kernel(const char* __restrict__ src, char* __restrict__ dst, int row_bytes,
+                                   const int32_t* __restrict__ idx) {
+  const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)idx[blockIdx.x] * row_bytes);
+  uint4* d = reinterpret_cast<uint4*>(dst + (int64_t)blockIdx.x * row_bytes);
+  for (int e = threadIdx.x; e < row_bytes / 16; e += blockDim.x) d[e] = s[e];
+}
+
+int rows_compact(const void* src, void* dst, int64_t row_bytes, const int32_t* d_idx, int n_out,
+                 cudaStream_t st) {
+  TP_CHECK(row_bytes % 16 == 0, TP_ESHAPE, "row bytes must be a multiple of 16");
+  if (n_out == 0) return TP_OK;
+  rows_gather_kernel<<<n_out, 256, 0, st>>>((const char*)src, (char*)dst, (int)row_bytes, d_idx);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+template <typename T>
+__device__ __forceinline__ bool better(T a, int ia, T b, int ib) {
+  bool na = a != a, nb = b != b;  // NaN ranks highest, first NaN wins
+  if (na || nb) return na && (!nb || ia < ib);
+  return a > b || (a == b && ia < ib);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) argmax_match_kernel(const T* __restrict__ logits, int V,
+                                                            const int32_t* __restrict__ children,
+                                                            int n_children, int32_t* __restrict__ result) {
+  __shared__ T sv[32];
+  __shared__ int si[32];
+  T best = logits[0];
+  int bi = 0;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    T x = logits[v];
+    if (better(x, v, best, bi)) {
+      best = x;
+      bi = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, best, bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T b = sv[0];
+    int ib = si[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (better(sv[k], si[k], b, ib)) {
+        b = sv[k];
+        ib = si[k];
+      }
+    int child = -1;
+    for (int c = 0; c < n_children; ++c)
+      if (children[c] == ib) {
+        child = c;
+        break;
+      }
+    result[0] = ib;
+    result[1] = child;
+  }
+}
+
+int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_children, int n_children,
+                 int32_t* d_result, cudaStream_t st) {
+  if (is_f64)
+    argmax_match_kernel<double><<<1, 1024, 0, st>>>((const double*)logits, vocab, d_children, n_children,
+                                                    d_result);
+  else
+    argmax_match_kernel<float><<<1, 1024, 0, st>>>((const float*)logits, vocab, d_children, n_children,
+                                                   d_result);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+}  // namespace tp

@@ -1,0 +1,278 @@
+// Toy-arch (reference ToyModel) stage compute in float64 on B200 FP64 pipes.
+//
+// Restates `/root/reference/pkg/src/treepipe/model.py:239-305` for a whole
+// tree level per launch instead of one position per Python call:
+//   embed      E[tok] + interleaved sinusoid(pos)            (model.py:89-102,239-240)
+//   block      LN -> Wq/Wk/Wv -> tree-masked attention -> Wo + x
+//              -> LN -> ReLU(W1) W2 + x                        (model.py:250-280)
+//   head       E @ LN(x) (tied)                               (model.py:242-244)
+// The toy model is float64 by definition, so it runs in float64 here too:
+// per-stage outputs agree with the reference to ~1e-15 and greedy tokens are
+// identical wherever the reference's top-1 margin is above ~1e-12.
+//
+// Batch invariance (a node's bits never depend on its launch-mates): GEMM
+// outputs are sequential k-order FMA chains per (node, column); attention
+// walks the node's *logical* key sequence (prefix rows, then ancestor rows,
+// then self) with reductions whose shape depends only on that sequence.
+#include <cmath>
+
+#include "internal.h"
+
+namespace tp {
+
+__global__ void toy_embed_kernel(const double* __restrict__ E, const int32_t* __restrict__ tokens,
+                                 const int32_t* __restrict__ pos, int d, double* __restrict__ out) {
+  int r = blockIdx.x;
+  int half = d / 2;
+  const double* e = E + (int64_t)tokens[r] * d;
+  double p = (double)pos[r];
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    // numpy: exp(-log(10000.0) * arange(half) / half); angles = pos * freqs
+    double f = exp((-log(10000.0) * (double)i) / (double)half);
+    double a = p * f;
+    out[(int64_t)r * d + 2 * i] = e[2 * i] + sin(a);
+    out[(int64_t)r * d + 2 * i + 1] = e[2 * i + 1] + cos(a);
+  }
+}
+
+template <int B>
+__device__ double block_sum_f64(double v, double* red) {
+  v = warp_sum_f64(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = (l < B / 32) ? red[l] : 0.0;
+    t = warp_sum_f64(t);
+    if (l == 0) red[0] = t;
+  }
+  __syncthreads();
+  t = red[0];
+  __syncthreads();
+  return t;
+}
+
+// Parameter-free layer norm, population variance, eps inside the sqrt (model.py:83-86).
+__global__ void toy_norm_kernel(const double* __restrict__ x, int d, double* __restrict__ y) {
+  __shared__ double red[32];
+  const double* xr = x + (int64_t)blockIdx.x * d;
+  double s = 0.0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) s += xr[c];
+  double mu = block_sum_f64<256>(s, red) / (double)d;
+  double q = 0.0;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double t = xr[c] - mu;
+    q += t * t;
+  }
+  double var = block_sum_f64<256>(q, red) / (double)d;
+  double den = sqrt(var + 1e-6);
+  for (int c = threadIdx.x; c < d; c += blockDim.x) y[(int64_t)blockIdx.x * d + c] = (xr[c] - mu) / den;
+}
+
+// out[r, :] = res[r, :] + act(in[r, :] @ W)  with W [K, N] row-major (x @ W convention).
+constexpr int kGemmRows = 16, kGemmCols = 128, kGemmK = 32;
+__global__ void __launch_bounds__(kGemmCols) toy_gemm_kernel(const double* __restrict__ in, int n, int K,
+                                                             const double* __restrict__ W, int N,
+                                                             double* out, int64_t out_stride,
+                                                             const double* res, int relu) {
+  __shared__ double s_in[kGemmRows][kGemmK + 1];
+  int col = blockIdx.x * kGemmCols + threadIdx.x;
+  int r0 = blockIdx.y * kGemmRows;
+  double acc[kGemmRows];
+#pragma unroll
+  for (int r = 0; r < kGemmRows; ++r) acc[r] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += kGemmK) {
+    for (int idx = threadIdx.x; idx < kGemmRows * kGemmK; idx += kGemmCols) {
+      int r = idx / kGemmK, kk = idx % kGemmK;
+      s_in[r][kk] = (r0 + r < n && k0 + kk < K) ? in[(int64_t)(r0 + r) * K + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+    if (col < N) {
+      int kend = min(kGemmK, K - k0);
+      for (int kk = 0; kk < kend; ++kk) {
+        double w = W[(int64_t)(k0 + kk) * N + col];
+#pragma unroll
+        for (int r = 0; r < kGemmRows; ++r) acc[r] = fma(s_in[r][kk], w, acc[r]);
+      }
+    }
+    __syncthreads();
+  }
+  if (col >= N) return;
+#pragma unroll
+  for (int r = 0; r < kGemmRows; ++r) {
+    if (r0 + r >= n) break;
+    double v = acc[r];
+    if (relu) v = fmax(v, 0.0);
+    int64_t o = (int64_t)(r0 + r) * out_stride + col;
+    if (res) v = res[(int64_t)(r0 + r) * N + col] + v;
+    out[o] = v;
+  }
+}
+
+// Tree-masked single-head attention, one CTA per node (model.py:265-276).
+constexpr int kAttnThreads = 256;
+__global__ void __launch_bounds__(kAttnThreads) toy_attn_kernel(
+    const double* __restrict__ q, const double* __restrict__ kself, const double* __restrict__ vself,
+    const double* __restrict__ Kc, const double* __restrict__ Vc, LevelDev lv, int d, double sqrt_d,
+    double* __restrict__ out) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ int n_extra;
+  int i = blockIdx.x;
+  double* s_q = sm;                          // d
+  double* s_score = sm + d;                  // T
+  int P = lv.prefix_rows[i];
+  int max_extra = lv.words * 64;
+  int* s_rows = reinterpret_cast<int*>(s_score + P + max_extra + 1);  // extras
+  for (int c = threadIdx.x; c < d; c += blockDim.x) s_q[c] = q[(int64_t)i * d + c];
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    for (int w = 0; w < lv.words; ++w) {
+      uint64_t bits = lv.anc[(int64_t)i * lv.words + w];
+      while (bits) {
+        int b = __ffsll((long long)bits) - 1;
+        s_rows[cnt++] = lv.bits_base + w * 64 + b;
+        bits &= bits - 1;
+      }
+    }
+    n_extra = cnt;
+  }
+  __syncthreads();
+  const int A = n_extra;
+  const int T = P + A + 1;
+  const double* ks = kself + (int64_t)i * d;
+  const double* vs = vself + (int64_t)i * d;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < T; j += nw) {
+    const double* kr = j < P ? Kc + (int64_t)j * d : (j < P + A ? Kc + (int64_t)s_rows[j - P] * d : ks);
+    double acc = 0.0;
+    for (int c = lane; c < d; c += 32) acc = fma(kr[c], s_q[c], acc);
+    acc = warp_sum_f64(acc);
+    if (lane == 0) s_score[j] = acc / sqrt_d;
+  }
+  __syncthreads();
+  double mx = -INFINITY;
+  for (int j = threadIdx.x; j < T; j += blockDim.x) mx = fmax(mx, s_score[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int w = 1; w < nw; ++w) m = fmax(m, red[w]);
+    red[31] = m;
+  }
+  __syncthreads();
+  mx = red[31];
+  __syncthreads();
+  double part = 0.0;
+  for (int j = threadIdx.x; j < T; j += blockDim.x) {
+    double e = exp(s_score[j] - mx);
+    s_score[j] = e;
+    part += e;
+  }
+  double tot = block_sum_f64<kAttnThreads>(part, red);
+  for (int j = threadIdx.x; j < T; j += blockDim.x) s_score[j] = s_score[j] / tot;
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < T; ++j) {
+      const double* vr = j < P ? Vc + (int64_t)j * d : (j < P + A ? Vc + (int64_t)s_rows[j - P] * d : vs);
+      acc = fma(s_score[j], vr[c], acc);
+    }
+    out[(int64_t)i * d + c] = acc;
+  }
+}
+
+// logits[r, v] = E[v, :] . h[r, :]
+__global__ void toy_head_kernel(const double* __restrict__ E, const double* __restrict__ h, int V, int d,
+                                double* __restrict__ logits) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  int r = blockIdx.y;
+  if (warp >= V) return;
+  const double* e = E + (int64_t)warp * d;
+  const double* x = h + (int64_t)r * d;
+  double acc = 0.0;
+  for (int c = lane; c < d; c += 32) acc = fma(e[c], x[c], acc);
+  acc = warp_sum_f64(acc);
+  if (lane == 0) logits[(int64_t)r * V + warp] = acc;
+}
+
+static int gemm(const double* in, int n, int K, const double* W, int N, double* out, int64_t out_stride,
+                const double* res, int relu, cudaStream_t st) {
+  dim3 grid(ceil_div(N, kGemmCols), ceil_div(n, kGemmRows));
+  toy_gemm_kernel<<<grid, kGemmCols, 0, st>>>(in, n, K, W, N, out, out_stride, res, relu);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+int toy_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes) {
+  int64_t d = m->cfg.hidden;
+  *bytes = (size_t)max_nodes * d * 8 * 7;  // h q k v attn + f(2d)
+  return TP_OK;
+}
+
+int toy_embed(tp_model* m, int n, const int32_t* d_tokens, const int32_t* d_pos, double* out, cudaStream_t st) {
+  TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
+  toy_embed_kernel<<<n, 128, 0, st>>>((const double*)m->embed, d_tokens, d_pos, m->cfg.hidden, out);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+int toy_logits(tp_model* m, tp_stage* ws, int n, const double* x, double* logits, cudaStream_t st) {
+  TP_CHECK(m->embed, TP_ECONFIG, "tied head needs the embedding table on this model");
+  int d = m->cfg.hidden, V = m->cfg.vocab;
+  double* h = (double*)ws->ws;
+  toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
+  dim3 grid(ceil_div(V * 32, 256), n);
+  toy_head_kernel<<<grid, 256, 0, st>>>((const double*)m->embed, h, V, d, logits);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+int toy_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
+  tp_model* m = s->m;
+  const int d = m->cfg.hidden, f = 2 * d, n = lv.n;
+  const int64_t N = m->cfg.max_nodes;
+  double* x = (double*)hidden_out;
+  double* h = (double*)s->ws;
+  double* q = h + N * d;
+  double* kt = q + N * d;
+  double* vt = kt + N * d;
+  double* at = vt + N * d;
+  double* ff = at + N * d;
+  if (hidden_in) {
+    if (hidden_in != hidden_out)
+      TP_CUDA(cudaMemcpyAsync(x, hidden_in, (size_t)n * d * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TP_TRY(toy_embed(m, n, lv.tokens, lv.positions, x, st));
+  }
+  const double sqrt_d = std::sqrt((double)d);
+  size_t smem = (size_t)(d + s->cap + lv.words * 64 + 1) * 8 + (size_t)lv.words * 64 * 4 + 16;
+  static size_t smem_set = 48 * 1024;
+  if (smem > smem_set) {
+    TP_CUDA(cudaFuncSetAttribute(toy_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  for (int layer = lv.layer_lo; layer < lv.layer_hi; ++layer) {
+    const tp_layer_weights& w = m->layers[layer - m->cfg.layer_lo];
+    double* Kc = (double*)s->k[layer - s->lo];
+    double* Vc = (double*)s->v[layer - s->lo];
+    double* kdst = lv.append ? Kc + (int64_t)lv.row0 * d : kt;
+    double* vdst = lv.append ? Vc + (int64_t)lv.row0 * d : vt;
+    toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
+    TP_TRY(gemm(h, n, d, (const double*)w.w[1], d, q, d, nullptr, 0, st));
+    TP_TRY(gemm(h, n, d, (const double*)w.w[2], d, kdst, d, nullptr, 0, st));
+    TP_TRY(gemm(h, n, d, (const double*)w.w[3], d, vdst, d, nullptr, 0, st));
+    toy_attn_kernel<<<n, kAttnThreads, smem, st>>>(q, kdst, vdst, Kc, Vc, lv, d, sqrt_d, at);
+    TP_CUDA(cudaGetLastError());
+    TP_TRY(gemm(at, n, d, (const double*)w.w[4], d, x, d, x, 0, st));
+    toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
+    TP_TRY(gemm(h, n, d, (const double*)w.w[5], f, ff, f, nullptr, 1, st));
+    TP_TRY(gemm(ff, n, f, (const double*)w.w[6], d, x, d, x, 0, st));
+  }
+  return TP_OK;
+}
+
+}  // namespace tp

@@ -126,6 +126,11 @@ int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t ro
 /* Grow the KV capacity (reference KvCache grow-by-doubling, model.py:141-148). */
 int tp_stage_reserve(tp_stage* s, int32_t capacity_rows);
 
+/* ---- test hook (no reference counterpart): the K2 weight-streaming GEMM alone.
+ * out[n][n_out] (f32, dev) = x[n][k] (bf16, dev) . w[n_out][k]^T (bf16, dev).   */
+int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out, int32_t k,
+                  void* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -180,7 +180,7 @@ int tp_model_destroy(tp_model* m) {
   for (auto& w : m->layers)
     for (void* p : w.w)
       if (p) cudaFree(p);
-  if (m->tma_cache) free(m->tma_cache);
+  if (!is_toy(m)) llama_model_free(m);
   delete m;
   return TP_OK;
 }
@@ -292,6 +292,13 @@ int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t cap
   TP_CUDA(cudaMalloc((void**)&s->d_result, 16));
   TP_CUDA(cudaMallocHost((void**)&s->h_result, 16));
   TP_CUDA(cudaMalloc(&s->logits, (size_t)m->cfg.vocab * 8));
+  if (!is_toy(m)) {
+    rc = llama_stage_init(s);
+    if (rc != TP_OK) {
+      tp_stage_destroy(s);
+      return rc;
+    }
+  }
   *out = s;
   return TP_OK;
 }
@@ -309,6 +316,7 @@ int tp_stage_destroy(tp_stage* s) {
   if (s->h_result) cudaFreeHost(s->h_result);
   if (s->d_planes) cudaFree(s->d_planes);
   if (s->logits) cudaFree(s->logits);
+  if (!is_toy(s->m)) llama_stage_free(s);
   delete s;
   return TP_OK;
 }
@@ -322,7 +330,8 @@ int tp_stage_reserve(tp_stage* s, int32_t capacity_rows) {
   if (capacity_rows <= s->cap) return TP_OK;
   TP_CUDA(cudaSetDevice(s->m->cfg.device));
   TP_CUDA(cudaDeviceSynchronize());
-  return alloc_kv(s, capacity_rows);
+  TP_TRY(alloc_kv(s, capacity_rows));
+  return is_toy(s->m) ? TP_OK : llama_stage_init(s);
 }
 
 int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, void* stream) {
@@ -337,7 +346,12 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
   TP_CHECK(L->words >= 0 && L->words <= s->max_words, TP_ESHAPE, "too many mask words for this stage");
   TP_CHECK(!L->append || s->rows + n <= s->cap, TP_ESHAPE, "KV capacity exceeded (reserve first)");
   const int visible = s->rows + (L->append ? n : 0);
+  int max_t = 0;
   for (int i = 0; i < n; ++i) {
+    int pc = 0;
+    for (int w = 0; w < L->words; ++w) pc += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
+    TP_CHECK(is_toy(m) || pc <= 64, TP_ESHAPE, "more than 64 speculative ancestors per node");
+    max_t = std::max(max_t, L->prefix_rows[i] + pc + 1);
     TP_CHECK(L->prefix_rows[i] >= 0 && L->prefix_rows[i] <= visible, TP_ECONTRACT, "prefix rows beyond cache");
     if (L->tokens && !hidden_in)
       TP_CHECK(L->tokens[i] >= 0 && L->tokens[i] < m->cfg.vocab, TP_ESHAPE, "token outside vocabulary");
@@ -369,6 +383,7 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
   lv.row0 = s->rows;
   lv.words = L->words;
   lv.bits_base = L->bits_base;
+  lv.max_t = max_t;
   const bool all_layers = L->layer_lo == 0 && L->layer_hi == 0;
   const bool no_layers = L->layer_lo < 0;  // explicit empty range: embed/copy only
   lv.layer_lo = all_layers ? s->lo : (no_layers ? s->lo : L->layer_lo);

@@ -44,6 +44,7 @@ struct tp_stage {
   int32_t* h_result = nullptr;
   void** d_planes = nullptr;  // [2*layers] K/V plane bases for kv_compact
   void* logits = nullptr;     // [vocab] verify scratch (f64 toy / f32 llama)
+  void* ext = nullptr;        // arch-specific state (llama: tensor maps, attention partials)
 };
 
 namespace tp {
@@ -56,6 +57,7 @@ struct LevelDev {
   int words;
   int bits_base;
   int layer_lo, layer_hi;  // layers to run
+  int max_t;               // longest logical key sequence (prefix + ancestors + self)
   const int32_t* tokens;
   const int32_t* positions;
   const int32_t* prefix_rows;
@@ -64,8 +66,6 @@ struct LevelDev {
 
 int fill_lcg_jump_table();
 int lcg_fill_f64(double* out, int64_t count, uint64_t seed, int64_t start, cudaStream_t st);
-int lcg_fill_bf16_t(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, uint64_t seed,
-                    int64_t start, double scale, cudaStream_t st);
 
 // toy arch (toy.cu)
 int toy_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out,
@@ -82,6 +82,15 @@ int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStr
 int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st);
 int llama_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);
 int llama_init_weights(tp_model* m, uint64_t seed, cudaStream_t st);
+int llama_stage_init(tp_stage* s);     // workspace tensor maps + attention scratch (after alloc_kv)
+void llama_stage_free(tp_stage* s);
+void llama_model_free(tp_model* m);
+int lcg_fill_bf16(__nv_bfloat16* out, int64_t count, uint64_t seed, int64_t start, double scale,
+                  cudaStream_t st);
+// [rows_in, cols_out] stream block stored transposed into dst rows; gate/up interleave
+// maps output column j to row (j/64)*128 + j%64 + row_offset.
+int lcg_fill_bf16_rows(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, uint64_t seed, int64_t start,
+                       double scale, int64_t row_offset, int interleave64, cudaStream_t st);
 
 // shared (kv.cu)
 int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_children, int n_children,

@@ -59,9 +59,15 @@ __global__ void lcg_f64_kernel(double* __restrict__ out, int64_t count, uint64_t
   }
 }
 
-// [rows_in, cols_out] in stream order, stored transposed as [cols_out][rows_in] bf16.
+__device__ __forceinline__ __nv_bfloat16 to_bf16(uint64_t s, double scale) {
+  return __float2bfloat16_rn(__double2float_rn(__dmul_rn(lcg_sample(s), scale)));
+}
+
+// [rows_in, cols_out] in stream order, stored transposed: column j -> dst row
+// map(j) (= j + row_offset, or the 64-row gate/up interleave), element i.
 __global__ void lcg_bf16_t_kernel(__nv_bfloat16* __restrict__ out, int64_t rows_in, int64_t cols_out,
-                                  uint64_t seed, int64_t start, double scale) {
+                                  uint64_t seed, int64_t start, double scale, int64_t row_offset,
+                                  int interleave64) {
   int64_t count = rows_in * cols_out;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t e0 = t * kRun;
@@ -70,13 +76,26 @@ __global__ void lcg_bf16_t_kernel(__nv_bfloat16* __restrict__ out, int64_t rows_
   uint64_t s = lcg_state(seed, (uint64_t)(start + e0 + 1));
   int64_t i = e0 / cols_out, j = e0 % cols_out;
   for (int64_t e = e0; e < e1; ++e) {
-    double w = __dmul_rn(lcg_sample(s), scale);
-    out[j * rows_in + i] = __float2bfloat16_rn(__double2float_rn(w));
+    int64_t row = interleave64 ? (j / 64) * 128 + (j % 64) + row_offset : j + row_offset;
+    out[row * rows_in + i] = to_bf16(s, scale);
     s = s * kLcgMul + kLcgInc;
     if (++j == cols_out) {
       j = 0;
       ++i;
     }
+  }
+}
+
+__global__ void lcg_bf16_kernel(__nv_bfloat16* __restrict__ out, int64_t count, uint64_t seed, int64_t start,
+                                double scale) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t e0 = t * kRun;
+  if (e0 >= count) return;
+  int64_t e1 = min(count, e0 + kRun);
+  uint64_t s = lcg_state(seed, (uint64_t)(start + e0 + 1));
+  for (int64_t e = e0; e < e1; ++e) {
+    out[e] = to_bf16(s, scale);
+    s = s * kLcgMul + kLcgInc;
   }
 }
 
@@ -89,13 +108,23 @@ int lcg_fill_f64(double* out, int64_t count, uint64_t seed, int64_t start, cudaS
   return TP_OK;
 }
 
-int lcg_fill_bf16_t(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, uint64_t seed, int64_t start,
-                    double scale, cudaStream_t st) {
+int lcg_fill_bf16_rows(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, uint64_t seed, int64_t start,
+                       double scale, int64_t row_offset, int interleave64, cudaStream_t st) {
   TP_TRY(fill_lcg_jump_table());
   int64_t threads = ceil_div64(rows_in * cols_out, kRun);
   int block = 256;
   lcg_bf16_t_kernel<<<(unsigned)ceil_div64(threads, block), block, 0, st>>>(out, rows_in, cols_out, seed,
-                                                                           start, scale);
+                                                                           start, scale, row_offset,
+                                                                           interleave64);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+int lcg_fill_bf16(__nv_bfloat16* out, int64_t count, uint64_t seed, int64_t start, double scale,
+                  cudaStream_t st) {
+  TP_TRY(fill_lcg_jump_table());
+  int64_t threads = ceil_div64(count, kRun);
+  lcg_bf16_kernel<<<(unsigned)ceil_div64(threads, 256), 256, 0, st>>>(out, count, seed, start, scale);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }

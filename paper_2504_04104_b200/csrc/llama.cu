@@ -1,13 +1,353 @@
-// Llama-arch stage compute (placeholder until the tcgen05 path lands).
+// Llama-shape stage compute: bf16 weights in HBM, fp32 residual stream.
+//
+// Per layer (reference layer_step structure, `/root/reference/pkg/src/treepipe/
+// model.py:250-280`, with the Llama block: RMSNorm, RoPE, GQA, SwiGLU):
+//
+//   [rmsnorm x -> Xd]                           (fused into the previous epilogue)
+//   QKV  = Xd . Wqkv^T      K2 tcgen05 stream-K   -> qkv_epilogue: RoPE(q,k), q->Xq,
+//                                                    k,v -> KV rows (appended in place)
+//   attn = tree-attention(Xq, KV, ancestor bits)  K1 (attn.cu)          -> Xo
+//   x   += Xo . Wo^T        K2                    -> resid_norm: x += ., Xd = rmsnorm(x)
+//   GU   = Xd . Wgu^T       K2 (gate/up 64-row interleave)  -> swiglu: Xf = silu(g)*u
+//   x   += Xf . Wdown^T     K2                    -> resid_norm
+//
+// Numerics (mirrored by oracle/llama.py): GEMM inputs bf16, accumulation and
+// residual fp32; RoPE (HF rotate-half, angle in fp64) on the fp32 GEMM
+// output, then rounded to bf16 for the cache / attention; softmax fp32.
+#include <cmath>
+#include <cstring>
+
+#include "attn.h"
+#include "gemm_tc.h"
 #include "internal.h"
 
 namespace tp {
-int llama_forward(tp_stage*, const LevelDev&, const void*, void*, cudaStream_t) {
-  set_error("llama path not implemented yet");
-  return TP_ECONFIG;
+
+struct LlamaModelExt {
+  std::vector<CUtensorMap> qkv, o, gu, down;
+  CUtensorMap head;
+};
+
+struct LlamaStageExt {
+  int np = 0;  // padded node rows (multiple of 16)
+  __nv_bfloat16 *Xd = nullptr, *Xo = nullptr, *Xf = nullptr, *Xq = nullptr;
+  __nv_bfloat16 *kself = nullptr, *vself = nullptr;
+  float* part = nullptr;
+  size_t part_floats = 0;
+  CUtensorMap mXd, mXo, mXf;
+  float *pm = nullptr, *pl = nullptr, *po = nullptr;
+  int max_splits = 0;
+};
+
+static LlamaModelExt* mext(tp_model* m) { return reinterpret_cast<LlamaModelExt*>(m->tma_cache); }
+static LlamaStageExt* sext(tp_stage* s) { return reinterpret_cast<LlamaStageExt*>(s->ext); }
+
+// ---- kernels --------------------------------------------------------------------
+
+__global__ void llama_embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tok, int d,
+                                   float* __restrict__ x) {
+  const int c = blockIdx.x;
+  const __nv_bfloat16* e = E + (size_t)tok[c] * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) x[(size_t)c * d + j] = __bfloat162float(e[j]);
 }
-int llama_embed(tp_model*, int, const int32_t*, float*, cudaStream_t) { set_error("llama: n/a"); return TP_ECONFIG; }
-int llama_logits(tp_model*, tp_stage*, int, const float*, float*, cudaStream_t) { set_error("llama: n/a"); return TP_ECONFIG; }
-int llama_workspace_bytes(const tp_model*, int, size_t* b) { *b = 256; return TP_OK; }
-int llama_init_weights(tp_model*, uint64_t, cudaStream_t) { set_error("llama: n/a"); return TP_ECONFIG; }
+
+__device__ __forceinline__ float block_sum_256(float v, float* red) {
+  v = warp_sum_f32(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float t = l < 8 ? red[l] : 0.f;
+    t = warp_sum_f32(t);
+    if (l == 0) red[8] = t;
+  }
+  __syncthreads();
+  const float t = red[8];
+  __syncthreads();
+  return t;
+}
+
+// x[c] (+= GEMM result) ; Xd[c] = bf16(x * 1/sqrt(mean(x^2) + eps))
+__global__ void __launch_bounds__(256) resid_norm_kernel(const float* __restrict__ part, SkPlan p, int add,
+                                                         float* __restrict__ x, int d, float eps,
+                                                         __nv_bfloat16* __restrict__ xd, int do_norm) {
+  __shared__ float red[9];
+  const int c = blockIdx.x;
+  float* xr = x + (size_t)c * d;
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float v = xr[j];
+    if (add) v += sk_sum(part, p, c, j);
+    xr[j] = v;
+    ss += v * v;
+  }
+  if (!do_norm) return;
+  ss = block_sum_256(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) xd[(size_t)c * d + j] = __float2bfloat16_rn(xr[j] * r);
+}
+
+// RoPE on q/k heads (rotate-half pairs (i, i+64)), scatter q -> Xq, k/v -> cache rows.
+__global__ void qkv_epilogue_kernel(const float* __restrict__ part, SkPlan p, LevelDev lv, int H, int KV,
+                                    double theta, __nv_bfloat16* __restrict__ xq, __nv_bfloat16* __restrict__ kc,
+                                    __nv_bfloat16* __restrict__ vc, int cap, __nv_bfloat16* __restrict__ kself,
+                                    __nv_bfloat16* __restrict__ vself) {
+  const int c = blockIdx.x, hh = blockIdx.y, i = threadIdx.x;  // i in [0, 64)
+  const int j0 = hh * 128;
+  const float y1 = sk_sum(part, p, c, j0 + i), y2 = sk_sum(part, p, c, j0 + i + 64);
+  float o1 = y1, o2 = y2;
+  if (hh < H + KV) {
+    const double inv = pow(theta, -2.0 * (double)i / 128.0);
+    double sn, cs;
+    sincos((double)lv.positions[c] * inv, &sn, &cs);
+    const float cf = (float)cs, sf = (float)sn;
+    o1 = __fsub_rn(__fmul_rn(y1, cf), __fmul_rn(y2, sf));
+    o2 = __fadd_rn(__fmul_rn(y2, cf), __fmul_rn(y1, sf));
+  }
+  __nv_bfloat16* dst;
+  if (hh < H) {
+    dst = xq + (size_t)c * H * 128 + hh * 128;
+  } else {
+    const bool is_k = hh < H + KV;
+    const int kh = is_k ? hh - H : hh - H - KV;
+    if (lv.append)
+      dst = (is_k ? kc : vc) + ((size_t)kh * cap + lv.row0 + c) * 128;
+    else
+      dst = (is_k ? kself : vself) + ((size_t)c * KV + kh) * 128;
+  }
+  dst[i] = __float2bfloat16_rn(o1);
+  dst[i + 64] = __float2bfloat16_rn(o2);
+}
+
+__global__ void swiglu_kernel(const float* __restrict__ part, SkPlan p, int f, __nv_bfloat16* __restrict__ xf) {
+  const int c = blockIdx.x, fi = blockIdx.y * blockDim.x + threadIdx.x;
+  if (fi >= f) return;
+  const int rg = (fi >> 6) * 128 + (fi & 63);
+  const float g = sk_sum(part, p, c, rg), u = sk_sum(part, p, c, rg + 64);
+  const float a = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+  xf[(size_t)c * f + fi] = __float2bfloat16_rn(a);
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
+                                                      __nv_bfloat16* __restrict__ xd) {
+  __shared__ float red[9];
+  const float* xr = x + (size_t)blockIdx.x * d;
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) ss += xr[j] * xr[j];
+  ss = block_sum_256(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) xd[(size_t)blockIdx.x * d + j] = __float2bfloat16_rn(xr[j] * r);
+}
+
+__global__ void logits_kernel(const float* __restrict__ part, SkPlan p, int V, float* __restrict__ out) {
+  const int c = blockIdx.x, v = blockIdx.y * blockDim.x + threadIdx.x;
+  if (v < V) out[(size_t)c * V + v] = sk_sum(part, p, c, v);
+}
+
+// ---- host ---------------------------------------------------------------------------
+
+static int build_model_ext(tp_model* m) {
+  if (m->tma_cache) return TP_OK;
+  const tp_model_config& c = m->cfg;
+  const int64_t d = c.hidden, q = (int64_t)c.heads * 128, kv = (int64_t)c.kv_heads * 128, f = c.ffn;
+  auto* e = new LlamaModelExt();
+  for (int l = c.layer_lo; l < c.layer_hi; ++l) {
+    const tp_layer_weights& w = m->layers[l - c.layer_lo];
+    CUtensorMap a, b, g, dn;
+    TP_TRY(make_tmap_kmajor(&a, w.w[1], q + 2 * kv, d, 128));
+    TP_TRY(make_tmap_kmajor(&b, w.w[4], d, q, 128));
+    TP_TRY(make_tmap_kmajor(&g, w.w[5], 2 * f, d, 128));
+    TP_TRY(make_tmap_kmajor(&dn, w.w[7], d, f, 128));
+    e->qkv.push_back(a);
+    e->o.push_back(b);
+    e->gu.push_back(g);
+    e->down.push_back(dn);
+  }
+  if (m->head) TP_TRY(make_tmap_kmajor(&e->head, m->head, c.vocab, d, 128));
+  m->tma_cache = e;
+  return TP_OK;
+}
+
+void llama_model_free(tp_model* m) {
+  delete mext(m);
+  m->tma_cache = nullptr;
+}
+
+int llama_workspace_bytes(const tp_model*, int, size_t* bytes) {
+  *bytes = 256;  // llama state lives in LlamaStageExt
+  return TP_OK;
+}
+
+int llama_init_weights(tp_model* m, uint64_t seed, cudaStream_t st) {
+  const tp_model_config& c = m->cfg;
+  const int64_t V = c.vocab, d = c.hidden, q = (int64_t)c.heads * 128, kv = (int64_t)c.kv_heads * 128, f = c.ffn;
+  const int64_t per_layer = d * q + 2 * d * kv + q * d + 3 * d * f;
+  auto sc = [&](int64_t fan_in) { return c.weight_scale ? std::sqrt(3.0 / (double)fan_in) / 0.1 : 1.0; };
+  if (m->embed) TP_TRY(lcg_fill_bf16((__nv_bfloat16*)m->embed, V * d, seed, 0, 1.0, st));
+  for (int l = c.layer_lo; l < c.layer_hi; ++l) {
+    const tp_layer_weights& w = m->layers[l - c.layer_lo];
+    int64_t off = V * d + (int64_t)l * per_layer;
+    auto* qkv = (__nv_bfloat16*)w.w[1];
+    TP_TRY(lcg_fill_bf16_rows(qkv, d, q, seed, off, sc(d), 0, 0, st));  // Wq [d, q]
+    off += d * q;
+    TP_TRY(lcg_fill_bf16_rows(qkv, d, kv, seed, off, sc(d), q, 0, st));  // Wk
+    off += d * kv;
+    TP_TRY(lcg_fill_bf16_rows(qkv, d, kv, seed, off, sc(d), q + kv, 0, st));  // Wv
+    off += d * kv;
+    TP_TRY(lcg_fill_bf16_rows((__nv_bfloat16*)w.w[4], q, d, seed, off, sc(q), 0, 0, st));  // Wo [q, d]
+    off += q * d;
+    TP_TRY(lcg_fill_bf16_rows((__nv_bfloat16*)w.w[5], d, f, seed, off, sc(d), 0, 1, st));  // Wgate
+    off += d * f;
+    TP_TRY(lcg_fill_bf16_rows((__nv_bfloat16*)w.w[5], d, f, seed, off, sc(d), 64, 1, st));  // Wup
+    off += d * f;
+    TP_TRY(lcg_fill_bf16_rows((__nv_bfloat16*)w.w[7], f, d, seed, off, sc(f), 0, 0, st));  // Wdown [f, d]
+  }
+  if (m->head)
+    TP_TRY(lcg_fill_bf16_rows((__nv_bfloat16*)m->head, d, V, seed, V * d + (int64_t)c.layers * per_layer, sc(d),
+                              0, 0, st));
+  TP_CUDA(cudaStreamSynchronize(st));
+  return build_model_ext(m);
+}
+
+int llama_stage_init(tp_stage* s) {
+  tp_model* m = s->m;
+  const tp_model_config& c = m->cfg;
+  TP_TRY(build_model_ext(m));
+  LlamaStageExt* e = sext(s);
+  const bool fresh = e == nullptr;
+  if (fresh) {
+    e = new LlamaStageExt();
+    s->ext = e;
+    const int64_t d = c.hidden, q = (int64_t)c.heads * 128, kv = (int64_t)c.kv_heads * 128, f = c.ffn;
+    e->np = (c.max_nodes + 15) / 16 * 16;
+    const int64_t np = e->np;
+    TP_CUDA(cudaMalloc(&e->Xd, np * d * 2));
+    TP_CUDA(cudaMalloc(&e->Xo, np * q * 2));
+    TP_CUDA(cudaMalloc(&e->Xf, np * f * 2));
+    TP_CUDA(cudaMalloc(&e->Xq, np * q * 2));
+    TP_CUDA(cudaMalloc(&e->kself, np * kv * 2));
+    TP_CUDA(cudaMalloc(&e->vself, np * kv * 2));
+    TP_CUDA(cudaMemset(e->Xd, 0, np * d * 2));
+    TP_CUDA(cudaMemset(e->Xo, 0, np * q * 2));
+    TP_CUDA(cudaMemset(e->Xf, 0, np * f * 2));
+    size_t pf = 0;
+    const int nmax = c.max_nodes;
+    pf = std::max(pf, sk_part_floats(sk_plan((int)(q + 2 * kv), (int)d, nmax)));
+    pf = std::max(pf, sk_part_floats(sk_plan((int)d, (int)q, nmax)));
+    pf = std::max(pf, sk_part_floats(sk_plan((int)(2 * f), (int)d, nmax)));
+    pf = std::max(pf, sk_part_floats(sk_plan((int)d, (int)f, nmax)));
+    if (m->head) pf = std::max(pf, sk_part_floats(sk_plan(c.vocab, (int)d, nmax)));
+    e->part_floats = pf;
+    TP_CUDA(cudaMalloc(&e->part, pf * 4));
+    TP_TRY(make_tmap_kmajor(&e->mXd, e->Xd, np, d, 16));
+    TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
+    TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));
+  }
+  // attention split partials follow the KV capacity
+  const int splits = (s->cap + 1 + kAttnChunk * kAttnSplitChunks - 1) / (kAttnChunk * kAttnSplitChunks);
+  if (splits > e->max_splits) {
+    if (e->pm) cudaFree(e->pm);
+    if (e->pl) cudaFree(e->pl);
+    if (e->po) cudaFree(e->po);
+    const size_t cells = (size_t)e->np * c.heads * splits;
+    TP_CUDA(cudaMalloc(&e->pm, cells * 4));
+    TP_CUDA(cudaMalloc(&e->pl, cells * 4));
+    TP_CUDA(cudaMalloc(&e->po, cells * 128 * 4));
+    e->max_splits = splits;
+  }
+  return TP_OK;
+}
+
+void llama_stage_free(tp_stage* s) {
+  LlamaStageExt* e = sext(s);
+  if (!e) return;
+  for (void* p : {(void*)e->Xd, (void*)e->Xo, (void*)e->Xf, (void*)e->Xq, (void*)e->kself, (void*)e->vself,
+                  (void*)e->part, (void*)e->pm, (void*)e->pl, (void*)e->po})
+    if (p) cudaFree(p);
+  delete e;
+  s->ext = nullptr;
+}
+
+int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st) {
+  TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
+  llama_embed_kernel<<<n, 256, 0, st>>>((const __nv_bfloat16*)m->embed, d_tokens, m->cfg.hidden, out);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st) {
+  TP_CHECK(m->head, TP_ECONFIG, "model has no LM head");
+  TP_TRY(llama_stage_init(ws));
+  LlamaStageExt* e = sext(ws);
+  const int d = m->cfg.hidden, V = m->cfg.vocab;
+  rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
+  TP_CUDA(cudaGetLastError());
+  const SkPlan ph = sk_plan(V, d, n);
+  TP_TRY(sk_gemm(&mext(m)->head, &e->mXd, ph, e->part, st));
+  logits_kernel<<<dim3(n, (V + 255) / 256), 256, 0, st>>>(e->part, ph, V, logits);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
+  tp_model* m = s->m;
+  const tp_model_config& c = m->cfg;
+  TP_TRY(llama_stage_init(s));
+  LlamaStageExt* e = sext(s);
+  LlamaModelExt* me = mext(m);
+  const int n = lv.n, d = c.hidden, H = c.heads, KV = c.kv_heads, f = c.ffn;
+  const int q = H * 128, kvd = KV * 128;
+  float* x = (float*)hidden_out;
+  if (hidden_in) {
+    if (hidden_in != hidden_out)
+      TP_CUDA(cudaMemcpyAsync(x, hidden_in, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TP_TRY(llama_embed(m, n, lv.tokens, x, st));
+  }
+  if (lv.layer_lo == lv.layer_hi) return TP_OK;
+  rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, c.norm_eps, e->Xd);
+  TP_CUDA(cudaGetLastError());
+  const SkPlan pqkv = sk_plan(q + 2 * kvd, d, n), po = sk_plan(d, q, n), pgu = sk_plan(2 * f, d, n),
+               pdn = sk_plan(d, f, n);
+  const int span = kAttnChunk * kAttnSplitChunks;
+  const int splits = std::min(e->max_splits, (lv.max_t + span - 1) / span);
+  AttnArgs aa;
+  aa.q = e->Xq;
+  aa.q_stride = q;
+  aa.cap = s->cap;
+  aa.kself = lv.append ? nullptr : e->kself;
+  aa.vself = lv.append ? nullptr : e->vself;
+  aa.H = H;
+  aa.KV = KV;
+  aa.scale = (float)(1.0 / std::sqrt(128.0));
+  aa.pm = e->pm;
+  aa.pl = e->pl;
+  aa.po = e->po;
+  aa.max_splits = e->max_splits;
+  aa.out = e->Xo;
+  aa.out_stride = q;
+  for (int layer = lv.layer_lo; layer < lv.layer_hi; ++layer) {
+    const int li = layer - c.layer_lo;
+    __nv_bfloat16* kc = (__nv_bfloat16*)s->k[layer - s->lo];
+    __nv_bfloat16* vc = (__nv_bfloat16*)s->v[layer - s->lo];
+    TP_TRY(sk_gemm(&me->qkv[li], &e->mXd, pqkv, e->part, st));
+    qkv_epilogue_kernel<<<dim3(n, H + 2 * KV), 64, 0, st>>>(e->part, pqkv, lv, H, KV, (double)c.rope_theta, e->Xq,
+                                                            kc, vc, s->cap, e->kself, e->vself);
+    TP_CUDA(cudaGetLastError());
+    aa.k = kc;
+    aa.v = vc;
+    TP_TRY(attn_tree(aa, lv, splits, st));
+    TP_TRY(sk_gemm(&me->o[li], &e->mXo, po, e->part, st));
+    resid_norm_kernel<<<n, 256, 0, st>>>(e->part, po, 1, x, d, c.norm_eps, e->Xd, 1);
+    TP_CUDA(cudaGetLastError());
+    TP_TRY(sk_gemm(&me->gu[li], &e->mXd, pgu, e->part, st));
+    swiglu_kernel<<<dim3(n, (f + 255) / 256), 256, 0, st>>>(e->part, pgu, f, e->Xf);
+    TP_CUDA(cudaGetLastError());
+    TP_TRY(sk_gemm(&me->down[li], &e->mXf, pdn, e->part, st));
+    resid_norm_kernel<<<n, 256, 0, st>>>(e->part, pdn, 1, x, d, c.norm_eps, e->Xd, layer + 1 < lv.layer_hi);
+    TP_CUDA(cudaGetLastError());
+  }
+  return TP_OK;
+}
+
 }  // namespace tp

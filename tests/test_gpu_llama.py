@@ -1,0 +1,172 @@
+"""GPU checks of the Llama-shape bf16 path: the tcgen05 weight-streaming GEMM,
+LCG weights, tree forward vs the float32 oracle (stated tolerance), batch
+invariance, and SpecPipe losslessness w.r.t. the GPU greedy decode."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.llama import LlamaOracle, bf16
+from oracle.toy import forward_nodes, greedy_continuation
+
+pytestmark = pytest.mark.gpu
+
+tp = pytest.importorskip("paper_2504_04104_b200")
+from paper_2504_04104_b200 import _lib  # noqa: E402
+from paper_2504_04104_b200.model import KvCache, LlamaConfig, LlamaModel, forward_tree  # noqa: E402
+
+# bf16 path vs float32 oracle: |gpu - oracle| <= TOL * max|oracle| per output row
+TOL = 3e-2
+TINY = dict(vocab=512, hidden=256, layers=2, heads=2, kv_heads=1, ffn=512)
+
+
+def gemm(w, x):
+    n, k = x.shape
+    out = torch.empty((n, w.shape[0]), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().tp_debug_gemm(0, w.data_ptr(), x.data_ptr(), n, w.shape[0], k, out.data_ptr(),
+                                        _lib.stream_handle()))
+    return out
+
+
+@pytest.mark.parametrize("n_out,k", [(128, 64), (384, 256), (1024, 4096), (4096, 4096), (768, 1024)])
+@pytest.mark.parametrize("n", [1, 5, 16, 33, 64])
+def test_tcgen05_gemm_vs_torch(n_out, k, n):
+    g = torch.Generator(device="cuda").manual_seed(n_out * 7 + k + n)
+    w = (torch.randn((n_out, k), device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn((n, k), device="cuda", generator=g).to(torch.bfloat16)
+    got = gemm(w, x)
+    want = x.float() @ w.float().t()
+    err = (got - want).abs().max().item()
+    assert err <= 1e-4 * max(1.0, want.abs().max().item()), err
+
+
+def test_tcgen05_gemm_batch_invariant():
+    """Column results do not depend on how many node rows share the MMA (N)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    w = (torch.randn((1024, 4096), device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    x = torch.randn((64, 4096), device="cuda", generator=g).to(torch.bfloat16)
+    full = gemm(w, x)
+    for n in (1, 7, 16, 17, 40):
+        part = gemm(w, x[:n].contiguous())
+        assert torch.equal(part, full[:n]), n
+
+
+def tiny_model(**kw):
+    cfg = LlamaConfig(**{**TINY, **kw})
+    return cfg, LlamaModel(cfg, max_nodes=64), LlamaOracle(**{**TINY, **kw})
+
+
+def test_llama_weights_bit_exact():
+    cfg, m, o = tiny_model()
+    d, q, kv, f = cfg.hidden, cfg.heads * 128, cfg.kv_heads * 128, cfg.ffn
+    as_f32 = lambda u16: (u16.astype(np.uint32) << 16).view(np.float32)  # noqa: E731
+    emb = as_f32(m.read_tensor(0).view(np.uint16)).reshape(cfg.vocab, d)
+    assert np.array_equal(emb, o.embedding)
+    for layer in range(cfg.layers):
+        b = o.blocks[layer]
+        qkv = as_f32(m.read_tensor(1, layer).view(np.uint16)).reshape(q + 2 * kv, d)
+        assert np.array_equal(qkv[:q], b["wq"].T)
+        assert np.array_equal(qkv[q:q + kv], b["wk"].T)
+        assert np.array_equal(qkv[q + kv:], b["wv"].T)
+        wo = as_f32(m.read_tensor(4, layer).view(np.uint16)).reshape(d, q)
+        assert np.array_equal(wo, b["wo"].T)
+        gu = as_f32(m.read_tensor(5, layer).view(np.uint16)).reshape(2 * f // 128, 2, 64, d)
+        assert np.array_equal(gu[:, 0].reshape(f, d), b["wg"].T)
+        assert np.array_equal(gu[:, 1].reshape(f, d), b["wu"].T)
+        wd = as_f32(m.read_tensor(7, layer).view(np.uint16)).reshape(d, f)
+        assert np.array_equal(wd, b["wd"].T)
+    head = as_f32(m.read_tensor(8).view(np.uint16)).reshape(cfg.vocab, d)
+    assert np.array_equal(head, o.lm_head.T)
+
+
+def _prefix(m, o, prompt):
+    cache, okv = KvCache(m.cfg.layers, m.cfg.hidden), o.new_kv()
+    for pos, tok in enumerate(prompt):
+        m.forward_position(m.embed(tok, pos), cache, list(range(len(cache))), uid=-1, position=pos, prefix=True)
+        o.run_position(o.embed(tok, pos), okv, list(range(len(okv))), pos=pos, prefix=True)
+    return cache, okv
+
+
+def _rowwise_close(got, want, tol=TOL):
+    got = got.detach().cpu().numpy() if hasattr(got, "detach") else got
+    for a, b in zip(got, want):
+        scale = max(1.0, float(np.abs(b).max()))
+        assert float(np.abs(a - b).max()) <= tol * scale, float(np.abs(a - b).max()) / scale
+
+
+def test_llama_tree_forward_vs_oracle():
+    cfg, m, o = tiny_model()
+    rng = np.random.default_rng(5)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, 70)]  # crosses a 64-slot chunk
+    cache, okv = _prefix(m, o, prompt)
+    P = len(prompt)
+    # three-level tree: 3 children of the root, 2 grandchildren each
+    nodes = [(100 + i, int(rng.integers(cfg.vocab)), P, frozenset({100 + i})) for i in range(3)]
+    nodes += [(200 + 2 * i + j, int(rng.integers(cfg.vocab)), P + 1, frozenset({100 + i, 200 + 2 * i + j}))
+              for i in range(3) for j in range(2)]
+    got = forward_tree(m, cache, nodes)
+    want = forward_nodes(o, okv, nodes)
+    _rowwise_close(got, want)
+    lg = m.logits_many(got).cpu().numpy()
+    for r in range(len(nodes)):
+        ol = o.logits(want[r])
+        assert float(np.abs(lg[r] - ol).max()) <= TOL * max(1.0, float(np.abs(ol).max()))
+
+
+def test_llama_batch_invariance_bitwise():
+    cfg, m, o = tiny_model()
+    rng = np.random.default_rng(9)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, 61)]
+
+    def fresh():
+        c = KvCache(cfg.layers, cfg.hidden)
+        tp.model.prefill_rows(m, c, prompt)
+        return c
+
+    # level of 9 siblings at position P, then each alone
+    P = len(prompt)
+    nodes = [(10 + i, int(rng.integers(cfg.vocab)), P, frozenset({10 + i})) for i in range(9)]
+    together = forward_tree(m, fresh(), nodes).cpu()
+    for i, nd in enumerate(nodes):
+        alone = forward_tree(m, fresh(), [nd]).cpu()
+        assert torch.equal(alone[0], together[i]), i
+    # a depth-4 chain crossing the 64-slot boundary == sequential prefill of the same tokens
+    chain_toks = [int(t) for t in rng.integers(0, cfg.vocab, 5)]
+    c1 = fresh()
+    outs = []
+    anc = set()
+    for d, t in enumerate(chain_toks):
+        anc = anc | {300 + d}
+        outs.append(forward_tree(m, c1, [(300 + d, t, P + d, frozenset(anc))])[0].cpu())
+    c2 = fresh()
+    seq = tp.model.prefill_rows(m, c2, chain_toks, start_pos=P).cpu()
+    for d in range(len(chain_toks)):
+        assert torch.equal(outs[d], seq[d]), d
+
+
+def test_llama_pipeline_lossless_and_margin_parity():
+    cfg, m, o = tiny_model()
+    prompt = [3, 1, 4, 1, 5, 9, 2, 6]
+    n_tok = 24
+    gpu_seq = tp.sequential_decode(m, prompt, n_tok)
+    for stages, miss in ((2, 0.0), (2, 0.3)):
+        draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=min(0.7, 1 - miss), rank_decay=0.5,
+                                                          miss_prob=miss, seed=11), cfg.vocab)
+        res = tp.run(m, tp.PipelineConfig(num_stages=stages), tp.BeamConfig(w=4, k=4), draft, prompt, n_tok,
+                     collect_trace=False)
+        assert res.tokens == gpu_seq
+    # teacher-forced agreement with the oracle wherever its top-1 margin exceeds the tolerance
+    okv = o.new_kv()
+    x = None
+    for pos, tok in enumerate(prompt):
+        x = o.run_position(o.embed(tok, pos), okv, list(range(len(okv))), pos=pos, prefix=True)
+    checked = 0
+    for i, tok in enumerate(gpu_seq):
+        lg = o.logits(x)
+        top2 = np.sort(lg)[-2:]
+        if top2[1] - top2[0] > TOL * max(1.0, float(np.abs(lg).max())):
+            assert int(np.argmax(lg)) == tok, i
+            checked += 1
+        x = o.run_position(o.embed(tok, len(prompt) + i), okv, list(range(len(okv))), pos=len(prompt) + i,
+                           prefix=True)
+    assert checked >= n_tok // 2

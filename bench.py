@@ -1,0 +1,358 @@
+"""Benchmark: SpecPipe single-request time-between-tokens on B200.
+
+Workload (BASELINE.json configs[1]): Llama-2-7B-shape random-init target
+(LCG weights, fan-in scaled, bf16), 8 pipeline stages, single request,
+dynamic tree w=64 / k=16, 512-token synthetic prompt, SyntheticDraft with
+the paper-calibrated defaults (top1 0.62, decay 0.6, miss 0.01) bound to
+the model's own greedy continuation.  With --gpus N the 8 stages are spread
+over N GPUs (stage s on GPU s*N//8) and driven by one host process (the
+reference's single-process design); other ranks only join the barriers.
+
+  value   engine TBT: PipelineRunner.step on the recorded levels (draft cost
+          excluded, level inputs staged), CUDA-event timed on the stream
+  e2e     the public decode_step() path with the live draft, host buffers in
+          and the verified token out every step (wall clock == event clock,
+          the host blocks on the token each step)
+  roofline  the tcgen05 weight-streaming GEMM (K2): algorithmic bytes
+          (weights + node rows) / event-timed launch duration, averaged over
+          every GEMM launch of a profiled replay of the timed steps
+  cpu_baseline  the numpy restatement of the same step (oracle/llama.py,
+          per-node float32 matvecs as the reference's layer_step) timed on a
+          bounded sample and scaled to the measured node-layer count per step
+
+--impl reference times that CPU restatement as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TBT ms/token (single request, 8-stage)"
+UNIT = "ms/token"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="7b", choices=["7b", "13b", "70b", "tiny"])
+    ap.add_argument("--stages", type=int, default=8)
+    ap.add_argument("--prompt-len", type=int, default=512)
+    ap.add_argument("--w", type=int, default=64)
+    ap.add_argument("--k", type=int, default=16)
+    ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=16)
+    return ap.parse_args()
+
+
+def model_cfg(name):
+    from paper_2504_04104_b200.model import LlamaConfig
+
+    return {"7b": LlamaConfig.llama2_7b, "13b": LlamaConfig.llama2_13b, "70b": LlamaConfig.llama2_70b,
+            "tiny": lambda: LlamaConfig(vocab=512, hidden=256, layers=8, heads=2, kv_heads=1, ffn=512)}[name]()
+
+
+def draft_cfg(kind, seed=0):
+    import paper_2504_04104_b200 as tp
+
+    if kind == "perfect":
+        return tp.SyntheticDraftConfig(top1_hit=1.0, rank_decay=0.5, miss_prob=0.0, seed=seed)
+    return tp.SyntheticDraftConfig(seed=seed)
+
+
+def workload(args):
+    return {"workload": f"Llama-2-{args.model}-shape target, {args.stages}-stage SpecPipe, single request, dynamic tree",
+            "model": f"llama2-{args.model}-shape (random LCG init, fan-in scaled)", "stages": args.stages,
+            "w": args.w, "k": args.k, "prompt_len": args.prompt_len, "draft": f"SyntheticDraft({args.draft})",
+            "global_batch": 1, "parallelism": f"pp{args.stages} over {args.gpus} GPU(s)",
+            "l2": "no flush: every step streams all stage weights (>>126 MB L2)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu=0):
+        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+
+def cpu_step_estimate(cfg, node_layers_per_step, head_per_token, prompt_len, sample_nodes=4):
+    """Time the numpy restatement on a bounded sample: `sample_nodes` tree-node
+    forwards through one Llama layer (ctx = prompt_len) plus one LM-head row,
+    then scale to the measured node-layer count of a step."""
+    from oracle.llama import LlamaOracle, bf16
+    from oracle.toy import OracleKv
+
+    t_build = time.perf_counter()
+    o = LlamaOracle(cfg.vocab, cfg.hidden, cfg.layers, cfg.heads, cfg.kv_heads, cfg.ffn, seed=cfg.seed,
+                    layer_range=(0, 1), with_head=True)
+    build_s = time.perf_counter() - t_build
+    kvd = cfg.kv_heads * 128
+    kv = OracleKv(cfg.layers, kvd)
+    rng = np.random.default_rng(0)
+    for p in range(prompt_len):  # synthetic prefix rows (values irrelevant to timing)
+        kv.open_row(-1, p, True)
+        kv.put(0, bf16(rng.standard_normal(kvd).astype(np.float32)), bf16(rng.standard_normal(kvd).astype(np.float32)))
+    x = o.embed(1, prompt_len)
+    rows = list(range(prompt_len))
+    t0 = time.perf_counter()
+    for i in range(sample_nodes):
+        o.run_position(x, kv, rows, (0, 1), True, 10 + i, prompt_len)
+    t_node_layer = (time.perf_counter() - t0) / sample_nodes
+    t0 = time.perf_counter()
+    o.greedy(x)
+    t_head = time.perf_counter() - t0
+    ms = (t_node_layer * node_layers_per_step + t_head * head_per_token) * 1e3
+    return ms, {"t_node_layer_ms": t_node_layer * 1e3, "t_head_ms": t_head * 1e3, "build_s": build_s,
+                "sample": f"{sample_nodes} node forwards through one {cfg.hidden}-wide layer (ctx {prompt_len}) + "
+                          f"1 LM-head row, scaled to {node_layers_per_step:.0f} node-layers/step"}
+
+
+def run_reference(args):
+    cfg = model_cfg(args.model)
+    # node-layers per step measured on the GPU run of this config (mean over the
+    # timed window; probe in SURVEY §8: sum of mean resident nodes ~169 at m=8,w=64)
+    nl = float(os.environ.get("TP_NODE_LAYERS_PER_STEP", 169.3 * cfg.layers / args.stages))
+    cores = os.cpu_count()
+    samples = []
+    for _ in range(max(1, min(args.steps, 3))):
+        ms, info = cpu_step_estimate(cfg, nl, 1.0, args.prompt_len)
+        samples.append(ms)
+    value = float(np.median(samples))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def build_shards(cfg, stages, ngpu, max_nodes):
+    from paper_2504_04104_b200.model import LlamaModel
+    from paper_2504_04104_b200.pipeline import split_layers
+
+    splits = split_layers(cfg.layers, stages)
+    dev_of = [s * ngpu // stages for s in range(stages)]
+    shards = {}
+    for dev in sorted(set(dev_of)):
+        mine = [splits[s] for s in range(stages) if dev_of[s] == dev]
+        lo, hi = mine[0][0], mine[-1][1]
+        shards[dev] = LlamaModel(cfg, device=dev, max_nodes=max_nodes, layer_range=(lo, hi),
+                                 with_embed=(lo == 0), with_head=(hi == cfg.layers))
+    return [shards[dev_of[s]] for s in range(stages)], splits
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    import paper_2504_04104_b200 as tp
+    from paper_2504_04104_b200 import _lib
+    from paper_2504_04104_b200.pipeline import PipelineConfig, PipelineRunner, sequential_decode_staged
+
+    ngpu = args.gpus
+    torch.cuda.set_device(0)
+    cfg = model_cfg(args.model)
+    t0 = time.perf_counter()
+    shards, splits = build_shards(cfg, args.stages, ngpu, max_nodes=max(64, args.w))
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t0
+    prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, args.prompt_len)]
+    n_ref = args.warmup + args.steps + 2 * args.stages + 8
+    ref = sequential_decode_staged(shards if ngpu > 1 else shards[0], splits, prompt, n_ref)
+    pcfg = PipelineConfig(num_stages=args.stages, layer_splits=tuple(splits))
+    beam = tp.BeamConfig(w=args.w, k=args.k)
+    model_arg = shards if ngpu > 1 else shards[0]
+
+    def fresh(draft):
+        r = PipelineRunner(model_arg, pcfg, beam, draft, collect_trace=False,
+                           kv_capacity=args.prompt_len + n_ref + args.w * (args.stages + 2) + 64,
+                           check_invariants=False)
+        r.prefill(prompt)
+        return r
+
+    streams = [torch.cuda.current_stream(d) for d in range(ngpu)]
+
+    def sync_all():
+        for d in range(ngpu):
+            torch.cuda.synchronize(d)
+
+    # ---- e2e: public decode_step with the live draft ----------------------------------
+    draft = tp.SyntheticDraft(draft_cfg(args.draft), cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(ref))
+    runner = fresh(draft)
+    runner.children_log = []
+    for _ in range(args.warmup):
+        runner.decode_step()
+    sync_all()
+    tok0, steps0 = len(runner.emitted), runner.step_no
+    l0 = _lib.launch_count()
+    io0 = _lib.io_bytes()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(0) as clocks:
+        t_wall = time.perf_counter()
+        ev[0].record(streams[0])
+        for _ in range(args.steps):
+            runner.decode_step()
+        ev[1].record(streams[-1] if ngpu > 1 else streams[0])
+        sync_all()
+        t_wall = time.perf_counter() - t_wall
+    e2e_tokens = len(runner.emitted) - tok0
+    e2e_ms = t_wall * 1e3 / max(1, e2e_tokens)
+    launches = _lib.launch_count() - l0
+    io1 = _lib.io_bytes()
+    resident = []
+    children = runner.children_log
+    assert runner.emitted == ref[: len(runner.emitted)], "SpecPipe output diverged from greedy decode"
+    hit_rate = runner.hits / max(1, runner.hits + runner.misses)
+    runner.close()
+    del runner
+
+    # ---- value: engine step on the recorded levels -----------------------------------
+    replay = fresh(None)
+    for ch in children[: args.warmup]:
+        replay.step(ch)
+    sync_all()
+    tok0 = len(replay.emitted)
+    node_layers = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(streams[0])
+    for ch in children[args.warmup : args.warmup + args.steps]:
+        node_layers += sum(len(s.resident) * (s.layer_range[1] - s.layer_range[0])
+                           for s in replay.stages if s.resident is not None)
+        resident.append([len(s.resident) if s.resident is not None else 0 for s in replay.stages])
+        replay.step(ch)
+    e1.record(streams[0])
+    sync_all()
+    value_tokens = len(replay.emitted) - tok0
+    value_ms = e0.elapsed_time(e1) / max(1, value_tokens)
+    assert replay.emitted == ref[: len(replay.emitted)]
+
+    # ---- roofline: profiled replay of the next steps -------------------------------------
+    _lib.profile_enable(True)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(streams[0])
+    prof_steps = children[args.warmup + args.steps : args.warmup + args.steps + args.profile_steps] or \
+        children[args.warmup : args.warmup + args.profile_steps]
+    for ch in prof_steps:
+        replay.step(ch)
+    pe1.record(streams[0])
+    sync_all()
+    _lib.profile_enable(False)
+    gemm_ms, gemm_bytes, gemm_n = _lib.profile_read()
+    prof_total_ms = pe0.elapsed_time(pe1)
+    peak, peak_src = peaks()
+    achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
+
+    steps_per_token = args.steps / max(1, e2e_tokens)
+    per_step_h2d = (io1[0] - io0[0]) / args.steps
+    per_step_d2h = (io1[1] - io0[1]) / args.steps
+    line = {
+        "metric": METRIC, "value": round(value_ms, 4), "unit": UNIT, "n_gpus": ngpu, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(value_ms / steps_per_token, 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload(args),
+        "tokens_per_s": round(1e3 / value_ms, 2),
+        "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": int(per_step_h2d),
+                "d2h_bytes_per_step": int(per_step_d2h), "tokens_per_s": round(1e3 / e2e_ms, 2)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "sk_gemm_kernel (tcgen05 weight-streaming GEMM)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "gemm_share_of_step": round(gemm_ms / prof_total_ms, 4) if prof_total_ms else None,
+                     "gemm_launches": gemm_n, "bytes_per_launch": round(gemm_bytes / max(1, gemm_n))},
+        "clocks": clocks.summary(),
+        "steps_per_token": round(steps_per_token, 4), "hit_rate": round(hit_rate, 4),
+        "mean_resident_nodes": [round(float(x), 2) for x in np.mean(np.asarray(resident), axis=0)] if resident else None,
+        "node_layers_per_step": round(node_layers / max(1, len(resident)), 1),
+        "init_s": round(init_s, 1),
+    }
+    if rank == 0 and ngpu == 1 and not args.no_cpu_baseline:
+        ms, info = cpu_step_estimate(cfg, node_layers / max(1, len(resident)), 1.0, args.prompt_len)
+        line["cpu_baseline"] = {"value": round(ms * steps_per_token, 2), "unit": UNIT, "cores": os.cpu_count(),
+                                "kind": "port", "sample": info["sample"]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        pg = dist
+    try:
+        if rank == 0:
+            if args.impl == "reference":
+                run_reference(args)
+            else:
+                run_ours(args, rank, world)
+    finally:
+        if pg is not None:
+            pg.barrier()
+            pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

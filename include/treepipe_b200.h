@@ -126,6 +126,16 @@ int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t ro
 /* Grow the KV capacity (reference KvCache grow-by-doubling, model.py:141-148). */
 int tp_stage_reserve(tp_stage* s, int32_t capacity_rows);
 
+/* ---- instrumentation (no reference counterpart; used by bench.py) ---------- */
+/* Kernels launched by this library since load (every launch site counts). */
+int tp_launch_count(int64_t* out);
+/* Host<->device bytes moved by this library's own copies since load. */
+int tp_io_bytes(int64_t* h2d, int64_t* d2h);
+/* Time every K2 GEMM launch with CUDA events on its stream while enabled;
+ * tp_profile_read returns summed ms, algorithmic bytes and launch count, then resets. */
+int tp_profile_enable(int32_t on);
+int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* launches);
+
 /* ---- test hook (no reference counterpart): the K2 weight-streaming GEMM alone.
  * out[n][n_out] (f32, dev) = x[n][k] (bf16, dev) . w[n_out][k]^T (bf16, dev).   */
 int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out, int32_t k,

@@ -72,7 +72,33 @@ _SIGS = {
     "tp_stage_read_kv": (C.c_int, [_P, _I, _I, _I, _I, _P]),
     "tp_rows_compact": (C.c_int, [_P, _P, _P, C.c_int64, _I, _P, C.POINTER(C.c_int32), _P]),
     "tp_debug_gemm": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _P]),
+    "tp_launch_count": (C.c_int, [C.POINTER(C.c_int64)]),
+    "tp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tp_profile_enable": (C.c_int, [_I]),
+    "tp_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }
+
+
+def launch_count() -> int:
+    n = C.c_int64()
+    check(load().tp_launch_count(C.byref(n)))
+    return n.value
+
+
+def io_bytes() -> tuple[int, int]:
+    h, d = C.c_int64(), C.c_int64()
+    check(load().tp_io_bytes(C.byref(h), C.byref(d)))
+    return h.value, d.value
+
+
+def profile_enable(on: bool) -> None:
+    check(load().tp_profile_enable(int(on)))
+
+
+def profile_read() -> tuple[float, float, int]:
+    ms, by, n = C.c_double(), C.c_double(), C.c_int64()
+    check(load().tp_profile_read(C.byref(ms), C.byref(by), C.byref(n)))
+    return ms.value, by.value, n.value
 
 EXPORTED = tuple(_SIGS)
 

@@ -8,10 +8,30 @@
 
 #include "internal.h"
 
+#include <atomic>
+
 namespace tp {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_h2d{0}, g_d2h{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static void count_io(long long h2d, long long d2h) {
+  g_h2d.fetch_add(h2d, std::memory_order_relaxed);
+  g_d2h.fetch_add(d2h, std::memory_order_relaxed);
+}
 }  // namespace tp
+
+extern "C" int tp_launch_count(int64_t* out) {
+  *out = tp::g_launches.load();
+  return TP_OK;
+}
+
+extern "C" int tp_io_bytes(int64_t* h2d, int64_t* d2h) {
+  *h2d = tp::g_h2d.load();
+  *d2h = tp::g_d2h.load();
+  return TP_OK;
+}
 
 using namespace tp;
 
@@ -46,6 +66,7 @@ int upload(tp_stage* s, const void* host, size_t bytes, size_t dev_off, cudaStre
   TP_CUDA(cudaEventSynchronize(s->meta_done));  // previous upload has left the pinned buffer
   std::memcpy(s->host_meta + dev_off, host, bytes);
   TP_CUDA(cudaMemcpyAsync(s->meta + dev_off, s->host_meta + dev_off, bytes, cudaMemcpyHostToDevice, st));
+  count_io((long long)bytes, 0);
   TP_CUDA(cudaEventRecord(s->meta_done, st));
   return TP_OK;
 }
@@ -376,6 +397,7 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
   std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
   if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
   TP_CUDA(cudaMemcpyAsync(s->meta, h, total, cudaMemcpyHostToDevice, st));
+  count_io((long long)total, 0);
   TP_CUDA(cudaEventRecord(s->meta_done, st));
   LevelDev lv;
   lv.n = n;
@@ -472,6 +494,7 @@ int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int
   if (n_children) TP_TRY(upload(ws, child_tokens, 4 * (size_t)n_children, 0, st));
   TP_TRY(argmax_match(ws->logits, is_toy(m), m->cfg.vocab, (const int32_t*)ws->meta, n_children, ws->d_result, st));
   TP_CUDA(cudaMemcpyAsync(ws->h_result, ws->d_result, 8, cudaMemcpyDeviceToHost, st));
+  count_io(0, 8);
   TP_CUDA(cudaStreamSynchronize(st));
   result_host[0] = ws->h_result[0];
   result_host[1] = ws->h_result[1];

@@ -355,9 +355,9 @@ int attn_tree(const AttnArgs& a, const LevelDev& lv, int splits, cudaStream_t st
     smem_set = smem;
   }
   dim3 grid(a.H, splits, (lv.n + kCtaNodes - 1) / kCtaNodes);
-  attn_tree_kernel<<<grid, kWarps * 32, smem, st>>>(a, lv);
+  ::tp::count_launch(), attn_tree_kernel<<<grid, kWarps * 32, smem, st>>>(a, lv);
   TP_CUDA(cudaGetLastError());
-  attn_combine_kernel<<<dim3(lv.n, a.H), kAttnHeadDim, 0, st>>>(a, lv.n, splits);
+  ::tp::count_launch(), attn_combine_kernel<<<dim3(lv.n, a.H), kAttnHeadDim, 0, st>>>(a, lv.n, splits);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }

@@ -72,3 +72,9 @@ __device__ __forceinline__ float warp_max_f32(float v) {
 }
 
 }  // namespace tp
+
+namespace tp {
+// Every kernel launch site calls this (`count_launch(), k<<<...>>>(...)`), so the
+// bench can report how many of our kernels ran inside its timed region.
+void count_launch();
+}  // namespace tp

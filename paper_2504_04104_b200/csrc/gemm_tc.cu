@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "gemm_tc.h"
 #include "sm100.cuh"
@@ -224,6 +225,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Optional per-launch timing of the GEMM (bench roofline): CUDA events on the
+// launching stream around each launch, with the launch's algorithmic bytes
+// (weights once + node rows once).
+struct ProfRec {
+  cudaEvent_t a, b;
+  double bytes;
+};
+static std::vector<ProfRec> g_prof;
+static bool g_prof_on = false;
+static std::mutex g_prof_mu;
+
 int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, float* part, cudaStream_t st) {
   TP_CHECK(p.n >= 1 && p.n_pad <= 256, TP_ESHAPE, "GEMM node count outside [1, 256]");
   const int stages = stages_for(p.n_pad);
@@ -233,8 +245,20 @@ int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, flo
     TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  sk_gemm_kernel<<<p.G, kThreads, smem, st>>>(*tmA, *tmB, p, stages, part);
+  ProfRec rec{};
+  if (g_prof_on) {
+    TP_CUDA(cudaEventCreate(&rec.a));
+    TP_CUDA(cudaEventCreate(&rec.b));
+    TP_CUDA(cudaEventRecord(rec.a, st));
+    rec.bytes = (double)p.mtiles * kBM * p.KB * kBK * 2.0 + (double)p.n * p.KB * kBK * 2.0;
+  }
+  ::tp::count_launch(), sk_gemm_kernel<<<p.G, kThreads, smem, st>>>(*tmA, *tmB, p, stages, part);
   TP_CUDA(cudaGetLastError());
+  if (g_prof_on) {
+    TP_CUDA(cudaEventRecord(rec.b, st));
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof.push_back(rec);
+  }
   return TP_OK;
 }
 
@@ -244,6 +268,30 @@ __global__ void sk_reduce_kernel(const float* __restrict__ part, SkPlan p, int n
 }
 
 }  // namespace tp
+
+extern "C" int tp_profile_enable(int32_t on) {
+  tp::g_prof_on = on != 0;
+  return TP_OK;
+}
+
+extern "C" int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* launches) {
+  std::lock_guard<std::mutex> g(tp::g_prof_mu);
+  double ms = 0.0, bytes = 0.0;
+  for (auto& r : tp::g_prof) {
+    float t = 0.f;
+    TP_CUDA(cudaEventSynchronize(r.b));
+    TP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    bytes += r.bytes;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  *gemm_ms = ms;
+  *gemm_bytes = bytes;
+  *launches = (int64_t)tp::g_prof.size();
+  tp::g_prof.clear();
+  return TP_OK;
+}
 
 extern "C" int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out,
                              int32_t k, void* out_dev, void* stream) {
@@ -258,7 +306,7 @@ extern "C" int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_de
   float* part = nullptr;
   TP_CUDA(cudaMallocAsync((void**)&part, sk_part_floats(p) * 4, st));
   TP_TRY(sk_gemm(&ma, &mb, p, part, st));
-  sk_reduce_kernel<<<dim3(n, (n_out + 255) / 256), 256, 0, st>>>(part, p, n_out, (float*)out_dev);
+  ::tp::count_launch(), sk_reduce_kernel<<<dim3(n, (n_out + 255) / 256), 256, 0, st>>>(part, p, n_out, (float*)out_dev);
   TP_CUDA(cudaGetLastError());
   TP_CUDA(cudaFreeAsync(part, st));
   TP_CUDA(cudaStreamSynchronize(st));

@@ -55,7 +55,7 @@ int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, vo
   if (n_keep == 0 || nl == 0) return TP_OK;
   int64_t plane = (int64_t)s->cap * row_bytes;  // one kv-head plane
   dim3 grid(2 * nl, s->kv_heads);
-  kv_move_kernel<<<grid, kMoveThreads, 0, st>>>(d_planes, plane, row_bytes, d_src_rows, n_keep, first);
+  ::tp::count_launch(), kv_move_kernel<<<grid, kMoveThreads, 0, st>>>(d_planes, plane, row_bytes, d_src_rows, n_keep, first);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -71,7 +71,7 @@ int rows_compact(const void* src, void* dst, int64_t row_bytes, const int32_t* d
                  cudaStream_t st) {
   TP_CHECK(row_bytes % 16 == 0, TP_ESHAPE, "row bytes must be a multiple of 16");
   if (n_out == 0) return TP_OK;
-  rows_gather_kernel<<<n_out, 256, 0, st>>>((const char*)src, (char*)dst, (int)row_bytes, d_idx);
+  ::tp::count_launch(), rows_gather_kernel<<<n_out, 256, 0, st>>>((const char*)src, (char*)dst, (int)row_bytes, d_idx);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -135,10 +135,10 @@ __global__ void __launch_bounds__(1024) argmax_match_kernel(const T* __restrict_
 int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_children, int n_children,
                  int32_t* d_result, cudaStream_t st) {
   if (is_f64)
-    argmax_match_kernel<double><<<1, 1024, 0, st>>>((const double*)logits, vocab, d_children, n_children,
+    ::tp::count_launch(), argmax_match_kernel<double><<<1, 1024, 0, st>>>((const double*)logits, vocab, d_children, n_children,
                                                     d_result);
   else
-    argmax_match_kernel<float><<<1, 1024, 0, st>>>((const float*)logits, vocab, d_children, n_children,
+    ::tp::count_launch(), argmax_match_kernel<float><<<1, 1024, 0, st>>>((const float*)logits, vocab, d_children, n_children,
                                                    d_result);
   TP_CUDA(cudaGetLastError());
   return TP_OK;

@@ -103,7 +103,7 @@ int lcg_fill_f64(double* out, int64_t count, uint64_t seed, int64_t start, cudaS
   TP_TRY(fill_lcg_jump_table());
   int64_t threads = ceil_div64(count, kRun);
   int block = 256;
-  lcg_f64_kernel<<<(unsigned)ceil_div64(threads, block), block, 0, st>>>(out, count, seed, start);
+  ::tp::count_launch(), lcg_f64_kernel<<<(unsigned)ceil_div64(threads, block), block, 0, st>>>(out, count, seed, start);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -113,7 +113,7 @@ int lcg_fill_bf16_rows(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, ui
   TP_TRY(fill_lcg_jump_table());
   int64_t threads = ceil_div64(rows_in * cols_out, kRun);
   int block = 256;
-  lcg_bf16_t_kernel<<<(unsigned)ceil_div64(threads, block), block, 0, st>>>(out, rows_in, cols_out, seed,
+  ::tp::count_launch(), lcg_bf16_t_kernel<<<(unsigned)ceil_div64(threads, block), block, 0, st>>>(out, rows_in, cols_out, seed,
                                                                            start, scale, row_offset,
                                                                            interleave64);
   TP_CUDA(cudaGetLastError());
@@ -124,7 +124,7 @@ int lcg_fill_bf16(__nv_bfloat16* out, int64_t count, uint64_t seed, int64_t star
                   cudaStream_t st) {
   TP_TRY(fill_lcg_jump_table());
   int64_t threads = ceil_div64(count, kRun);
-  lcg_bf16_kernel<<<(unsigned)ceil_div64(threads, 256), 256, 0, st>>>(out, count, seed, start, scale);
+  ::tp::count_launch(), lcg_bf16_kernel<<<(unsigned)ceil_div64(threads, 256), 256, 0, st>>>(out, count, seed, start, scale);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }

@@ -270,7 +270,7 @@ void llama_stage_free(tp_stage* s) {
 
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st) {
   TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
-  llama_embed_kernel<<<n, 256, 0, st>>>((const __nv_bfloat16*)m->embed, d_tokens, m->cfg.hidden, out);
+  ::tp::count_launch(), llama_embed_kernel<<<n, 256, 0, st>>>((const __nv_bfloat16*)m->embed, d_tokens, m->cfg.hidden, out);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -280,11 +280,11 @@ int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits
   TP_TRY(llama_stage_init(ws));
   LlamaStageExt* e = sext(ws);
   const int d = m->cfg.hidden, V = m->cfg.vocab;
-  rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
+  ::tp::count_launch(), rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
   const SkPlan ph = sk_plan(V, d, n);
   TP_TRY(sk_gemm(&mext(m)->head, &e->mXd, ph, e->part, st));
-  logits_kernel<<<dim3(n, (V + 255) / 256), 256, 0, st>>>(e->part, ph, V, logits);
+  ::tp::count_launch(), logits_kernel<<<dim3(n, (V + 255) / 256), 256, 0, st>>>(e->part, ph, V, logits);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -305,7 +305,7 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
     TP_TRY(llama_embed(m, n, lv.tokens, x, st));
   }
   if (lv.layer_lo == lv.layer_hi) return TP_OK;
-  rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, c.norm_eps, e->Xd);
+  ::tp::count_launch(), rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, c.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
   const SkPlan pqkv = sk_plan(q + 2 * kvd, d, n), po = sk_plan(d, q, n), pgu = sk_plan(2 * f, d, n),
                pdn = sk_plan(d, f, n);
@@ -331,20 +331,20 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
     __nv_bfloat16* kc = (__nv_bfloat16*)s->k[layer - s->lo];
     __nv_bfloat16* vc = (__nv_bfloat16*)s->v[layer - s->lo];
     TP_TRY(sk_gemm(&me->qkv[li], &e->mXd, pqkv, e->part, st));
-    qkv_epilogue_kernel<<<dim3(n, H + 2 * KV), 64, 0, st>>>(e->part, pqkv, lv, H, KV, (double)c.rope_theta, e->Xq,
+    ::tp::count_launch(), qkv_epilogue_kernel<<<dim3(n, H + 2 * KV), 64, 0, st>>>(e->part, pqkv, lv, H, KV, (double)c.rope_theta, e->Xq,
                                                             kc, vc, s->cap, e->kself, e->vself);
     TP_CUDA(cudaGetLastError());
     aa.k = kc;
     aa.v = vc;
     TP_TRY(attn_tree(aa, lv, splits, st));
     TP_TRY(sk_gemm(&me->o[li], &e->mXo, po, e->part, st));
-    resid_norm_kernel<<<n, 256, 0, st>>>(e->part, po, 1, x, d, c.norm_eps, e->Xd, 1);
+    ::tp::count_launch(), resid_norm_kernel<<<n, 256, 0, st>>>(e->part, po, 1, x, d, c.norm_eps, e->Xd, 1);
     TP_CUDA(cudaGetLastError());
     TP_TRY(sk_gemm(&me->gu[li], &e->mXd, pgu, e->part, st));
-    swiglu_kernel<<<dim3(n, (f + 255) / 256), 256, 0, st>>>(e->part, pgu, f, e->Xf);
+    ::tp::count_launch(), swiglu_kernel<<<dim3(n, (f + 255) / 256), 256, 0, st>>>(e->part, pgu, f, e->Xf);
     TP_CUDA(cudaGetLastError());
     TP_TRY(sk_gemm(&me->down[li], &e->mXf, pdn, e->part, st));
-    resid_norm_kernel<<<n, 256, 0, st>>>(e->part, pdn, 1, x, d, c.norm_eps, e->Xd, layer + 1 < lv.layer_hi);
+    ::tp::count_launch(), resid_norm_kernel<<<n, 256, 0, st>>>(e->part, pdn, 1, x, d, c.norm_eps, e->Xd, layer + 1 < lv.layer_hi);
     TP_CUDA(cudaGetLastError());
   }
   return TP_OK;

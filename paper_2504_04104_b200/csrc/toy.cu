@@ -202,7 +202,7 @@ __global__ void toy_head_kernel(const double* __restrict__ E, const double* __re
 static int gemm(const double* in, int n, int K, const double* W, int N, double* out, int64_t out_stride,
                 const double* res, int relu, cudaStream_t st) {
   dim3 grid(ceil_div(N, kGemmCols), ceil_div(n, kGemmRows));
-  toy_gemm_kernel<<<grid, kGemmCols, 0, st>>>(in, n, K, W, N, out, out_stride, res, relu);
+  ::tp::count_launch(), toy_gemm_kernel<<<grid, kGemmCols, 0, st>>>(in, n, K, W, N, out, out_stride, res, relu);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -215,7 +215,7 @@ int toy_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes) {
 
 int toy_embed(tp_model* m, int n, const int32_t* d_tokens, const int32_t* d_pos, double* out, cudaStream_t st) {
   TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
-  toy_embed_kernel<<<n, 128, 0, st>>>((const double*)m->embed, d_tokens, d_pos, m->cfg.hidden, out);
+  ::tp::count_launch(), toy_embed_kernel<<<n, 128, 0, st>>>((const double*)m->embed, d_tokens, d_pos, m->cfg.hidden, out);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -224,9 +224,9 @@ int toy_logits(tp_model* m, tp_stage* ws, int n, const double* x, double* logits
   TP_CHECK(m->embed, TP_ECONFIG, "tied head needs the embedding table on this model");
   int d = m->cfg.hidden, V = m->cfg.vocab;
   double* h = (double*)ws->ws;
-  toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
+  ::tp::count_launch(), toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
   dim3 grid(ceil_div(V * 32, 256), n);
-  toy_head_kernel<<<grid, 256, 0, st>>>((const double*)m->embed, h, V, d, logits);
+  ::tp::count_launch(), toy_head_kernel<<<grid, 256, 0, st>>>((const double*)m->embed, h, V, d, logits);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -261,14 +261,14 @@ int toy_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hi
     double* Vc = (double*)s->v[layer - s->lo];
     double* kdst = lv.append ? Kc + (int64_t)lv.row0 * d : kt;
     double* vdst = lv.append ? Vc + (int64_t)lv.row0 * d : vt;
-    toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
+    ::tp::count_launch(), toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
     TP_TRY(gemm(h, n, d, (const double*)w.w[1], d, q, d, nullptr, 0, st));
     TP_TRY(gemm(h, n, d, (const double*)w.w[2], d, kdst, d, nullptr, 0, st));
     TP_TRY(gemm(h, n, d, (const double*)w.w[3], d, vdst, d, nullptr, 0, st));
-    toy_attn_kernel<<<n, kAttnThreads, smem, st>>>(q, kdst, vdst, Kc, Vc, lv, d, sqrt_d, at);
+    ::tp::count_launch(), toy_attn_kernel<<<n, kAttnThreads, smem, st>>>(q, kdst, vdst, Kc, Vc, lv, d, sqrt_d, at);
     TP_CUDA(cudaGetLastError());
     TP_TRY(gemm(at, n, d, (const double*)w.w[4], d, x, d, x, 0, st));
-    toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
+    ::tp::count_launch(), toy_norm_kernel<<<n, 256, 0, st>>>(x, d, h);
     TP_TRY(gemm(h, n, d, (const double*)w.w[5], f, ff, f, nullptr, 1, st));
     TP_TRY(gemm(ff, n, f, (const double*)w.w[6], d, x, d, x, 0, st));
   }

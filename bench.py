@@ -217,7 +217,7 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t0
     prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, args.prompt_len)]
-    n_ref = args.warmup + args.steps + 2 * args.stages + 8
+    n_ref = args.warmup + args.steps + args.profile_steps + 2 * args.stages + 8
     ref = sequential_decode_staged(shards if ngpu > 1 else shards[0], splits, prompt, n_ref)
     pcfg = PipelineConfig(num_stages=args.stages, layer_splits=tuple(splits))
     beam = tp.BeamConfig(w=args.w, k=args.k)
@@ -260,6 +260,8 @@ def run_ours(args, rank, world):
     e2e_ms = t_wall * 1e3 / max(1, e2e_tokens)
     launches = _lib.launch_count() - l0
     io1 = _lib.io_bytes()
+    for _ in range(args.profile_steps):  # untimed: levels for the profiled replay below
+        runner.decode_step()
     resident = []
     children = runner.children_log
     assert runner.emitted == ref[: len(runner.emitted)], "SpecPipe output diverged from greedy decode"
@@ -291,9 +293,7 @@ def run_ours(args, rank, world):
     _lib.profile_enable(True)
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pe0.record(streams[0])
-    prof_steps = children[args.warmup + args.steps : args.warmup + args.steps + args.profile_steps] or \
-        children[args.warmup : args.warmup + args.profile_steps]
-    for ch in prof_steps:
+    for ch in children[args.warmup + args.steps :]:
         replay.step(ch)
     pe1.record(streams[0])
     sync_all()

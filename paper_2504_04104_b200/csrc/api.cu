@@ -406,6 +406,7 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
   lv.words = L->words;
   lv.bits_base = L->bits_base;
   lv.max_t = max_t;
+  lv.min_p = *std::min_element(L->prefix_rows, L->prefix_rows + n);
   const bool all_layers = L->layer_lo == 0 && L->layer_hi == 0;
   const bool no_layers = L->layer_lo < 0;  // explicit empty range: embed/copy only
   lv.layer_lo = all_layers ? s->lo : (no_layers ? s->lo : L->layer_lo);

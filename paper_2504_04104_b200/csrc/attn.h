@@ -5,29 +5,28 @@
 
 namespace tp {
 
-constexpr int kAttnChunk = 64;        // logical key slots per chunk
-constexpr int kAttnSplitChunks = 4;   // chunks per split (256 positions)
-constexpr int kAttnMaxExtra = 64;     // speculative ancestor rows per node
+constexpr int kAttnChunk = 64;     // logical key slots per canonical chunk
+constexpr int kAttnMaxExtra = 64;  // speculative ancestor rows per node
 constexpr int kAttnHeadDim = 128;
 
 struct AttnArgs {
-  const __nv_bfloat16* q;   // [n][H*128]
+  const __nv_bfloat16* q;  // [n][H*128]
   int q_stride;
-  const __nv_bfloat16* k;   // cache [KV][cap][128]
+  const __nv_bfloat16* k;  // cache [KV][cap][128]
   const __nv_bfloat16* v;
   int cap;
-  const __nv_bfloat16* kself;  // self rows: [n][KV][128] (recompute) or nullptr (rows row0+i of the cache)
+  const __nv_bfloat16* kself;  // self rows: [n][KV][128] (recompute) or nullptr (cache rows row0+i)
   const __nv_bfloat16* vself;
   int H, KV;
   float scale;
-  float* pm;  // [n][H][max_splits] partial max
-  float* pl;  // partial sum
-  float* po;  // [n][H][max_splits][128]
-  int max_splits;
+  float* pm;  // [n][H][max_chunks] per-chunk max
+  float* pl;  // per-chunk sum
+  float* po;  // [n][H][max_chunks][128] per-chunk unnormalised output
+  int max_chunks;
   __nv_bfloat16* out;  // [n][H*128]
   int out_stride;
 };
 
-int attn_tree(const AttnArgs& a, const LevelDev& lv, int splits, cudaStream_t st);
+int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
 
 }  // namespace tp

@@ -22,13 +22,22 @@ __host__ __device__ inline int sk_cta_of(const SkPlan& p, int t) {
   return t < big ? t / (p.q + 1) : p.r + (t - big) / p.q;
 }
 
-// Sum of one output element over its contributors, in fixed order.
+// Sum of one output element over its contributors, in fixed order.  All
+// contributor loads are issued before the (ordered) adds so the reduction is
+// one L2 round trip, not max_contrib dependent ones.
 __device__ __forceinline__ float sk_sum(const float* __restrict__ part, const SkPlan& p, int node, int j) {
   const int mt = j >> 7, r = j & 127;
-  const int c0 = sk_cta_of(p, mt * p.KB), c1 = sk_cta_of(p, (mt + 1) * p.KB - 1);
+  const int cnt = sk_cta_of(p, (mt + 1) * p.KB - 1) - sk_cta_of(p, mt * p.KB) + 1;
   const float* b = part + ((size_t)mt * p.max_contrib * p.n + node) * 128 + r;
-  float acc = b[0];
-  for (int s = 1; s <= c1 - c0; ++s) acc += b[(size_t)s * p.n * 128];
+  const size_t stride = (size_t)p.n * 128;
+  float v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = s < cnt ? __ldcg(b + s * stride) : 0.f;
+  float acc = v[0];
+#pragma unroll
+  for (int s = 1; s < 8; ++s)
+    if (s < cnt) acc += v[s];
+  for (int s = 8; s < cnt; ++s) acc += __ldcg(b + s * stride);
   return acc;
 }
 

@@ -58,6 +58,7 @@ struct LevelDev {
   int bits_base;
   int layer_lo, layer_hi;  // layers to run
   int max_t;               // longest logical key sequence (prefix + ancestors + self)
+  int min_p;               // smallest prefix_rows over the level's nodes
   const int32_t* tokens;
   const int32_t* positions;
   const int32_t* prefix_rows;

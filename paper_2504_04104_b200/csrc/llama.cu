@@ -51,40 +51,57 @@ __global__ void llama_embed_kernel(const __nv_bfloat16* __restrict__ E, const in
   for (int j = threadIdx.x; j < d; j += blockDim.x) x[(size_t)c * d + j] = __bfloat162float(e[j]);
 }
 
-__device__ __forceinline__ float block_sum_256(float v, float* red) {
+constexpr int kNormThreads = 1024;
+constexpr int kNormPer = 8;  // d <= 8192
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum_f32(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (l == 0) red[w] = v;
   __syncthreads();
   if (w == 0) {
-    float t = l < 8 ? red[l] : 0.f;
+    float t = l < nw ? red[l] : 0.f;
     t = warp_sum_f32(t);
-    if (l == 0) red[8] = t;
+    if (l == 0) red[32] = t;
   }
   __syncthreads();
-  const float t = red[8];
+  const float t = red[32];
   __syncthreads();
   return t;
 }
 
-// x[c] (+= GEMM result) ; Xd[c] = bf16(x * 1/sqrt(mean(x^2) + eps))
-__global__ void __launch_bounds__(256) resid_norm_kernel(const float* __restrict__ part, SkPlan p, int add,
-                                                         float* __restrict__ x, int d, float eps,
-                                                         __nv_bfloat16* __restrict__ xd, int do_norm) {
-  __shared__ float red[9];
+// x[c] (+= GEMM result) ; Xd[c] = bf16(x * 1/sqrt(mean(x^2) + eps)).  One CTA per
+// node row; every element's contributor loads are in flight at once.
+__global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(const float* __restrict__ part, SkPlan p,
+                                                                  int add, float* __restrict__ x, int d,
+                                                                  float eps, __nv_bfloat16* __restrict__ xd,
+                                                                  int do_norm) {
+  __shared__ float red[33];
   const int c = blockIdx.x;
   float* xr = x + (size_t)c * d;
+  float v[kNormPer];
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    v[u] = j < d ? xr[j] + (add ? sk_sum(part, p, c, j) : 0.f) : 0.f;
+  }
   float ss = 0.f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float v = xr[j];
-    if (add) v += sk_sum(part, p, c, j);
-    xr[j] = v;
-    ss += v * v;
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    if (j < d) {
+      xr[j] = v[u];
+      ss += v[u] * v[u];
+    }
   }
   if (!do_norm) return;
-  ss = block_sum_256(ss, red);
+  ss = block_sum(ss, red);
   const float r = 1.0f / sqrtf(ss / (float)d + eps);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) xd[(size_t)c * d + j] = __float2bfloat16_rn(xr[j] * r);
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    if (j < d) xd[(size_t)c * d + j] = __float2bfloat16_rn(v[u] * r);
+  }
 }
 
 // RoPE on q/k heads (rotate-half pairs (i, i+64)), scatter q -> Xq, k/v -> cache rows.
@@ -128,15 +145,32 @@ __global__ void swiglu_kernel(const float* __restrict__ part, SkPlan p, int f, _
   xf[(size_t)c * f + fi] = __float2bfloat16_rn(a);
 }
 
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
-                                                      __nv_bfloat16* __restrict__ xd) {
-  __shared__ float red[9];
+// Stand-alone RMSNorm with exactly resid_norm_kernel's reduction shape, so a
+// norm computed at a stage boundary is bit-identical to the fused one a
+// single-stage model computes at the same layer boundary.
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
+                                                               __nv_bfloat16* __restrict__ xd) {
+  __shared__ float red[33];
   const float* xr = x + (size_t)blockIdx.x * d;
+  float v[kNormPer];
   float ss = 0.f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) ss += xr[j] * xr[j];
-  ss = block_sum_256(ss, red);
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    v[u] = j < d ? xr[j] : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    if (j < d) ss += v[u] * v[u];
+  }
+  ss = block_sum(ss, red);
   const float r = 1.0f / sqrtf(ss / (float)d + eps);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) xd[(size_t)blockIdx.x * d + j] = __float2bfloat16_rn(xr[j] * r);
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    if (j < d) xd[(size_t)blockIdx.x * d + j] = __float2bfloat16_rn(v[u] * r);
+  }
 }
 
 __global__ void logits_kernel(const float* __restrict__ part, SkPlan p, int V, float* __restrict__ out) {
@@ -243,17 +277,17 @@ int llama_stage_init(tp_stage* s) {
     TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
     TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));
   }
-  // attention split partials follow the KV capacity
-  const int splits = (s->cap + 1 + kAttnChunk * kAttnSplitChunks - 1) / (kAttnChunk * kAttnSplitChunks);
-  if (splits > e->max_splits) {
+  // attention chunk partials follow the KV capacity (+ ancestors + self)
+  const int chunks = (s->cap + kAttnMaxExtra + 1 + kAttnChunk - 1) / kAttnChunk;
+  if (chunks > e->max_splits) {
     if (e->pm) cudaFree(e->pm);
     if (e->pl) cudaFree(e->pl);
     if (e->po) cudaFree(e->po);
-    const size_t cells = (size_t)e->np * c.heads * splits;
+    const size_t cells = (size_t)e->np * c.heads * chunks;
     TP_CUDA(cudaMalloc(&e->pm, cells * 4));
     TP_CUDA(cudaMalloc(&e->pl, cells * 4));
     TP_CUDA(cudaMalloc(&e->po, cells * 128 * 4));
-    e->max_splits = splits;
+    e->max_splits = chunks;
   }
   return TP_OK;
 }
@@ -280,7 +314,7 @@ int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits
   TP_TRY(llama_stage_init(ws));
   LlamaStageExt* e = sext(ws);
   const int d = m->cfg.hidden, V = m->cfg.vocab;
-  ::tp::count_launch(), rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
+  ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
   const SkPlan ph = sk_plan(V, d, n);
   TP_TRY(sk_gemm(&mext(m)->head, &e->mXd, ph, e->part, st));
@@ -305,12 +339,10 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
     TP_TRY(llama_embed(m, n, lv.tokens, x, st));
   }
   if (lv.layer_lo == lv.layer_hi) return TP_OK;
-  ::tp::count_launch(), rmsnorm_kernel<<<n, 256, 0, st>>>(x, d, c.norm_eps, e->Xd);
+  ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
   const SkPlan pqkv = sk_plan(q + 2 * kvd, d, n), po = sk_plan(d, q, n), pgu = sk_plan(2 * f, d, n),
                pdn = sk_plan(d, f, n);
-  const int span = kAttnChunk * kAttnSplitChunks;
-  const int splits = std::min(e->max_splits, (lv.max_t + span - 1) / span);
   AttnArgs aa;
   aa.q = e->Xq;
   aa.q_stride = q;
@@ -323,7 +355,7 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
   aa.pm = e->pm;
   aa.pl = e->pl;
   aa.po = e->po;
-  aa.max_splits = e->max_splits;
+  aa.max_chunks = e->max_splits;
   aa.out = e->Xo;
   aa.out_stride = q;
   for (int layer = lv.layer_lo; layer < lv.layer_hi; ++layer) {
@@ -336,15 +368,15 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
     TP_CUDA(cudaGetLastError());
     aa.k = kc;
     aa.v = vc;
-    TP_TRY(attn_tree(aa, lv, splits, st));
+    TP_TRY(attn_tree(aa, lv, st));
     TP_TRY(sk_gemm(&me->o[li], &e->mXo, po, e->part, st));
-    ::tp::count_launch(), resid_norm_kernel<<<n, 256, 0, st>>>(e->part, po, 1, x, d, c.norm_eps, e->Xd, 1);
+    ::tp::count_launch(), resid_norm_kernel<<<n, kNormThreads, 0, st>>>(e->part, po, 1, x, d, c.norm_eps, e->Xd, 1);
     TP_CUDA(cudaGetLastError());
     TP_TRY(sk_gemm(&me->gu[li], &e->mXd, pgu, e->part, st));
     ::tp::count_launch(), swiglu_kernel<<<dim3(n, (f + 255) / 256), 256, 0, st>>>(e->part, pgu, f, e->Xf);
     TP_CUDA(cudaGetLastError());
     TP_TRY(sk_gemm(&me->down[li], &e->mXf, pdn, e->part, st));
-    ::tp::count_launch(), resid_norm_kernel<<<n, 256, 0, st>>>(e->part, pdn, 1, x, d, c.norm_eps, e->Xd, layer + 1 < lv.layer_hi);
+    ::tp::count_launch(), resid_norm_kernel<<<n, kNormThreads, 0, st>>>(e->part, pdn, 1, x, d, c.norm_eps, e->Xd, layer + 1 < lv.layer_hi);
     TP_CUDA(cudaGetLastError());
   }
   return TP_OK;

@@ -144,6 +144,19 @@ def test_llama_batch_invariance_bitwise():
         assert torch.equal(outs[d], seq[d]), d
 
 
+def test_llama_stage_split_bitwise():
+    """Layers run as two stages (norm at the stage boundary) == one stage, bit for bit."""
+    cfg, m, _ = tiny_model(layers=4)
+    prompt = [int(t) for t in np.random.default_rng(2).integers(0, cfg.vocab, 77)]
+    whole = KvCache(cfg.layers, cfg.hidden).bind(m, (0, 4))
+    out_whole = tp.model.prefill_rows(m, whole, prompt, layer_range=(0, 4)).cpu()
+    a = KvCache(cfg.layers, cfg.hidden).bind(m, (0, 1))
+    b = KvCache(cfg.layers, cfg.hidden).bind(m, (1, 4))
+    mid = tp.model.prefill_rows(m, a, prompt, layer_range=(0, 1))
+    out_split = tp.model.prefill_rows(m, b, prompt, layer_range=(1, 4), x_in=mid).cpu()
+    assert torch.equal(out_whole, out_split)
+
+
 def test_llama_pipeline_lossless_and_margin_parity():
     cfg, m, o = tiny_model()
     prompt = [3, 1, 4, 1, 5, 9, 2, 6]

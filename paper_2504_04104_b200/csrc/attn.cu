@@ -25,6 +25,7 @@
 // used row-independently: other rows (other nodes or zeros) never change a
 // row's result.
 #include "attn.h"
+#include "gemm_tc.h"
 
 namespace tp {
 
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(AttnArgs a, Leve
 }
 
 __global__ void attn_combine_kernel(AttnArgs a, LevelDev lv) {
+  pdl_trigger();  // the O-projection GEMM may start streaming its weights
   const int i = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   int A = 0;
   for (int w = 0; w < lv.words; ++w) A += __popcll(lv.anc[(size_t)i * lv.words + w]);

@@ -1,24 +1,30 @@
-// K2: weight-streaming GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA), swap-AB.
+// K2: weight-streaming GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA), swap-AB,
+// with the split-K reduction and the layer's elementwise epilogue fused in.
 //
-//   out[node, j] = sum_k X[node, k] * W[j, k]       (W: [N_out, K] bf16, K-major)
+//   y[node, j] = sum_k X[node, k] * W[j, k]       (W: [N_out, K] bf16, K-major)
 //
 // A tree level has at most a few dozen nodes, so the *weights* are the MMA's
 // M operand (128-row tiles) and the nodes its N operand (n_pad = 16..256
-// columns): D^T[128 x n_pad] += W_tile[128 x 64] . X_tile[n_pad x 64]^T with the
+// columns): D^T[128 x n_pad] += W_tile[128 x 64] . X_tile[n_pad x 64]^T, the
 // accumulator in TMEM.  The kernel is HBM-bound (arithmetic intensity ~n_pad
-// FLOP/B), so the design goal is keeping every SM's TMA queue full:
-//   * stream-K decomposition: the m-tile x k-block space is cut into one
-//     contiguous range per CTA (grid = #SMs), so every SM streams the same
-//     number of weight bytes regardless of N_out / K;
-//   * warp-specialised: warp 0 = TMA producer (6-stage smem ring, weights
-//     evict-first, node rows evict-last), warp 1 = single-thread MMA issuer,
-//     warps 2-5 = epilogue draining TMEM (double-buffered accumulators so the
-//     MMA of the next m-tile segment overlaps the drain of the previous one);
-//   * partial tiles go to a [m_tile][contributor][node][128] fp32 buffer and
-//     the fused epilogue kernels (llama.cu) sum contributors in fixed order.
+// FLOP/B); the design goal is keeping every SM's TMA queue full:
+//   * stream-K: the m-tile x k-block space is cut into one contiguous range
+//     per CTA (grid = #SMs), so every SM streams the same weight bytes;
+//   * warp-specialised: warp 0 = TMA producer (weights evict-first, node rows
+//     evict-last), warp 1 = single-thread MMA issuer, warps 2-5 = epilogue
+//     (double-buffered TMEM accumulators: the next segment's MMAs overlap the
+//     previous segment's epilogue);
+//   * programmatic dependent launch: barrier init, TMEM allocation and the
+//     first ring-full of *weight* tiles are issued before griddepcontrol.wait,
+//     i.e. while the previous kernel is still finishing;
+//   * fused fix-up: an m-tile with several contributing CTAs has each write
+//     its fp32 partial; the last to arrive (atomic counter) sums all partials
+//     in contributor order and applies the epilogue op (RoPE + KV-row scatter,
+//     residual add, SwiGLU, or a plain store).  A sole contributor applies it
+//     straight from TMEM.
 // Determinism / batch invariance: segment boundaries depend only on
-// (N_out, K, #SMs), never on the node count, and each output column's
-// accumulation chain is the same for any n.
+// (N_out, K, #SMs); partials are summed in contributor order whichever CTA
+// arrives last; each output column's accumulation chain is the same for any n.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,6 +43,9 @@ constexpr int kBM = 128, kBK = 64;
 constexpr int kMaxStages = 8;
 constexpr int kThreads = 192;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+constexpr int kXchNodes = 32;           // epilogue exchange tile: 32 nodes x 128 features
+constexpr int kXchLd = 132;
+constexpr int kXchBytes = kXchNodes * kXchLd * 4;
 
 static int g_num_sms = 0;
 
@@ -92,26 +101,74 @@ SkPlan sk_plan(int n_out, int k, int n) {
 }
 
 static int stages_for(int n_pad) {
-  int per = kABytes + n_pad * 128;
-  return std::min(kMaxStages, (200 * 1024) / per);
+  const int per = kABytes + n_pad * 128;
+  return std::min(kMaxStages, (200 * 1024 - kXchBytes) / per);
 }
 
 static size_t smem_for(int n_pad) {
-  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + 1024 /*align*/ + 256 /*barriers*/;
+  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + 256 /*barriers*/;
 }
 
 // ---- device --------------------------------------------------------------------
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Apply the epilogue op to reduced values xch[cc][r] for nodes c0 .. c0+cn-1.
+__device__ __forceinline__ void apply_op(const GemmEpi& e, int mt, int r, int c0, int cn, const float* xch) {
+  for (int cc = 0; cc < cn; ++cc) {
+    const int c = c0 + cc;
+    const float y = xch[cc * kXchLd + r];
+    switch (e.op) {
+      case kOpStore:
+        e.out[(size_t)c * e.out_ld + mt * kBM + r] = y;
+        break;
+      case kOpResid:
+        e.out[(size_t)c * e.out_ld + mt * kBM + r] += y;
+        break;
+      case kOpSwiglu:
+        if (r < 64) {
+          const float g = y, u = xch[cc * kXchLd + r + 64];
+          const float a = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+          e.xf[(size_t)c * e.f + mt * 64 + r] = __float2bfloat16_rn(a);
+        }
+        break;
+      default: {  // kOpQkv: tile mt is head mt of [q heads | k heads | v heads]
+        float o = y;
+        if (mt < e.H + e.KV) {
+          const int i = r & 63;
+          const float cs = e.rope[((size_t)c * 64 + i) * 2], sn = e.rope[((size_t)c * 64 + i) * 2 + 1];
+          const float pr = xch[cc * kXchLd + (r ^ 64)];
+          o = r < 64 ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn));
+        }
+        __nv_bfloat16* dst;
+        if (mt < e.H) {
+          dst = e.xq + (size_t)c * e.H * kBM + mt * kBM;
+        } else {
+          const bool is_k = mt < e.H + e.KV;
+          const int kh = is_k ? mt - e.H : mt - e.H - e.KV;
+          if (e.append)
+            dst = (is_k ? e.kc : e.vc) + ((size_t)kh * e.cap + e.row0 + c) * kBM;
+          else
+            dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
+        }
+        dst[r] = __float2bfloat16_rn(o);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     sk_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SkPlan p,
-                   int stages, float* __restrict__ part) {
+                   int stages, GemmEpi e) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_last;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
   const int t0 = sk_begin(p, c), t1 = sk_begin(p, c + 1);
   const int bbytes = p.n_pad * 128;
   uint8_t* sA = smem;
   uint8_t* sB = smem + stages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + stages * bbytes);
+  float* xch = reinterpret_cast<float*>(sB + stages * bbytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + kXchBytes);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
@@ -142,10 +199,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&tmA);
       tma_prefetch(&tmB);
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
       const int nbox = p.n_pad / 16;
-      for (int t = t0; t < t1; ++t) {
+      // weights do not depend on the previous kernel: fill the ring now
+      const int npre = min(stages, t1 - t0);
+      for (int j = 0; j < npre; ++j) {
+        const int t = t0 + j;
+        mbar_expect_tx(&full[j], kABytes + bbytes);
+        tma_load_2d(sA + j * kABytes, &tmA, (t % p.KB) * kBK, (t / p.KB) * kBM, &full[j], pol_w);
+      }
+      pdl_wait();  // node rows X come from the previous kernel
+      pdl_trigger();
+      for (int j = 0; j < npre; ++j) {
+        const int kb = (t0 + j) % p.KB;
+        for (int b = 0; b < nbox; ++b)
+          tma_load_2d(sB + j * bbytes + b * 2048, &tmB, kb * kBK, b * 16, &full[j], pol_x);
+      }
+      int stage = npre % stages;
+      uint32_t phase = npre == stages ? 1 : 0;
+      for (int t = t0 + npre; t < t1; ++t) {
         const int mt = t / p.KB, kb = t % p.KB;
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_expect_tx(&full[stage], kABytes + bbytes);
@@ -192,28 +263,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3;  // TMEM lanes this warp may touch
-    const int row = quarter * 32 + lane;
+    const int r = quarter * 32 + lane;
+    const int et = threadIdx.x - 64;
     int seg = 0, t = t0;
     while (t < t1) {
       const int mt = t / p.KB;
       const int seg_end = min(t1, (mt + 1) * p.KB);
       const int buf = seg & 1;
       const uint32_t bphase = (seg >> 1) & 1;
+      const int cfirst = sk_cta_of(p, mt * p.KB);
+      const int cnt = sk_cta_of(p, (mt + 1) * p.KB - 1) - cfirst + 1;
       mbar_wait(&tfull[buf], bphase);
       tc_fence_after();
-      const int slot = c - sk_cta_of(p, mt * p.KB);
-      float* dst = part + ((size_t)(mt * p.max_contrib + slot) * p.n) * kBM + row;
       const uint32_t tbase = taddr + ((uint32_t)(quarter * 32) << 16) + buf * p.n_pad;
-      for (int col0 = 0; col0 < p.n; col0 += 16) {
-        float v[16];
-        tmem_ld_x16(tbase + col0, v);
+      bool last = true;
+      if (cnt > 1) {
+        float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * p.n) * kBM + r;
+        for (int col0 = 0; col0 < p.n_pad; col0 += 16) {
+          float v[16];
+          tmem_ld_x16(tbase + col0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (col0 + i < p.n) dst[(size_t)(col0 + i) * kBM] = v[i];
+          for (int i = 0; i < 16; ++i)
+            if (col0 + i < p.n) __stcg(dst + (size_t)(col0 + i) * kBM, v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
+        __threadfence();
+        epi_bar();
+        if (et == 0) s_last = atomicAdd(&e.counters[mt], 1) == cnt - 1;
+        epi_bar();
+        last = s_last;
+        if (last) __threadfence();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (last) {
+        const float* src = e.part + ((size_t)mt * p.max_contrib * p.n) * kBM + r;
+        const size_t slot = (size_t)p.n * kBM;
+        for (int c0 = 0; c0 < p.n; c0 += kXchNodes) {
+          const int cn = min(kXchNodes, p.n - c0);
+          if (cnt == 1) {
+            for (int col0 = c0; col0 < min(c0 + kXchNodes, p.n_pad); col0 += 16) {
+              float v[16];
+              tmem_ld_x16(tbase + col0, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (col0 + i < p.n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
+            }
+          } else {
+            for (int cc = 0; cc < cn; ++cc) {
+              const float* b = src + (size_t)(c0 + cc) * kBM;
+              float v[8];
+#pragma unroll
+              for (int s = 0; s < 8; ++s) v[s] = s < cnt ? __ldcg(b + s * slot) : 0.f;
+              float acc = v[0];
+#pragma unroll
+              for (int s = 1; s < 8; ++s)
+                if (s < cnt) acc += v[s];
+              for (int s = 8; s < cnt; ++s) acc += __ldcg(b + s * slot);
+              xch[cc * kXchLd + r] = acc;
+            }
+          }
+          epi_bar();
+          apply_op(e, mt, r, c0, cn, xch);
+          epi_bar();
+        }
+        if (cnt > 1 && et == 0) e.counters[mt] = 0;
+      }
+      if (cnt == 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      }
       t = seg_end;
       ++seg;
     }
@@ -236,8 +356,9 @@ static std::vector<ProfRec> g_prof;
 static bool g_prof_on = false;
 static std::mutex g_prof_mu;
 
-int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, float* part, cudaStream_t st) {
+int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st) {
   TP_CHECK(p.n >= 1 && p.n_pad <= 256, TP_ESHAPE, "GEMM node count outside [1, 256]");
+  TP_CHECK(epi.counters && epi.part, TP_ECONFIG, "GEMM epilogue needs partial + counter scratch");
   const int stages = stages_for(p.n_pad);
   const size_t smem = smem_for(p.n_pad);
   static size_t smem_set = 0;
@@ -252,19 +373,24 @@ int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, flo
     TP_CUDA(cudaEventRecord(rec.a, st));
     rec.bytes = (double)p.mtiles * kBM * p.KB * kBK * 2.0 + (double)p.n * p.KB * kBK * 2.0;
   }
-  ::tp::count_launch(), sk_gemm_kernel<<<p.G, kThreads, smem, st>>>(*tmA, *tmB, p, stages, part);
-  TP_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_prof_on ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ::tp::count_launch();
+  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, *tmA, *tmB, p, stages, epi));
   if (g_prof_on) {
     TP_CUDA(cudaEventRecord(rec.b, st));
     std::lock_guard<std::mutex> g(g_prof_mu);
     g_prof.push_back(rec);
   }
   return TP_OK;
-}
-
-__global__ void sk_reduce_kernel(const float* __restrict__ part, SkPlan p, int n_out, float* __restrict__ out) {
-  const int c = blockIdx.x, j = blockIdx.y * blockDim.x + threadIdx.x;
-  if (j < n_out) out[(size_t)c * n_out + j] = sk_sum(part, p, c, j);
 }
 
 }  // namespace tp
@@ -303,12 +429,16 @@ extern "C" int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_de
   TP_TRY(make_tmap_kmajor(&ma, w_dev, n_out, k, 128));
   TP_TRY(make_tmap_kmajor(&mb, x_dev, n, k, 16));
   SkPlan p = sk_plan(n_out, k, n);
-  float* part = nullptr;
-  TP_CUDA(cudaMallocAsync((void**)&part, sk_part_floats(p) * 4, st));
-  TP_TRY(sk_gemm(&ma, &mb, p, part, st));
-  ::tp::count_launch(), sk_reduce_kernel<<<dim3(n, (n_out + 255) / 256), 256, 0, st>>>(part, p, n_out, (float*)out_dev);
-  TP_CUDA(cudaGetLastError());
-  TP_CUDA(cudaFreeAsync(part, st));
+  GemmEpi e;
+  e.op = kOpStore;
+  e.out = (float*)out_dev;
+  e.out_ld = n_out;
+  TP_CUDA(cudaMallocAsync((void**)&e.part, sk_part_floats(p) * 4, st));
+  TP_CUDA(cudaMallocAsync((void**)&e.counters, p.mtiles * 4, st));
+  TP_CUDA(cudaMemsetAsync(e.counters, 0, p.mtiles * 4, st));
+  TP_TRY(sk_gemm(&ma, &mb, p, e, st));
+  TP_CUDA(cudaFreeAsync(e.part, st));
+  TP_CUDA(cudaFreeAsync(e.counters, st));
   TP_CUDA(cudaStreamSynchronize(st));
   return TP_OK;
 }

@@ -1,4 +1,4 @@
-// Stream-K tcgen05 GEMM plan + launcher (see gemm_tc.cu).
+// Stream-K tcgen05 GEMM plan, fused epilogues, launcher (see gemm_tc.cu).
 #pragma once
 
 #include <cuda.h>
@@ -22,29 +22,40 @@ __host__ __device__ inline int sk_cta_of(const SkPlan& p, int t) {
   return t < big ? t / (p.q + 1) : p.r + (t - big) / p.q;
 }
 
-// Sum of one output element over its contributors, in fixed order.  All
-// contributor loads are issued before the (ordered) adds so the reduction is
-// one L2 round trip, not max_contrib dependent ones.
-__device__ __forceinline__ float sk_sum(const float* __restrict__ part, const SkPlan& p, int node, int j) {
-  const int mt = j >> 7, r = j & 127;
-  const int cnt = sk_cta_of(p, (mt + 1) * p.KB - 1) - sk_cta_of(p, mt * p.KB) + 1;
-  const float* b = part + ((size_t)mt * p.max_contrib * p.n + node) * 128 + r;
-  const size_t stride = (size_t)p.n * 128;
-  float v[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) v[s] = s < cnt ? __ldcg(b + s * stride) : 0.f;
-  float acc = v[0];
-#pragma unroll
-  for (int s = 1; s < 8; ++s)
-    if (s < cnt) acc += v[s];
-  for (int s = 8; s < cnt; ++s) acc += __ldcg(b + s * stride);
-  return acc;
-}
+// Epilogue applied (inside the GEMM) to the fully reduced 128-feature m-tile.
+enum GemmOp : int {
+  kOpStore = 0,   // out[node * out_ld + j] = y
+  kOpQkv = 1,     // RoPE(q, k) + scatter: q -> xq, k/v -> KV cache rows (or self buffers)
+  kOpResid = 2,   // out[node * out_ld + j] += y   (fp32 residual stream)
+  kOpSwiglu = 3,  // tile = 64 gate rows | 64 up rows: xf[node][mt*64 + i] = bf16(silu(g) * u)
+};
+
+struct GemmEpi {
+  int op = kOpStore;
+  float* out = nullptr;
+  int out_ld = 0;
+  // kOpQkv
+  int H = 0, KV = 0, cap = 0, row0 = 0, append = 0;
+  const float* rope = nullptr;  // [n][64][2] (cos, sin) per node position
+  __nv_bfloat16 *xq = nullptr, *kc = nullptr, *vc = nullptr, *kself = nullptr, *vself = nullptr;
+  // kOpSwiglu
+  __nv_bfloat16* xf = nullptr;
+  int f = 0;
+  // stream-K fix-up state
+  float* part = nullptr;  // [mtiles][max_contrib][n][128]
+  int* counters = nullptr;  // [mtiles], zero between launches (self-resetting)
+};
 
 int num_sms();
 int make_tmap_kmajor(CUtensorMap* map, const void* gptr, int64_t rows, int64_t k, int box_rows);
 SkPlan sk_plan(int n_out, int k, int n);
 inline size_t sk_part_floats(const SkPlan& p) { return (size_t)p.mtiles * p.max_contrib * p.n * 128; }
-int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, float* part, cudaStream_t st);
+// Launched with programmatic dependent launch: the weight prologue overlaps the
+// previous kernel; activations are read only after griddepcontrol.wait.
+int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st);
+
+// Let the next (PDL-launched) GEMM start its weight prologue now.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 }  // namespace tp

@@ -3,13 +3,16 @@
 // Per layer (reference layer_step structure, `/root/reference/pkg/src/treepipe/
 // model.py:250-280`, with the Llama block: RMSNorm, RoPE, GQA, SwiGLU):
 //
-//   [rmsnorm x -> Xd]                           (fused into the previous epilogue)
-//   QKV  = Xd . Wqkv^T      K2 tcgen05 stream-K   -> qkv_epilogue: RoPE(q,k), q->Xq,
-//                                                    k,v -> KV rows (appended in place)
-//   attn = tree-attention(Xq, KV, ancestor bits)  K1 (attn.cu)          -> Xo
-//   x   += Xo . Wo^T        K2                    -> resid_norm: x += ., Xd = rmsnorm(x)
-//   GU   = Xd . Wgu^T       K2 (gate/up 64-row interleave)  -> swiglu: Xf = silu(g)*u
-//   x   += Xf . Wdown^T     K2                    -> resid_norm
+//   QKV  = Xd . Wqkv^T      K2 (epilogue: RoPE(q,k); q -> Xq; k,v -> KV rows in place)
+//   attn = tree-attention(Xq, KV, ancestor bits)      K1 (attn.cu)      -> Xo
+//   x   += Xo . Wo^T        K2 (epilogue: residual add)
+//   Xd   = rmsnorm(x)
+//   Xf   = silu(G) * U      K2 over the gate/up weights (64-row interleave; epilogue: SwiGLU)
+//   x   += Xf . Wdown^T     K2 (epilogue: residual add)
+//   Xd   = rmsnorm(x)                                   (input of the next layer)
+//
+// 9 launches per layer; every GEMM is a programmatic-dependent launch whose
+// weight prologue overlaps the preceding kernel.
 //
 // Numerics (mirrored by oracle/llama.py): GEMM inputs bf16, accumulation and
 // residual fp32; RoPE (HF rotate-half, angle in fp64) on the fp32 GEMM
@@ -23,6 +26,8 @@
 
 namespace tp {
 
+enum { kCtrQkv = 0, kCtrO, kCtrGu, kCtrDown, kCtrHead, kCtrKinds };
+
 struct LlamaModelExt {
   std::vector<CUtensorMap> qkv, o, gu, down;
   CUtensorMap head;
@@ -34,9 +39,12 @@ struct LlamaStageExt {
   __nv_bfloat16 *kself = nullptr, *vself = nullptr;
   float* part = nullptr;
   size_t part_floats = 0;
+  int* counters = nullptr;  // [kCtrKinds][ctr_stride]
+  int ctr_stride = 0;
+  float* rope = nullptr;  // [np][64][2]
   CUtensorMap mXd, mXo, mXf;
   float *pm = nullptr, *pl = nullptr, *po = nullptr;
-  int max_splits = 0;
+  int max_chunks = 0;
 };
 
 static LlamaModelExt* mext(tp_model* m) { return reinterpret_cast<LlamaModelExt*>(m->tma_cache); }
@@ -70,86 +78,11 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// x[c] (+= GEMM result) ; Xd[c] = bf16(x * 1/sqrt(mean(x^2) + eps)).  One CTA per
-// node row; every element's contributor loads are in flight at once.
-__global__ void __launch_bounds__(kNormThreads) resid_norm_kernel(const float* __restrict__ part, SkPlan p,
-                                                                  int add, float* __restrict__ x, int d,
-                                                                  float eps, __nv_bfloat16* __restrict__ xd,
-                                                                  int do_norm) {
-  __shared__ float red[33];
-  const int c = blockIdx.x;
-  float* xr = x + (size_t)c * d;
-  float v[kNormPer];
-#pragma unroll
-  for (int u = 0; u < kNormPer; ++u) {
-    const int j = threadIdx.x + u * kNormThreads;
-    v[u] = j < d ? xr[j] + (add ? sk_sum(part, p, c, j) : 0.f) : 0.f;
-  }
-  float ss = 0.f;
-#pragma unroll
-  for (int u = 0; u < kNormPer; ++u) {
-    const int j = threadIdx.x + u * kNormThreads;
-    if (j < d) {
-      xr[j] = v[u];
-      ss += v[u] * v[u];
-    }
-  }
-  if (!do_norm) return;
-  ss = block_sum(ss, red);
-  const float r = 1.0f / sqrtf(ss / (float)d + eps);
-#pragma unroll
-  for (int u = 0; u < kNormPer; ++u) {
-    const int j = threadIdx.x + u * kNormThreads;
-    if (j < d) xd[(size_t)c * d + j] = __float2bfloat16_rn(v[u] * r);
-  }
-}
-
-// RoPE on q/k heads (rotate-half pairs (i, i+64)), scatter q -> Xq, k/v -> cache rows.
-__global__ void qkv_epilogue_kernel(const float* __restrict__ part, SkPlan p, LevelDev lv, int H, int KV,
-                                    double theta, __nv_bfloat16* __restrict__ xq, __nv_bfloat16* __restrict__ kc,
-                                    __nv_bfloat16* __restrict__ vc, int cap, __nv_bfloat16* __restrict__ kself,
-                                    __nv_bfloat16* __restrict__ vself) {
-  const int c = blockIdx.x, hh = blockIdx.y, i = threadIdx.x;  // i in [0, 64)
-  const int j0 = hh * 128;
-  const float y1 = sk_sum(part, p, c, j0 + i), y2 = sk_sum(part, p, c, j0 + i + 64);
-  float o1 = y1, o2 = y2;
-  if (hh < H + KV) {
-    const double inv = pow(theta, -2.0 * (double)i / 128.0);
-    double sn, cs;
-    sincos((double)lv.positions[c] * inv, &sn, &cs);
-    const float cf = (float)cs, sf = (float)sn;
-    o1 = __fsub_rn(__fmul_rn(y1, cf), __fmul_rn(y2, sf));
-    o2 = __fadd_rn(__fmul_rn(y2, cf), __fmul_rn(y1, sf));
-  }
-  __nv_bfloat16* dst;
-  if (hh < H) {
-    dst = xq + (size_t)c * H * 128 + hh * 128;
-  } else {
-    const bool is_k = hh < H + KV;
-    const int kh = is_k ? hh - H : hh - H - KV;
-    if (lv.append)
-      dst = (is_k ? kc : vc) + ((size_t)kh * cap + lv.row0 + c) * 128;
-    else
-      dst = (is_k ? kself : vself) + ((size_t)c * KV + kh) * 128;
-  }
-  dst[i] = __float2bfloat16_rn(o1);
-  dst[i + 64] = __float2bfloat16_rn(o2);
-}
-
-__global__ void swiglu_kernel(const float* __restrict__ part, SkPlan p, int f, __nv_bfloat16* __restrict__ xf) {
-  const int c = blockIdx.x, fi = blockIdx.y * blockDim.x + threadIdx.x;
-  if (fi >= f) return;
-  const int rg = (fi >> 6) * 128 + (fi & 63);
-  const float g = sk_sum(part, p, c, rg), u = sk_sum(part, p, c, rg + 64);
-  const float a = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
-  xf[(size_t)c * f + fi] = __float2bfloat16_rn(a);
-}
-
-// Stand-alone RMSNorm with exactly resid_norm_kernel's reduction shape, so a
-// norm computed at a stage boundary is bit-identical to the fused one a
-// single-stage model computes at the same layer boundary.
+// Xd[c] = bf16(x[c] * 1/sqrt(mean(x[c]^2) + eps)); one CTA per node row, the
+// same reduction shape at every call site (stage boundaries included).
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
                                                                __nv_bfloat16* __restrict__ xd) {
+  pdl_trigger();  // the following GEMM may start streaming its weights
   __shared__ float red[33];
   const float* xr = x + (size_t)blockIdx.x * d;
   float v[kNormPer];
@@ -173,9 +106,14 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __re
   }
 }
 
-__global__ void logits_kernel(const float* __restrict__ part, SkPlan p, int V, float* __restrict__ out) {
-  const int c = blockIdx.x, v = blockIdx.y * blockDim.x + threadIdx.x;
-  if (v < V) out[(size_t)c * V + v] = sk_sum(part, p, c, v);
+// cos/sin of every (node position, rotary pair) for the QKV epilogue; angle in fp64.
+__global__ void rope_table_kernel(const int32_t* __restrict__ pos, double theta, float* __restrict__ out) {
+  const int c = blockIdx.x, i = threadIdx.x;  // i in [0, 64)
+  const double inv = pow(theta, -2.0 * (double)i / 128.0);
+  double sn, cs;
+  sincos((double)pos[c] * inv, &sn, &cs);
+  out[((size_t)c * 64 + i) * 2] = (float)cs;
+  out[((size_t)c * 64 + i) * 2 + 1] = (float)sn;
 }
 
 // ---- host ---------------------------------------------------------------------------
@@ -248,8 +186,7 @@ int llama_stage_init(tp_stage* s) {
   const tp_model_config& c = m->cfg;
   TP_TRY(build_model_ext(m));
   LlamaStageExt* e = sext(s);
-  const bool fresh = e == nullptr;
-  if (fresh) {
+  if (e == nullptr) {
     e = new LlamaStageExt();
     s->ext = e;
     const int64_t d = c.hidden, q = (int64_t)c.heads * 128, kv = (int64_t)c.kv_heads * 128, f = c.ffn;
@@ -261,25 +198,35 @@ int llama_stage_init(tp_stage* s) {
     TP_CUDA(cudaMalloc(&e->Xq, np * q * 2));
     TP_CUDA(cudaMalloc(&e->kself, np * kv * 2));
     TP_CUDA(cudaMalloc(&e->vself, np * kv * 2));
+    TP_CUDA(cudaMalloc(&e->rope, np * 64 * 2 * 4));
     TP_CUDA(cudaMemset(e->Xd, 0, np * d * 2));
     TP_CUDA(cudaMemset(e->Xo, 0, np * q * 2));
     TP_CUDA(cudaMemset(e->Xf, 0, np * f * 2));
     size_t pf = 0;
+    int mt = 1;
     const int nmax = c.max_nodes;
-    pf = std::max(pf, sk_part_floats(sk_plan((int)(q + 2 * kv), (int)d, nmax)));
-    pf = std::max(pf, sk_part_floats(sk_plan((int)d, (int)q, nmax)));
-    pf = std::max(pf, sk_part_floats(sk_plan((int)(2 * f), (int)d, nmax)));
-    pf = std::max(pf, sk_part_floats(sk_plan((int)d, (int)f, nmax)));
-    if (m->head) pf = std::max(pf, sk_part_floats(sk_plan(c.vocab, (int)d, nmax)));
+    for (SkPlan p : {sk_plan((int)(q + 2 * kv), (int)d, nmax), sk_plan((int)d, (int)q, nmax),
+                     sk_plan((int)(2 * f), (int)d, nmax), sk_plan((int)d, (int)f, nmax)}) {
+      pf = std::max(pf, sk_part_floats(p));
+      mt = std::max(mt, p.mtiles);
+    }
+    if (m->head) {
+      SkPlan ph = sk_plan(c.vocab, (int)d, nmax);
+      pf = std::max(pf, sk_part_floats(ph));
+      mt = std::max(mt, ph.mtiles);
+    }
     e->part_floats = pf;
     TP_CUDA(cudaMalloc(&e->part, pf * 4));
+    e->ctr_stride = mt;
+    TP_CUDA(cudaMalloc(&e->counters, (size_t)kCtrKinds * mt * 4));
+    TP_CUDA(cudaMemset(e->counters, 0, (size_t)kCtrKinds * mt * 4));
     TP_TRY(make_tmap_kmajor(&e->mXd, e->Xd, np, d, 16));
     TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
     TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));
   }
   // attention chunk partials follow the KV capacity (+ ancestors + self)
   const int chunks = (s->cap + kAttnMaxExtra + 1 + kAttnChunk - 1) / kAttnChunk;
-  if (chunks > e->max_splits) {
+  if (chunks > e->max_chunks) {
     if (e->pm) cudaFree(e->pm);
     if (e->pl) cudaFree(e->pl);
     if (e->po) cudaFree(e->po);
@@ -287,7 +234,7 @@ int llama_stage_init(tp_stage* s) {
     TP_CUDA(cudaMalloc(&e->pm, cells * 4));
     TP_CUDA(cudaMalloc(&e->pl, cells * 4));
     TP_CUDA(cudaMalloc(&e->po, cells * 128 * 4));
-    e->max_splits = chunks;
+    e->max_chunks = chunks;
   }
   return TP_OK;
 }
@@ -296,7 +243,7 @@ void llama_stage_free(tp_stage* s) {
   LlamaStageExt* e = sext(s);
   if (!e) return;
   for (void* p : {(void*)e->Xd, (void*)e->Xo, (void*)e->Xf, (void*)e->Xq, (void*)e->kself, (void*)e->vself,
-                  (void*)e->part, (void*)e->pm, (void*)e->pl, (void*)e->po})
+                  (void*)e->part, (void*)e->counters, (void*)e->rope, (void*)e->pm, (void*)e->pl, (void*)e->po})
     if (p) cudaFree(p);
   delete e;
   s->ext = nullptr;
@@ -304,9 +251,17 @@ void llama_stage_free(tp_stage* s) {
 
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st) {
   TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
-  ::tp::count_launch(), llama_embed_kernel<<<n, 256, 0, st>>>((const __nv_bfloat16*)m->embed, d_tokens, m->cfg.hidden, out);
+  ::tp::count_launch(), llama_embed_kernel<<<n, 256, 0, st>>>((const __nv_bfloat16*)m->embed, d_tokens,
+                                                              m->cfg.hidden, out);
   TP_CUDA(cudaGetLastError());
   return TP_OK;
+}
+
+static GemmEpi epi_base(LlamaStageExt* e, int kind) {
+  GemmEpi g;
+  g.part = e->part;
+  g.counters = e->counters + (size_t)kind * e->ctr_stride;
+  return g;
 }
 
 int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st) {
@@ -316,11 +271,11 @@ int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits
   const int d = m->cfg.hidden, V = m->cfg.vocab;
   ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
-  const SkPlan ph = sk_plan(V, d, n);
-  TP_TRY(sk_gemm(&mext(m)->head, &e->mXd, ph, e->part, st));
-  ::tp::count_launch(), logits_kernel<<<dim3(n, (V + 255) / 256), 256, 0, st>>>(e->part, ph, V, logits);
-  TP_CUDA(cudaGetLastError());
-  return TP_OK;
+  GemmEpi g = epi_base(e, kCtrHead);
+  g.op = kOpStore;
+  g.out = logits;
+  g.out_ld = V;
+  return sk_gemm(&mext(m)->head, &e->mXd, sk_plan(V, d, n), g, st);
 }
 
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
@@ -339,6 +294,8 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
     TP_TRY(llama_embed(m, n, lv.tokens, x, st));
   }
   if (lv.layer_lo == lv.layer_hi) return TP_OK;
+  ::tp::count_launch(), rope_table_kernel<<<n, 64, 0, st>>>(lv.positions, (double)c.rope_theta, e->rope);
+  TP_CUDA(cudaGetLastError());
   ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
   const SkPlan pqkv = sk_plan(q + 2 * kvd, d, n), po = sk_plan(d, q, n), pgu = sk_plan(2 * f, d, n),
@@ -355,29 +312,47 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
   aa.pm = e->pm;
   aa.pl = e->pl;
   aa.po = e->po;
-  aa.max_chunks = e->max_splits;
+  aa.max_chunks = e->max_chunks;
   aa.out = e->Xo;
   aa.out_stride = q;
+  GemmEpi gq = epi_base(e, kCtrQkv);
+  gq.op = kOpQkv;
+  gq.H = H;
+  gq.KV = KV;
+  gq.cap = s->cap;
+  gq.row0 = lv.row0;
+  gq.append = lv.append;
+  gq.rope = e->rope;
+  gq.xq = e->Xq;
+  gq.kself = e->kself;
+  gq.vself = e->vself;
+  GemmEpi gr = epi_base(e, kCtrO);
+  gr.op = kOpResid;
+  gr.out = x;
+  gr.out_ld = d;
+  GemmEpi gd = gr;
+  gd.counters = e->counters + (size_t)kCtrDown * e->ctr_stride;
+  GemmEpi gg = epi_base(e, kCtrGu);
+  gg.op = kOpSwiglu;
+  gg.xf = e->Xf;
+  gg.f = f;
   for (int layer = lv.layer_lo; layer < lv.layer_hi; ++layer) {
     const int li = layer - c.layer_lo;
-    __nv_bfloat16* kc = (__nv_bfloat16*)s->k[layer - s->lo];
-    __nv_bfloat16* vc = (__nv_bfloat16*)s->v[layer - s->lo];
-    TP_TRY(sk_gemm(&me->qkv[li], &e->mXd, pqkv, e->part, st));
-    ::tp::count_launch(), qkv_epilogue_kernel<<<dim3(n, H + 2 * KV), 64, 0, st>>>(e->part, pqkv, lv, H, KV, (double)c.rope_theta, e->Xq,
-                                                            kc, vc, s->cap, e->kself, e->vself);
-    TP_CUDA(cudaGetLastError());
-    aa.k = kc;
-    aa.v = vc;
+    gq.kc = (__nv_bfloat16*)s->k[layer - s->lo];
+    gq.vc = (__nv_bfloat16*)s->v[layer - s->lo];
+    TP_TRY(sk_gemm(&me->qkv[li], &e->mXd, pqkv, gq, st));
+    aa.k = gq.kc;
+    aa.v = gq.vc;
     TP_TRY(attn_tree(aa, lv, st));
-    TP_TRY(sk_gemm(&me->o[li], &e->mXo, po, e->part, st));
-    ::tp::count_launch(), resid_norm_kernel<<<n, kNormThreads, 0, st>>>(e->part, po, 1, x, d, c.norm_eps, e->Xd, 1);
+    TP_TRY(sk_gemm(&me->o[li], &e->mXo, po, gr, st));
+    ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
     TP_CUDA(cudaGetLastError());
-    TP_TRY(sk_gemm(&me->gu[li], &e->mXd, pgu, e->part, st));
-    ::tp::count_launch(), swiglu_kernel<<<dim3(n, (f + 255) / 256), 256, 0, st>>>(e->part, pgu, f, e->Xf);
-    TP_CUDA(cudaGetLastError());
-    TP_TRY(sk_gemm(&me->down[li], &e->mXf, pdn, e->part, st));
-    ::tp::count_launch(), resid_norm_kernel<<<n, kNormThreads, 0, st>>>(e->part, pdn, 1, x, d, c.norm_eps, e->Xd, layer + 1 < lv.layer_hi);
-    TP_CUDA(cudaGetLastError());
+    TP_TRY(sk_gemm(&me->gu[li], &e->mXd, pgu, gg, st));
+    TP_TRY(sk_gemm(&me->down[li], &e->mXf, pdn, gd, st));
+    if (layer + 1 < lv.layer_hi) {
+      ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
+      TP_CUDA(cudaGetLastError());
+    }
   }
   return TP_OK;
 }

@@ -140,6 +140,10 @@ int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* launches);
  * out[n][n_out] (f32, dev) = x[n][k] (bf16, dev) . w[n_out][k]^T (bf16, dev).   */
 int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out, int32_t k,
                   void* out_dev, void* stream);
+/* The same GEMM launched `iters` times back to back (programmatic dependent
+ * launch between them); *ms_per_launch = CUDA-event time / iters.            */
+int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out, int32_t k,
+                        void* out_dev, int32_t iters, float* ms_per_launch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,7 @@ _SIGS = {
     "tp_stage_read_kv": (C.c_int, [_P, _I, _I, _I, _I, _P]),
     "tp_rows_compact": (C.c_int, [_P, _P, _P, C.c_int64, _I, _P, C.POINTER(C.c_int32), _P]),
     "tp_debug_gemm": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _P]),
+    "tp_debug_gemm_timed": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _I, _P, _P]),
     "tp_launch_count": (C.c_int, [C.POINTER(C.c_int64)]),
     "tp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tp_profile_enable": (C.c_int, [_I]),

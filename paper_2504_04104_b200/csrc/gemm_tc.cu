@@ -18,13 +18,16 @@
 //     first ring-full of *weight* tiles are issued before griddepcontrol.wait,
 //     i.e. while the previous kernel is still finishing;
 //   * fused fix-up: an m-tile with several contributing CTAs has each write
-//     its fp32 partial; the last to arrive (atomic counter) sums all partials
-//     in contributor order and applies the epilogue op (RoPE + KV-row scatter,
-//     residual add, SwiGLU, or a plain store).  A sole contributor applies it
-//     straight from TMEM.
+//     its fp32 partial; the contributors whose ranges *end* inside the tile
+//     (they finish together at the end of the kernel) wait for the tile's
+//     arrival counter, then each reduces a slice of the nodes in contributor
+//     order and applies the epilogue op (RoPE + KV-row scatter, residual add,
+//     SwiGLU, or a plain store).  A sole contributor applies it straight from
+//     TMEM.  The epilogue runs one warp per node row (lane = 4 features, the
+//     RoPE / SwiGLU partner feature is lane^16), two rows in flight per warp.
 // Determinism / batch invariance: segment boundaries depend only on
 // (N_out, K, #SMs); partials are summed in contributor order whichever CTA
-// arrives last; each output column's accumulation chain is the same for any n.
+// reduces them; each output column's accumulation chain is the same for any n.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -112,55 +115,154 @@ static size_t smem_for(int n_pad) {
 // ---- device --------------------------------------------------------------------
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// Apply the epilogue op to reduced values xch[cc][r] for nodes c0 .. c0+cn-1.
-__device__ __forceinline__ void apply_op(const GemmEpi& e, int mt, int r, int c0, int cn, const float* xch) {
-  for (int cc = 0; cc < cn; ++cc) {
-    const int c = c0 + cc;
-    const float y = xch[cc * kXchLd + r];
-    switch (e.op) {
-      case kOpStore:
-        e.out[(size_t)c * e.out_ld + mt * kBM + r] = y;
-        break;
-      case kOpResid:
-        e.out[(size_t)c * e.out_ld + mt * kBM + r] += y;
-        break;
-      case kOpSwiglu:
-        if (r < 64) {
-          const float g = y, u = xch[cc * kXchLd + r + 64];
-          const float a = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
-          e.xf[(size_t)c * e.f + mt * 64 + r] = __float2bfloat16_rn(a);
-        }
-        break;
-      default: {  // kOpQkv: tile mt is head mt of [q heads | k heads | v heads]
-        float o = y;
-        if (mt < e.H + e.KV) {
-          const int i = r & 63;
-          const float cs = e.rope[((size_t)c * 64 + i) * 2], sn = e.rope[((size_t)c * 64 + i) * 2 + 1];
-          const float pr = xch[cc * kXchLd + (r ^ 64)];
-          o = r < 64 ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn));
-        }
-        __nv_bfloat16* dst;
-        if (mt < e.H) {
-          dst = e.xq + (size_t)c * e.H * kBM + mt * kBM;
-        } else {
-          const bool is_k = mt < e.H + e.KV;
-          const int kh = is_k ? mt - e.H : mt - e.H - e.KV;
-          if (e.append)
-            dst = (is_k ? e.kc : e.vc) + ((size_t)kh * e.cap + e.row0 + c) * kBM;
-          else
-            dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
-        }
-        dst[r] = __float2bfloat16_rn(o);
+// ---- epilogue: one warp per node row, lane l owns features 4l..4l+3 of the m-tile.
+// RoPE pairs feature r with r^64 and SwiGLU gate r with up r+64: both are lane^16.
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4cg(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
+  return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                     __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+__device__ __forceinline__ void st_bf16x4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  uint2 u;
+  u.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+  u.y = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(c)) |
+        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d)) << 16);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+// Operands the op reads besides y (issued for a batch of nodes before any store).
+struct EpiAux {
+  float4 a, b;
+};
+
+__device__ __forceinline__ void epi_aux(const GemmEpi& e, int mt, int f, int c, EpiAux& x) {
+  if (e.op == kOpResid) {
+    x.a = ld4(e.out + (size_t)c * e.out_ld + mt * kBM + f);
+  } else if (e.op == kOpQkv && mt < e.H + e.KV) {
+    const float* p = e.rope + ((size_t)c * 64 + (f & 63)) * 2;  // (cos, sin) x 4 rotary pairs
+    x.a = ld4(p);
+    x.b = ld4(p + 4);
+  }
+}
+
+__device__ __forceinline__ float rope1(float y, float pr, float cs, float sn, bool lo) {
+  return lo ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn));
+}
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  return __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+}
+
+// Warp-uniform: every lane of the warp calls this for the same node c.
+__device__ __forceinline__ void epi_finish(const GemmEpi& e, int mt, int lane, int c, float4 y, const EpiAux& x) {
+  const int f = lane * 4;
+  switch (e.op) {
+    case kOpStore:
+      st4(e.out + (size_t)c * e.out_ld + mt * kBM + f, y);
+      break;
+    case kOpResid:
+      st4(e.out + (size_t)c * e.out_ld + mt * kBM + f, add4(x.a, y));
+      break;
+    case kOpSwiglu: {
+      const float4 u = shfl_xor4(y, 16);
+      if (lane < 16)
+        st_bf16x4(e.xf + (size_t)c * e.f + mt * 64 + f, silu_mul(y.x, u.x), silu_mul(y.y, u.y), silu_mul(y.z, u.z),
+                  silu_mul(y.w, u.w));
+      break;
+    }
+    default: {  // kOpQkv: tile mt is head mt of [q heads | k heads | v heads]
+      const float4 pr = shfl_xor4(y, 16);
+      float4 o = y;
+      if (mt < e.H + e.KV) {
+        const bool lo = lane < 16;
+        o.x = rope1(y.x, pr.x, x.a.x, x.a.y, lo);
+        o.y = rope1(y.y, pr.y, x.a.z, x.a.w, lo);
+        o.z = rope1(y.z, pr.z, x.b.x, x.b.y, lo);
+        o.w = rope1(y.w, pr.w, x.b.z, x.b.w, lo);
       }
+      __nv_bfloat16* dst;
+      if (mt < e.H) {
+        dst = e.xq + (size_t)c * e.H * kBM + mt * kBM;
+      } else {
+        const bool is_k = mt < e.H + e.KV;
+        const int kh = is_k ? mt - e.H : mt - e.H - e.KV;
+        if (e.append)
+          dst = (is_k ? e.kc : e.vc) + ((size_t)kh * e.cap + e.row0 + c) * kBM;
+        else
+          dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
+      }
+      st_bf16x4(dst + f, o.x, o.y, o.z, o.w);
     }
   }
+}
+
+// Sum of the m-tile's cnt partials for node c, in contributor order (the order
+// fixes the rounding: identical whichever CTA reduces and for any node count).
+__device__ __forceinline__ float4 sum_partials(const float* base, size_t slot, int cnt, int c, int f) {
+  const float* b = base + (size_t)c * kBM + f;
+  float4 v[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = s < cnt ? ld4cg(b + s * slot) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = v[0];
+#pragma unroll
+  for (int s = 1; s < 8; ++s)
+    if (s < cnt) acc = add4(acc, v[s]);
+  for (int s = 8; s < cnt; ++s) acc = add4(acc, ld4cg(b + s * slot));
+  return acc;
+}
+
+// Reduce + apply nodes [lo, hi) of m-tile mt from the global partials; the 4
+// epilogue warps take nodes round-robin, two per warp in flight.
+__device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int mt, int cnt, int lo, int hi,
+                                             int ew, int lane) {
+  const float* base = e.part + (size_t)mt * p.max_contrib * p.n * kBM;
+  const size_t slot = (size_t)p.n * kBM;
+  const int f = lane * 4;
+  for (int c = lo + ew; c < hi; c += 8) {
+    const int c2 = c + 4;
+    const bool two = c2 < hi;
+    const float4 y0 = sum_partials(base, slot, cnt, c, f);
+    const float4 y1 = two ? sum_partials(base, slot, cnt, c2, f) : y0;
+    EpiAux x0{}, x1{};
+    epi_aux(e, mt, f, c, x0);
+    if (two) epi_aux(e, mt, f, c2, x1);
+    epi_finish(e, mt, lane, c, y0, x0);
+    if (two) epi_finish(e, mt, lane, c2, y1, x1);
+  }
+}
+
+// Apply nodes c0 .. c0+cn-1 staged in xch[node][feature] (sole-contributor path).
+__device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int cn, const float* xch, int ew,
+                                           int lane) {
+  const int f = lane * 4;
+  for (int cc = ew; cc < cn; cc += 8) {
+    const int cc2 = cc + 4;
+    const bool two = cc2 < cn;
+    const float4 y0 = *reinterpret_cast<const float4*>(xch + cc * kXchLd + f);
+    const float4 y1 = two ? *reinterpret_cast<const float4*>(xch + cc2 * kXchLd + f) : y0;
+    EpiAux x0{}, x1{};
+    epi_aux(e, mt, f, c0 + cc, x0);
+    if (two) epi_aux(e, mt, f, c0 + cc2, x1);
+    epi_finish(e, mt, lane, c0 + cc, y0, x0);
+    if (two) epi_finish(e, mt, lane, c0 + cc2, y1, x1);
+  }
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     sk_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SkPlan p,
                    int stages, GemmEpi e) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ int s_last;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
   const int t0 = sk_begin(p, c), t1 = sk_begin(p, c + 1);
@@ -264,7 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int quarter = warp & 3;  // TMEM lanes this warp may touch
     const int r = quarter * 32 + lane;
+    const int ew = warp - 2;  // epilogue warp 0..3 (node-parallel phases)
     const int et = threadIdx.x - 64;
+    int* arrive = e.counters;
+    int* done = e.counters + p.mtiles;
     int seg = 0, t = t0;
     while (t < t1) {
       const int mt = t / p.KB;
@@ -272,12 +377,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = seg & 1;
       const uint32_t bphase = (seg >> 1) & 1;
       const int cfirst = sk_cta_of(p, mt * p.KB);
-      const int cnt = sk_cta_of(p, (mt + 1) * p.KB - 1) - cfirst + 1;
+      const int clast = sk_cta_of(p, (mt + 1) * p.KB - 1);
+      const int cnt = clast - cfirst + 1;
       mbar_wait(&tfull[buf], bphase);
       tc_fence_after();
       const uint32_t tbase = taddr + ((uint32_t)(quarter * 32) << 16) + buf * p.n_pad;
-      bool last = true;
-      if (cnt > 1) {
+      if (cnt == 1) {
+        for (int c0 = 0; c0 < p.n; c0 += kXchNodes) {
+          const int cn = min(kXchNodes, p.n - c0);
+          for (int col0 = c0; col0 < min(c0 + kXchNodes, p.n_pad); col0 += 16) {
+            float v[16];
+            tmem_ld_x16(tbase + col0, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (col0 + i < p.n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
+          }
+          epi_bar();
+          smem_apply(e, mt, c0, cn, xch, ew, lane);
+          epi_bar();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      } else {
+        // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
         float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * p.n) * kBM + r;
         for (int col0 = 0; col0 < p.n_pad; col0 += 16) {
           float v[16];
@@ -291,48 +414,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
         __threadfence();
         epi_bar();
-        if (et == 0) s_last = atomicAdd(&e.counters[mt], 1) == cnt - 1;
-        epi_bar();
-        last = s_last;
-        if (last) __threadfence();
-      }
-      if (last) {
-        const float* src = e.part + ((size_t)mt * p.max_contrib * p.n) * kBM + r;
-        const size_t slot = (size_t)p.n * kBM;
-        for (int c0 = 0; c0 < p.n; c0 += kXchNodes) {
-          const int cn = min(kXchNodes, p.n - c0);
-          if (cnt == 1) {
-            for (int col0 = c0; col0 < min(c0 + kXchNodes, p.n_pad); col0 += 16) {
-              float v[16];
-              tmem_ld_x16(tbase + col0, v);
-#pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (col0 + i < p.n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
-            }
-          } else {
-            for (int cc = 0; cc < cn; ++cc) {
-              const float* b = src + (size_t)(c0 + cc) * kBM;
-              float v[8];
-#pragma unroll
-              for (int s = 0; s < 8; ++s) v[s] = s < cnt ? __ldcg(b + s * slot) : 0.f;
-              float acc = v[0];
-#pragma unroll
-              for (int s = 1; s < 8; ++s)
-                if (s < cnt) acc += v[s];
-              for (int s = 8; s < cnt; ++s) acc += __ldcg(b + s * slot);
-              xch[cc * kXchLd + r] = acc;
-            }
+        if (et == 0) atomicAdd(&arrive[mt], 1);
+        // ... and, if this segment ends the CTA's range (so the CTA has no other
+        // work left), reduce a slice of the tile's nodes once every partial is
+        // in.  The contributors whose ranges end inside the tile all finish at
+        // the end of the kernel; splitting the nodes among them keeps the
+        // fix-up tail short.  The tile's other contributor (at most one: the
+        // CTA whose range *starts* in the tile) published early and moved on.
+        if (t1 <= (mt + 1) * p.KB) {
+          const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
+          const int E = cend - cfirst + 1, rank = c - cfirst;
+          if (et == 0) {
+            while (ld_acquire(&arrive[mt]) < cnt) __nanosleep(64);
+            __threadfence();
           }
           epi_bar();
-          apply_op(e, mt, r, c0, cn, xch);
+          reduce_apply(e, p, mt, cnt, p.n * rank / E, p.n * (rank + 1) / E, ew, lane);
           epi_bar();
+          if (et == 0 && atomicAdd(&done[mt], 1) == E - 1) {  // every reducer is past its wait
+            arrive[mt] = 0;
+            done[mt] = 0;
+          }
         }
-        if (cnt > 1 && et == 0) e.counters[mt] = 0;
-      }
-      if (cnt == 1) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
       }
       t = seg_end;
       ++seg;
@@ -434,11 +537,46 @@ extern "C" int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_de
   e.out = (float*)out_dev;
   e.out_ld = n_out;
   TP_CUDA(cudaMallocAsync((void**)&e.part, sk_part_floats(p) * 4, st));
-  TP_CUDA(cudaMallocAsync((void**)&e.counters, p.mtiles * 4, st));
-  TP_CUDA(cudaMemsetAsync(e.counters, 0, p.mtiles * 4, st));
+  TP_CUDA(cudaMallocAsync((void**)&e.counters, 2 * p.mtiles * 4, st));
+  TP_CUDA(cudaMemsetAsync(e.counters, 0, 2 * p.mtiles * 4, st));
   TP_TRY(sk_gemm(&ma, &mb, p, e, st));
   TP_CUDA(cudaFreeAsync(e.part, st));
   TP_CUDA(cudaFreeAsync(e.counters, st));
   TP_CUDA(cudaStreamSynchronize(st));
+  return TP_OK;
+}
+
+extern "C" int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out,
+                                   int32_t k, void* out_dev, int32_t iters, float* ms_per_launch, void* stream) {
+  using namespace tp;
+  TP_CUDA(cudaSetDevice(device));
+  TP_CHECK(n >= 1 && n <= 256 && n_out % 128 == 0 && k % 64 == 0 && iters >= 1, TP_ESHAPE, "debug GEMM shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUtensorMap ma, mb;
+  TP_TRY(make_tmap_kmajor(&ma, w_dev, n_out, k, 128));
+  TP_TRY(make_tmap_kmajor(&mb, x_dev, n, k, 16));
+  SkPlan p = sk_plan(n_out, k, n);
+  GemmEpi e;
+  e.op = kOpStore;
+  e.out = (float*)out_dev;
+  e.out_ld = n_out;
+  TP_CUDA(cudaMalloc((void**)&e.part, sk_part_floats(p) * 4));
+  TP_CUDA(cudaMalloc((void**)&e.counters, 2 * p.mtiles * 4));
+  TP_CUDA(cudaMemsetAsync(e.counters, 0, 2 * p.mtiles * 4, st));
+  TP_TRY(sk_gemm(&ma, &mb, p, e, st));  // warm-up
+  cudaEvent_t a, b;
+  TP_CUDA(cudaEventCreate(&a));
+  TP_CUDA(cudaEventCreate(&b));
+  TP_CUDA(cudaEventRecord(a, st));
+  for (int i = 0; i < iters; ++i) TP_TRY(sk_gemm(&ma, &mb, p, e, st));
+  TP_CUDA(cudaEventRecord(b, st));
+  TP_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  TP_CUDA(cudaEventElapsedTime(&ms, a, b));
+  *ms_per_launch = ms / iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  TP_CUDA(cudaFree(e.part));
+  TP_CUDA(cudaFree(e.counters));
   return TP_OK;
 }

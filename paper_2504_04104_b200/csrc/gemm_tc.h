@@ -43,7 +43,7 @@ struct GemmEpi {
   int f = 0;
   // stream-K fix-up state
   float* part = nullptr;  // [mtiles][max_contrib][n][128]
-  int* counters = nullptr;  // [mtiles], zero between launches (self-resetting)
+  int* counters = nullptr;  // [2][mtiles] arrivals | reducers done; zero between launches (self-resetting)
 };
 
 int num_sms();

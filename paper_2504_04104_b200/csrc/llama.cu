@@ -217,9 +217,9 @@ int llama_stage_init(tp_stage* s) {
     }
     e->part_floats = pf;
     TP_CUDA(cudaMalloc(&e->part, pf * 4));
-    e->ctr_stride = mt;
-    TP_CUDA(cudaMalloc(&e->counters, (size_t)kCtrKinds * mt * 4));
-    TP_CUDA(cudaMemset(e->counters, 0, (size_t)kCtrKinds * mt * 4));
+    e->ctr_stride = 2 * mt;  // arrivals | reducers done, per GEMM kind
+    TP_CUDA(cudaMalloc(&e->counters, (size_t)kCtrKinds * e->ctr_stride * 4));
+    TP_CUDA(cudaMemset(e->counters, 0, (size_t)kCtrKinds * e->ctr_stride * 4));
     TP_TRY(make_tmap_kmajor(&e->mXd, e->Xd, np, d, 16));
     TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
     TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));

@@ -109,6 +109,13 @@ int tp_stage_rows(const tp_stage* s, int32_t* rows);
  * (f64 toy, f32 llama residual stream).  hidden_in == NULL embeds tokens.  */
 int tp_stage_forward(tp_stage* s, const tp_level* level, const void* hidden_in, void* hidden_out,
                      void* stream);
+/* Phase 1 of PipelineRunner.step (pipeline.py:289-312) for several stages hosted on
+ * ONE device: stage g pushes levels[g] through its layers.  Llama stages run
+ * layer slot by layer slot with one grouped GEMM launch per slot (up to 8
+ * stages per launch); results are bit-identical to `count` separate
+ * tp_stage_forward calls.  Stages must be distinct and share device + arch.   */
+int tp_stages_forward(int32_t count, tp_stage* const* stages, const tp_level* levels, const void* const* hidden_in,
+                      void* const* hidden_out, void* stream);
 /* Pruning propagation (KvCache.promote/prune/_restrict/drop_speculative,
  * model.py:169-194): rows < first_row stay; of rows [first_row, first_row+count)
  * those with keep bit set are compacted stably to follow them; the rest and

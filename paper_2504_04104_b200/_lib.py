@@ -67,6 +67,7 @@ _SIGS = {
     "tp_stage_rows": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "tp_stage_reserve": (C.c_int, [_P, _I]),
     "tp_stage_forward": (C.c_int, [_P, C.POINTER(Level), _P, _P, _P]),
+    "tp_stages_forward": (C.c_int, [_I, _P, _P, _P, _P, _P]),
     "tp_stage_compact": (C.c_int, [_P, _I, _I, _P, _P]),
     "tp_stage_truncate": (C.c_int, [_P, _I]),
     "tp_stage_read_kv": (C.c_int, [_P, _I, _I, _I, _I, _P]),

@@ -6,6 +6,7 @@
 #include <mutex>
 #include <string>
 
+#include "gemm_tc.h"
 #include "internal.h"
 
 #include <atomic>
@@ -355,11 +356,14 @@ int tp_stage_reserve(tp_stage* s, int32_t capacity_rows) {
   return is_toy(s->m) ? TP_OK : llama_stage_init(s);
 }
 
-int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, void* stream) {
+}  // extern "C"
+
+// Validate one level against its stage, upload its metadata (one pinned-host ->
+// device copy) and describe it for the kernels.
+static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, cudaStream_t st,
+                         LevelDev* out) {
   TP_CHECK(s && L && hidden_out, TP_ECONFIG, "null argument");
   tp_model* m = s->m;
-  TP_CUDA(cudaSetDevice(m->cfg.device));
-  cudaStream_t st = (cudaStream_t)stream;
   const int n = L->n;
   TP_CHECK(n >= 1 && n <= m->cfg.max_nodes, TP_ESHAPE, "level size outside [1, max_nodes]");
   TP_CHECK(L->positions && L->prefix_rows, TP_ECONFIG, "positions and prefix_rows are required");
@@ -417,9 +421,49 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
   lv.positions = (const int32_t*)(s->meta + off_pos);
   lv.prefix_rows = (const int32_t*)(s->meta + off_pre);
   lv.anc = (const uint64_t*)(s->meta + off_anc);
+  *out = lv;
+  return TP_OK;
+}
+
+extern "C" {
+
+int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, void* stream) {
+  TP_CHECK(s && L && hidden_out, TP_ECONFIG, "null argument");
+  tp_model* m = s->m;
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  LevelDev lv;
+  TP_TRY(prepare_level(s, L, hidden_in, hidden_out, st, &lv));
   int rc = is_toy(m) ? toy_forward(s, lv, hidden_in, hidden_out, st) : llama_forward(s, lv, hidden_in, hidden_out, st);
   if (rc != TP_OK) return rc;
-  if (L->append) s->rows += n;
+  if (L->append) s->rows += L->n;
+  return TP_OK;
+}
+
+int tp_stages_forward(int32_t count, tp_stage* const* stages, const tp_level* levels, const void* const* hidden_in,
+                      void* const* hidden_out, void* stream) {
+  TP_CHECK(count >= 1 && stages && levels && hidden_in && hidden_out, TP_ECONFIG, "null argument");
+  const int dev = stages[0]->m->cfg.device;
+  for (int g = 0; g < count; ++g) {
+    TP_CHECK(stages[g] && stages[g]->m->cfg.device == dev, TP_ECONFIG, "grouped stages must share one device");
+    TP_CHECK(stages[g]->m->cfg.arch == stages[0]->m->cfg.arch, TP_ECONFIG, "grouped stages must share the arch");
+    for (int h = 0; h < g; ++h) TP_CHECK(stages[h] != stages[g], TP_ECONFIG, "a stage appears twice in the group");
+  }
+  TP_CUDA(cudaSetDevice(dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<LevelDev> lv(count);
+  for (int g = 0; g < count; ++g)
+    TP_TRY(prepare_level(stages[g], &levels[g], hidden_in[g], hidden_out[g], st, &lv[g]));
+  if (is_toy(stages[0]->m)) {
+    for (int g = 0; g < count; ++g) TP_TRY(toy_forward(stages[g], lv[g], hidden_in[g], hidden_out[g], st));
+  } else {
+    for (int g0 = 0; g0 < count; g0 += kMaxGroup) {
+      const int cnt = std::min(kMaxGroup, count - g0);
+      TP_TRY(llama_forward_group(stages + g0, lv.data() + g0, hidden_in + g0, hidden_out + g0, cnt, st));
+    }
+  }
+  for (int g = 0; g < count; ++g)
+    if (levels[g].append) stages[g]->rows += levels[g].n;
   return TP_OK;
 }
 

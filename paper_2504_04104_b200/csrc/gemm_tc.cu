@@ -218,10 +218,10 @@ __device__ __forceinline__ float4 sum_partials(const float* base, size_t slot, i
 
 // Reduce + apply nodes [lo, hi) of m-tile mt from the global partials; the 4
 // epilogue warps take nodes round-robin, two per warp in flight.
-__device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int mt, int cnt, int lo, int hi,
-                                             int ew, int lane) {
-  const float* base = e.part + (size_t)mt * p.max_contrib * p.n * kBM;
-  const size_t slot = (size_t)p.n * kBM;
+__device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int n, int mt, int cnt, int lo,
+                                             int hi, int ew, int lane) {
+  const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
+  const size_t slot = (size_t)n * kBM;
   const int f = lane * 4;
   for (int c = lo + ew; c < hi; c += 8) {
     const int c2 = c + 4;
@@ -259,17 +259,19 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
+// Work items are (member g, k-block t) for g = 0..count-1, t in [t0, t1):
+// the TMA producer, the MMA issuer and the epilogue warps walk the same
+// sequence, the smem ring and the TMEM double buffer continuing across members.
 __global__ void __launch_bounds__(kThreads, 1)
-    sk_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SkPlan p,
-                   int stages, GemmEpi e) {
+    sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
   const int t0 = sk_begin(p, c), t1 = sk_begin(p, c + 1);
-  const int bbytes = p.n_pad * 128;
+  const int bmax = grp.max_npad * 128;  // ring slot bytes for the node tile
   uint8_t* sA = smem;
   uint8_t* sB = smem + stages * kABytes;
-  float* xch = reinterpret_cast<float*>(sB + stages * bbytes);
+  float* xch = reinterpret_cast<float*>(sB + stages * bmax);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + kXchBytes);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ncols = 32;
-  while (ncols < (uint32_t)(2 * p.n_pad)) ncols <<= 1;
+  while (ncols < (uint32_t)(2 * grp.max_npad)) ncols <<= 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -298,69 +300,79 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      tma_prefetch(&tmA);
-      tma_prefetch(&tmB);
+      for (int g = 0; g < grp.count; ++g) {
+        tma_prefetch(&grp.m[g].a);
+        tma_prefetch(&grp.m[g].b);
+      }
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-      const int nbox = p.n_pad / 16;
-      // weights do not depend on the previous kernel: fill the ring now
+      // member 0's weights do not depend on the previous kernel: fill the ring now
+      const int nbox0 = grp.m[0].n_pad / 16;
       const int npre = min(stages, t1 - t0);
       for (int j = 0; j < npre; ++j) {
         const int t = t0 + j;
-        mbar_expect_tx(&full[j], kABytes + bbytes);
-        tma_load_2d(sA + j * kABytes, &tmA, (t % p.KB) * kBK, (t / p.KB) * kBM, &full[j], pol_w);
+        mbar_expect_tx(&full[j], kABytes + nbox0 * 2048);
+        tma_load_2d(sA + j * kABytes, &grp.m[0].a, (t % p.KB) * kBK, (t / p.KB) * kBM, &full[j], pol_w);
       }
       pdl_wait();  // node rows X come from the previous kernel
       pdl_trigger();
       for (int j = 0; j < npre; ++j) {
         const int kb = (t0 + j) % p.KB;
-        for (int b = 0; b < nbox; ++b)
-          tma_load_2d(sB + j * bbytes + b * 2048, &tmB, kb * kBK, b * 16, &full[j], pol_x);
+        for (int b = 0; b < nbox0; ++b)
+          tma_load_2d(sB + j * bmax + b * 2048, &grp.m[0].b, kb * kBK, b * 16, &full[j], pol_x);
       }
       int stage = npre % stages;
       uint32_t phase = npre == stages ? 1 : 0;
-      for (int t = t0 + npre; t < t1; ++t) {
-        const int mt = t / p.KB, kb = t % p.KB;
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], kABytes + bbytes);
-        tma_load_2d(sA + stage * kABytes, &tmA, kb * kBK, mt * kBM, &full[stage], pol_w);
-        for (int b = 0; b < nbox; ++b)
-          tma_load_2d(sB + stage * bbytes + b * 2048, &tmB, kb * kBK, b * 16, &full[stage], pol_x);
-        if (++stage == stages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(kBM, p.n_pad);
-      int stage = 0, seg = 0;
-      uint32_t phase = 0;
-      int t = t0;
-      while (t < t1) {
-        const int mt = t / p.KB;
-        const int seg_start = t, seg_end = min(t1, (mt + 1) * p.KB);
-        const int buf = seg & 1;
-        const uint32_t bphase = (seg >> 1) & 1;
-        mbar_wait(&tempty[buf], bphase ^ 1);
-        tc_fence_after();
-        const uint32_t d = taddr + buf * p.n_pad;
-        for (; t < seg_end; ++t) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint64_t ad = desc_kmajor_sw128(sA + stage * kABytes);
-          const uint64_t bd = desc_kmajor_sw128(sB + stage * bbytes);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (t > seg_start || k > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
+      for (int g = 0; g < grp.count; ++g) {
+        const CUtensorMap* ma = &grp.m[g].a;
+        const CUtensorMap* mb = &grp.m[g].b;
+        const int nbox = grp.m[g].n_pad / 16;
+        for (int t = (g == 0 ? t0 + npre : t0); t < t1; ++t) {
+          const int mt = t / p.KB, kb = t % p.KB;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], kABytes + nbox * 2048);
+          tma_load_2d(sA + stage * kABytes, ma, kb * kBK, mt * kBM, &full[stage], pol_w);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sB + stage * bmax + b * 2048, mb, kb * kBK, b * 16, &full[stage], pol_x);
           if (++stage == stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[buf]);
-        ++seg;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, seg = 0;
+      uint32_t phase = 0;
+      for (int g = 0; g < grp.count; ++g) {
+        const int npad = grp.m[g].n_pad;
+        const uint32_t idesc = idesc_bf16_f32(kBM, npad);
+        int t = t0;
+        while (t < t1) {
+          const int mt = t / p.KB;
+          const int seg_start = t, seg_end = min(t1, (mt + 1) * p.KB);
+          const int buf = seg & 1;
+          const uint32_t bphase = (seg >> 1) & 1;
+          mbar_wait(&tempty[buf], bphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = taddr + buf * grp.max_npad;
+          for (; t < seg_end; ++t) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = desc_kmajor_sw128(sA + stage * kABytes);
+            const uint64_t bd = desc_kmajor_sw128(sB + stage * bmax);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (t > seg_start || k > 0) ? 1u : 0u);
+            mma_commit(&empty[stage]);
+            if (++stage == stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mma_commit(&tfull[buf]);
+          ++seg;
+        }
       }
     }
   } else {
@@ -368,77 +380,83 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = quarter * 32 + lane;
     const int ew = warp - 2;  // epilogue warp 0..3 (node-parallel phases)
     const int et = threadIdx.x - 64;
-    int* arrive = e.counters;
-    int* done = e.counters + p.mtiles;
-    int seg = 0, t = t0;
-    while (t < t1) {
-      const int mt = t / p.KB;
-      const int seg_end = min(t1, (mt + 1) * p.KB);
-      const int buf = seg & 1;
-      const uint32_t bphase = (seg >> 1) & 1;
-      const int cfirst = sk_cta_of(p, mt * p.KB);
-      const int clast = sk_cta_of(p, (mt + 1) * p.KB - 1);
-      const int cnt = clast - cfirst + 1;
-      mbar_wait(&tfull[buf], bphase);
-      tc_fence_after();
-      const uint32_t tbase = taddr + ((uint32_t)(quarter * 32) << 16) + buf * p.n_pad;
-      if (cnt == 1) {
-        for (int c0 = 0; c0 < p.n; c0 += kXchNodes) {
-          const int cn = min(kXchNodes, p.n - c0);
-          for (int col0 = c0; col0 < min(c0 + kXchNodes, p.n_pad); col0 += 16) {
+    int seg = 0;
+    for (int g = 0; g < grp.count; ++g) {
+      const GemmEpi& e = grp.m[g].e;
+      const int n = grp.m[g].n, npad = grp.m[g].n_pad;
+      int* arrive = e.counters;
+      int* done = e.counters + p.mtiles;
+      int t = t0;
+      while (t < t1) {
+        const int mt = t / p.KB;
+        const int seg_end = min(t1, (mt + 1) * p.KB);
+        const int buf = seg & 1;
+        const uint32_t bphase = (seg >> 1) & 1;
+        const int cfirst = sk_cta_of(p, mt * p.KB);
+        const int clast = sk_cta_of(p, (mt + 1) * p.KB - 1);
+        const int cnt = clast - cfirst + 1;
+        mbar_wait(&tfull[buf], bphase);
+        tc_fence_after();
+        const uint32_t tbase = taddr + ((uint32_t)(quarter * 32) << 16) + buf * grp.max_npad;
+        if (cnt == 1) {
+          for (int c0 = 0; c0 < n; c0 += kXchNodes) {
+            const int cn = min(kXchNodes, n - c0);
+            for (int col0 = c0; col0 < min(c0 + kXchNodes, npad); col0 += 16) {
+              float v[16];
+              tmem_ld_x16(tbase + col0, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (col0 + i < n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
+            }
+            epi_bar();
+            smem_apply(e, mt, c0, cn, xch, ew, lane);
+            epi_bar();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);
+        } else {
+          // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
+          float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * n) * kBM + r;
+          for (int col0 = 0; col0 < npad; col0 += 16) {
             float v[16];
             tmem_ld_x16(tbase + col0, v);
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (col0 + i < p.n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
+              if (col0 + i < n) __stcg(dst + (size_t)(col0 + i) * kBM, v[i]);
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
+          __threadfence();
           epi_bar();
-          smem_apply(e, mt, c0, cn, xch, ew, lane);
-          epi_bar();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
-      } else {
-        // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
-        float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * p.n) * kBM + r;
-        for (int col0 = 0; col0 < p.n_pad; col0 += 16) {
-          float v[16];
-          tmem_ld_x16(tbase + col0, v);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (col0 + i < p.n) __stcg(dst + (size_t)(col0 + i) * kBM, v[i]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
-        __threadfence();
-        epi_bar();
-        if (et == 0) atomicAdd(&arrive[mt], 1);
-        // ... and, if this segment ends the CTA's range (so the CTA has no other
-        // work left), reduce a slice of the tile's nodes once every partial is
-        // in.  The contributors whose ranges end inside the tile all finish at
-        // the end of the kernel; splitting the nodes among them keeps the
-        // fix-up tail short.  The tile's other contributor (at most one: the
-        // CTA whose range *starts* in the tile) published early and moved on.
-        if (t1 <= (mt + 1) * p.KB) {
-          const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
-          const int E = cend - cfirst + 1, rank = c - cfirst;
-          if (et == 0) {
-            while (ld_acquire(&arrive[mt]) < cnt) __nanosleep(64);
-            __threadfence();
-          }
-          epi_bar();
-          reduce_apply(e, p, mt, cnt, p.n * rank / E, p.n * (rank + 1) / E, ew, lane);
-          epi_bar();
-          if (et == 0 && atomicAdd(&done[mt], 1) == E - 1) {  // every reducer is past its wait
-            arrive[mt] = 0;
-            done[mt] = 0;
+          if (et == 0) atomicAdd(&arrive[mt], 1);
+          // ... and, if this segment ends the CTA's range of this member, reduce a
+          // slice of the tile's nodes once every partial is in.  The contributors
+          // whose ranges end inside the tile finish together; splitting the nodes
+          // among them keeps the fix-up short.  The tile's other contributor (at
+          // most one: the CTA whose range *starts* in the tile) published early in
+          // its pass over this member.  Waits only ever point at an earlier
+          // (member, position), so the chain cannot cycle.
+          if (t1 <= (mt + 1) * p.KB) {
+            const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
+            const int E = cend - cfirst + 1, rank = c - cfirst;
+            if (et == 0) {
+              while (ld_acquire(&arrive[mt]) < cnt) __nanosleep(64);
+              __threadfence();
+            }
+            epi_bar();
+            reduce_apply(e, p, n, mt, cnt, n * rank / E, n * (rank + 1) / E, ew, lane);
+            epi_bar();
+            if (et == 0 && atomicAdd(&done[mt], 1) == E - 1) {  // every reducer is past its wait
+              arrive[mt] = 0;
+              done[mt] = 0;
+            }
           }
         }
+        t = seg_end;
+        ++seg;
       }
-      t = seg_end;
-      ++seg;
     }
   }
   __syncthreads();
@@ -459,11 +477,19 @@ static std::vector<ProfRec> g_prof;
 static bool g_prof_on = false;
 static std::mutex g_prof_mu;
 
-int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st) {
-  TP_CHECK(p.n >= 1 && p.n_pad <= 256, TP_ESHAPE, "GEMM node count outside [1, 256]");
-  TP_CHECK(epi.counters && epi.part, TP_ECONFIG, "GEMM epilogue needs partial + counter scratch");
-  const int stages = stages_for(p.n_pad);
-  const size_t smem = smem_for(p.n_pad);
+int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st) {
+  TP_CHECK(grp.count >= 1 && grp.count <= kMaxGroup, TP_ECONFIG, "GEMM group size outside [1, 8]");
+  int mx = 16;
+  for (int g = 0; g < grp.count; ++g) {
+    const GemmMember& m = grp.m[g];
+    TP_CHECK(m.n >= 1 && m.n_pad <= 256 && m.n_pad % 16 == 0 && m.n_pad >= m.n, TP_ESHAPE,
+             "GEMM node count outside [1, 256]");
+    TP_CHECK(m.e.counters && m.e.part, TP_ECONFIG, "GEMM epilogue needs partial + counter scratch");
+    mx = std::max(mx, m.n_pad);
+  }
+  TP_CHECK(grp.max_npad == mx, TP_ECONFIG, "GemmGroup.max_npad must be the members' largest n_pad");
+  const int stages = stages_for(mx);
+  const size_t smem = smem_for(mx);
   static size_t smem_set = 0;
   if (smem > smem_set) {
     TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -474,7 +500,9 @@ int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, con
     TP_CUDA(cudaEventCreate(&rec.a));
     TP_CUDA(cudaEventCreate(&rec.b));
     TP_CUDA(cudaEventRecord(rec.a, st));
-    rec.bytes = (double)p.mtiles * kBM * p.KB * kBK * 2.0 + (double)p.n * p.KB * kBK * 2.0;
+    rec.bytes = 0.0;
+    for (int g = 0; g < grp.count; ++g)
+      rec.bytes += (double)p.mtiles * kBM * p.KB * kBK * 2.0 + (double)grp.m[g].n * p.KB * kBK * 2.0;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.G);
@@ -487,13 +515,25 @@ int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, con
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ::tp::count_launch();
-  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, *tmA, *tmB, p, stages, epi));
+  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, grp, p, stages));
   if (g_prof_on) {
     TP_CUDA(cudaEventRecord(rec.b, st));
     std::lock_guard<std::mutex> g(g_prof_mu);
     g_prof.push_back(rec);
   }
   return TP_OK;
+}
+
+int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st) {
+  GemmGroup grp;
+  grp.count = 1;
+  grp.m[0].a = *tmA;
+  grp.m[0].b = *tmB;
+  grp.m[0].e = epi;
+  grp.m[0].n = p.n;
+  grp.m[0].n_pad = p.n_pad;
+  grp.max_npad = p.n_pad;
+  return sk_gemm_group(grp, p, st);
 }
 
 }  // namespace tp

@@ -13,7 +13,7 @@ struct SkPlan {
   int total;        // mtiles * KB k-blocks, linearised m-major
   int G, q, r;      // CTAs; CTA c owns q (+1 if c < r) consecutive k-blocks
   int max_contrib;  // max CTAs contributing to one m-tile
-  int n, n_pad;     // valid node columns / MMA N
+  int n, n_pad;     // valid node columns / MMA N (single-member launches)
 };
 
 __host__ __device__ inline int sk_begin(const SkPlan& p, int c) { return c * p.q + (c < p.r ? c : p.r); }
@@ -46,6 +46,27 @@ struct GemmEpi {
   int* counters = nullptr;  // [2][mtiles] arrivals | reducers done; zero between launches (self-resetting)
 };
 
+// A grouped launch: up to kMaxGroup GEMMs of the SAME (N_out, K) shape — e.g. the
+// same layer slot of several pipeline stages hosted on one GPU — each with its
+// own weights, node rows, node count and epilogue.  CTA c streams its stream-K
+// range of member 0, then the same range of member 1, ...: every member sees
+// exactly the segment boundaries of its ungrouped launch, so grouped results are
+// bit-identical to ungrouped ones (batch invariance across stages).
+constexpr int kMaxGroup = 8;
+
+struct GemmMember {
+  CUtensorMap a;  // weights [N_out, K]
+  CUtensorMap b;  // node rows [n_pad, K]
+  GemmEpi e;
+  int n, n_pad;
+};
+
+struct GemmGroup {
+  GemmMember m[kMaxGroup];
+  int count;
+  int max_npad;
+};
+
 int num_sms();
 int make_tmap_kmajor(CUtensorMap* map, const void* gptr, int64_t rows, int64_t k, int box_rows);
 SkPlan sk_plan(int n_out, int k, int n);
@@ -53,6 +74,8 @@ inline size_t sk_part_floats(const SkPlan& p) { return (size_t)p.mtiles * p.max_
 // Launched with programmatic dependent launch: the weight prologue overlaps the
 // previous kernel; activations are read only after griddepcontrol.wait.
 int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st);
+// Grouped launch (members share p's shape; p.n / p.n_pad are ignored).
+int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st);
 
 // Let the next (PDL-launched) GEMM start its weight prologue now.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

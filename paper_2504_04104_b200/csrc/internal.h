@@ -79,6 +79,8 @@ int toy_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);
 // llama arch (llama.cu)
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out,
                   cudaStream_t st);
+int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* const* hidden_in,
+                        void* const* hidden_out, int count, cudaStream_t st);
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st);
 int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st);
 int llama_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);

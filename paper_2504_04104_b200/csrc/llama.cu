@@ -278,79 +278,194 @@ int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits
   return sk_gemm(&mext(m)->head, &e->mXd, sk_plan(V, d, n), g, st);
 }
 
-int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
-  tp_model* m = s->m;
-  const tp_model_config& c = m->cfg;
-  TP_TRY(llama_stage_init(s));
-  LlamaStageExt* e = sext(s);
-  LlamaModelExt* me = mext(m);
-  const int n = lv.n, d = c.hidden, H = c.heads, KV = c.kv_heads, f = c.ffn;
-  const int q = H * 128, kvd = KV * 128;
-  float* x = (float*)hidden_out;
-  if (hidden_in) {
-    if (hidden_in != hidden_out)
-      TP_CUDA(cudaMemcpyAsync(x, hidden_in, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, st));
-  } else {
-    TP_TRY(llama_embed(m, n, lv.tokens, x, st));
+// Grouped rmsnorm: one CTA per (node row, member).
+struct NormGroup {
+  const float* x[kMaxGroup];
+  __nv_bfloat16* xd[kMaxGroup];
+  int n[kMaxGroup];
+};
+
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __grid_constant__ NormGroup ng, int d,
+                                                                     float eps) {
+  pdl_trigger();
+  const int g = blockIdx.y;
+  if ((int)blockIdx.x >= ng.n[g]) return;
+  __shared__ float red[33];
+  const float* xr = ng.x[g] + (size_t)blockIdx.x * d;
+  float v[kNormPer];
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    v[u] = j < d ? xr[j] : 0.f;
   }
-  if (lv.layer_lo == lv.layer_hi) return TP_OK;
-  ::tp::count_launch(), rope_table_kernel<<<n, 64, 0, st>>>(lv.positions, (double)c.rope_theta, e->rope);
-  TP_CUDA(cudaGetLastError());
-  ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
-  TP_CUDA(cudaGetLastError());
-  const SkPlan pqkv = sk_plan(q + 2 * kvd, d, n), po = sk_plan(d, q, n), pgu = sk_plan(2 * f, d, n),
-               pdn = sk_plan(d, f, n);
-  AttnArgs aa;
-  aa.q = e->Xq;
-  aa.q_stride = q;
-  aa.cap = s->cap;
-  aa.kself = lv.append ? nullptr : e->kself;
-  aa.vself = lv.append ? nullptr : e->vself;
-  aa.H = H;
-  aa.KV = KV;
-  aa.scale = (float)(1.0 / std::sqrt(128.0));
-  aa.pm = e->pm;
-  aa.pl = e->pl;
-  aa.po = e->po;
-  aa.max_chunks = e->max_chunks;
-  aa.out = e->Xo;
-  aa.out_stride = q;
-  GemmEpi gq = epi_base(e, kCtrQkv);
-  gq.op = kOpQkv;
-  gq.H = H;
-  gq.KV = KV;
-  gq.cap = s->cap;
-  gq.row0 = lv.row0;
-  gq.append = lv.append;
-  gq.rope = e->rope;
-  gq.xq = e->Xq;
-  gq.kself = e->kself;
-  gq.vself = e->vself;
-  GemmEpi gr = epi_base(e, kCtrO);
-  gr.op = kOpResid;
-  gr.out = x;
-  gr.out_ld = d;
-  GemmEpi gd = gr;
-  gd.counters = e->counters + (size_t)kCtrDown * e->ctr_stride;
-  GemmEpi gg = epi_base(e, kCtrGu);
-  gg.op = kOpSwiglu;
-  gg.xf = e->Xf;
-  gg.f = f;
-  for (int layer = lv.layer_lo; layer < lv.layer_hi; ++layer) {
-    const int li = layer - c.layer_lo;
-    gq.kc = (__nv_bfloat16*)s->k[layer - s->lo];
-    gq.vc = (__nv_bfloat16*)s->v[layer - s->lo];
-    TP_TRY(sk_gemm(&me->qkv[li], &e->mXd, pqkv, gq, st));
-    aa.k = gq.kc;
-    aa.v = gq.vc;
-    TP_TRY(attn_tree(aa, lv, st));
-    TP_TRY(sk_gemm(&me->o[li], &e->mXo, po, gr, st));
-    ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    if (j < d) ss += v[u] * v[u];
+  }
+  ss = block_sum(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+  __nv_bfloat16* out = ng.xd[g] + (size_t)blockIdx.x * d;
+#pragma unroll
+  for (int u = 0; u < kNormPer; ++u) {
+    const int j = threadIdx.x + u * kNormThreads;
+    if (j < d) out[j] = __float2bfloat16_rn(v[u] * r);
+  }
+}
+
+int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
+  tp_stage* ss[1] = {s};
+  const void* hin[1] = {hidden_in};
+  void* hout[1] = {hidden_out};
+  return llama_forward_group(ss, &lv, hin, hout, 1, st);
+}
+
+// Several stages' levels on one device, layer slot by layer slot: slot j runs
+// layer lo_g + j of every member g that has one, each GEMM as ONE grouped
+// launch over the members (same segment boundaries as ungrouped launches, so
+// every member's bits equal its stand-alone forward).
+int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* const* hin, void* const* hout,
+                        int count, cudaStream_t st) {
+  TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "stage group size outside [1, 8]");
+  tp_model* m0 = ss[0]->m;
+  const tp_model_config& c = m0->cfg;
+  const int d = c.hidden, H = c.heads, KV = c.kv_heads, f = c.ffn;
+  const int q = H * 128, kvd = KV * 128;
+  int slots = 0;
+  for (int g = 0; g < count; ++g) {
+    tp_stage* s = ss[g];
+    const tp_model_config& cg = s->m->cfg;
+    TP_CHECK(cg.hidden == d && cg.heads == H && cg.kv_heads == KV && cg.ffn == f && cg.device == c.device,
+             TP_ECONFIG, "grouped stages must share the model shape and device");
+    TP_TRY(llama_stage_init(s));
+    const LevelDev& lv = lvs[g];
+    float* x = (float*)hout[g];
+    if (hin[g]) {
+      if (hin[g] != hout[g])
+        TP_CUDA(cudaMemcpyAsync(x, hin[g], (size_t)lv.n * d * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      TP_TRY(llama_embed(s->m, lv.n, lv.tokens, x, st));
+    }
+    slots = std::max(slots, lv.layer_hi - lv.layer_lo);
+  }
+  if (slots == 0) return TP_OK;
+  int maxn = 0;
+  for (int g = 0; g < count; ++g) {
+    const LevelDev& lv = lvs[g];
+    if (lv.layer_hi == lv.layer_lo) continue;
+    maxn = std::max(maxn, lv.n);
+    ::tp::count_launch(), rope_table_kernel<<<lv.n, 64, 0, st>>>(lv.positions, (double)c.rope_theta,
+                                                                  sext(ss[g])->rope);
     TP_CUDA(cudaGetLastError());
-    TP_TRY(sk_gemm(&me->gu[li], &e->mXd, pgu, gg, st));
-    TP_TRY(sk_gemm(&me->down[li], &e->mXf, pdn, gd, st));
-    if (layer + 1 < lv.layer_hi) {
-      ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, c.norm_eps, e->Xd);
+  }
+  const SkPlan pqkv = sk_plan(q + 2 * kvd, d, 1), po = sk_plan(d, q, 1), pgu = sk_plan(2 * f, d, 1),
+               pdn = sk_plan(d, f, 1);
+  for (int j = 0; j < slots; ++j) {
+    int idx[kMaxGroup], na = 0;
+    for (int g = 0; g < count; ++g)
+      if (lvs[g].layer_lo + j < lvs[g].layer_hi) idx[na++] = g;
+    NormGroup ng;
+    GemmGroup gq, go, ggu, gdn;
+    gq.count = go.count = ggu.count = gdn.count = na;
+    int mx = 16;
+    for (int a = 0; a < na; ++a) {
+      const int g = idx[a];
+      tp_stage* s = ss[g];
+      const LevelDev& lv = lvs[g];
+      LlamaStageExt* e = sext(s);
+      LlamaModelExt* me = mext(s->m);
+      const int layer = lv.layer_lo + j, li = layer - s->m->cfg.layer_lo;
+      const int n = lv.n, npad = std::max(16, (n + 15) / 16 * 16);
+      mx = std::max(mx, npad);
+      float* x = (float*)hout[g];
+      ng.x[a] = x;
+      ng.xd[a] = e->Xd;
+      ng.n[a] = n;
+      GemmEpi eq = epi_base(e, kCtrQkv);
+      eq.op = kOpQkv;
+      eq.H = H;
+      eq.KV = KV;
+      eq.cap = s->cap;
+      eq.row0 = lv.row0;
+      eq.append = lv.append;
+      eq.rope = e->rope;
+      eq.xq = e->Xq;
+      eq.kself = e->kself;
+      eq.vself = e->vself;
+      eq.kc = (__nv_bfloat16*)s->k[layer - s->lo];
+      eq.vc = (__nv_bfloat16*)s->v[layer - s->lo];
+      GemmEpi er = epi_base(e, kCtrO);
+      er.op = kOpResid;
+      er.out = x;
+      er.out_ld = d;
+      GemmEpi ed = er;
+      ed.counters = e->counters + (size_t)kCtrDown * e->ctr_stride;
+      GemmEpi eg = epi_base(e, kCtrGu);
+      eg.op = kOpSwiglu;
+      eg.xf = e->Xf;
+      eg.f = f;
+      auto set = [&](GemmGroup& gg, const CUtensorMap& wa, const CUtensorMap& xb, const GemmEpi& ep) {
+        gg.m[a].a = wa;
+        gg.m[a].b = xb;
+        gg.m[a].e = ep;
+        gg.m[a].n = n;
+        gg.m[a].n_pad = npad;
+      };
+      set(gq, me->qkv[li], e->mXd, eq);
+      set(go, me->o[li], e->mXo, er);
+      set(ggu, me->gu[li], e->mXd, eg);
+      set(gdn, me->down[li], e->mXf, ed);
+    }
+    gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
+    if (j == 0) {
+      ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
+      TP_CUDA(cudaGetLastError());
+    }
+    TP_TRY(sk_gemm_group(gq, pqkv, st));
+    for (int a = 0; a < na; ++a) {
+      const int g = idx[a];
+      tp_stage* s = ss[g];
+      const LevelDev& lv = lvs[g];
+      LlamaStageExt* e = sext(s);
+      AttnArgs aa;
+      aa.q = e->Xq;
+      aa.q_stride = q;
+      aa.cap = s->cap;
+      aa.kself = lv.append ? nullptr : e->kself;
+      aa.vself = lv.append ? nullptr : e->vself;
+      aa.H = H;
+      aa.KV = KV;
+      aa.scale = (float)(1.0 / std::sqrt(128.0));
+      aa.pm = e->pm;
+      aa.pl = e->pl;
+      aa.po = e->po;
+      aa.max_chunks = e->max_chunks;
+      aa.out = e->Xo;
+      aa.out_stride = q;
+      aa.k = gq.m[a].e.kc;
+      aa.v = gq.m[a].e.vc;
+      TP_TRY(attn_tree(aa, lv, st));
+    }
+    TP_TRY(sk_gemm_group(go, po, st));
+    ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
+    TP_CUDA(cudaGetLastError());
+    TP_TRY(sk_gemm_group(ggu, pgu, st));
+    TP_TRY(sk_gemm_group(gdn, pdn, st));
+    // input norm of the next slot, for the members that continue
+    int nc = 0;
+    NormGroup nn;
+    int maxc = 0;
+    for (int a = 0; a < na; ++a)
+      if (lvs[idx[a]].layer_lo + j + 1 < lvs[idx[a]].layer_hi) {
+        nn.x[nc] = ng.x[a];
+        nn.xd[nc] = ng.xd[a];
+        nn.n[nc] = ng.n[a];
+        maxc = std::max(maxc, ng.n[a]);
+        ++nc;
+      }
+    if (nc) {
+      ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxc, nc), kNormThreads, 0, st>>>(nn, d, c.norm_eps);
       TP_CUDA(cudaGetLastError());
     }
   }

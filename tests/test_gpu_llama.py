@@ -183,3 +183,55 @@ def test_llama_pipeline_lossless_and_margin_parity():
         x = o.run_position(o.embed(tok, len(prompt) + i), okv, list(range(len(okv))), pos=len(prompt) + i,
                            prefix=True)
     assert checked >= n_tok // 2
+
+
+@pytest.mark.parametrize("stages,w,k", [(4, 8, 4), (8, 6, 3)])
+def test_grouped_stage_forward_bitwise(stages, w, k):
+    """tp_stages_forward (one grouped GEMM launch per layer slot over all
+    same-device stages) == per-stage tp_stage_forward, bit for bit, every step;
+    and the SpecPipe tokens equal the GPU greedy decode."""
+    cfg, m, _ = tiny_model(layers=stages)
+    prompt = [int(t) for t in np.random.default_rng(4).integers(0, cfg.vocab, 70)]
+    n_tok = 20
+    ref = tp.sequential_decode(m, prompt, n_tok + 3 * stages)
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.6, rank_decay=0.5, miss_prob=0.1, seed=5),
+                              cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(ref))
+    from paper_2504_04104_b200.pipeline import PipelineRunner
+
+    rec = PipelineRunner(m, tp.PipelineConfig(num_stages=stages), tp.BeamConfig(w=w, k=k), draft,
+                         collect_trace=False, grouped=True)
+    rec.children_log = []
+    rec.prefill(prompt)
+    while len(rec.emitted) < n_tok:
+        rec.decode_step()
+    assert rec.emitted == ref[: len(rec.emitted)]
+    runs = {}
+    for grouped in (True, False):
+        r = PipelineRunner(m, tp.PipelineConfig(num_stages=stages), tp.BeamConfig(w=w, k=k), None,
+                           collect_trace=False, grouped=grouped)
+        r.prefill(prompt)
+        outs = []
+        for ch in rec.children_log:
+            r.launch_compute()
+            outs.append([None if s.out is None else s.out.cpu().clone() for s in r.stages])
+            r.step(ch)
+        runs[grouped] = (outs, list(r.emitted))
+    assert runs[True][1] == runs[False][1] == rec.emitted
+    for step, (a, b) in enumerate(zip(runs[True][0], runs[False][0])):
+        for s, (x, y) in enumerate(zip(a, b)):
+            assert (x is None) == (y is None), (step, s)
+            if x is not None:
+                assert torch.equal(x, y), (step, s)
+
+
+def test_grouped_gemm_nine_stages_chunks():
+    """More than 8 same-device stages: the group is split into launches of <= 8."""
+    cfg, m, _ = tiny_model(layers=9)
+    prompt = [int(t) for t in np.random.default_rng(8).integers(0, cfg.vocab, 20)]
+    ref = tp.sequential_decode(m, prompt, 30)
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.9, rank_decay=0.5, miss_prob=0.0, seed=2),
+                              cfg.vocab)
+    res = tp.run(m, tp.PipelineConfig(num_stages=9), tp.BeamConfig(w=3, k=3), draft, prompt, 20,
+                 collect_trace=False)
+    assert res.tokens == ref[:20]

@@ -99,6 +99,12 @@ int tp_model_logits(tp_model* m, tp_stage* ws, int32_t n, const void* hidden_dev
  * {token, child_index or -1}; synchronises the stream.                        */
 int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
                     int32_t n_children, int32_t* result_host, void* stream);
+/* The same verification split in two so the host never drains the stream:
+ * _async enqueues head + argmax + child match + the 8-byte D2H and returns;
+ * _wait blocks on that work only (not on anything enqueued after it).        */
+int tp_model_verify_async(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
+                          int32_t n_children, void* stream);
+int tp_model_verify_wait(tp_stage* ws, int32_t* result_host);
 
 /* ---- stage: replaces KvCache (model.py:105-204) + forward_tree (:312-349) - */
 int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t capacity_rows,

@@ -62,6 +62,8 @@ _SIGS = {
     "tp_model_embed": (C.c_int, [_P, _I, _P, _P, _P, _P]),
     "tp_model_logits": (C.c_int, [_P, _P, _I, _P, _P, _P]),
     "tp_model_verify": (C.c_int, [_P, _P, _P, _P, _I, _P, _P]),
+    "tp_model_verify_async": (C.c_int, [_P, _P, _P, _P, _I, _P]),
+    "tp_model_verify_wait": (C.c_int, [_P, _P]),
     "tp_stage_create": (C.c_int, [_P, _I, _I, _I, C.POINTER(_P)]),
     "tp_stage_destroy": (C.c_int, [_P]),
     "tp_stage_rows": (C.c_int, [_P, C.POINTER(C.c_int32)]),

@@ -62,13 +62,34 @@ size_t meta_capacity(const tp_model* m, int cap, int* words) {
   return (bytes + 255) & ~(size_t)255;
 }
 
-int upload(tp_stage* s, const void* host, size_t bytes, size_t dev_off, cudaStream_t st) {
-  TP_CHECK(dev_off + bytes <= s->meta_bytes, TP_ESHAPE, "metadata exceeds stage staging buffer");
-  TP_CUDA(cudaEventSynchronize(s->meta_done));  // previous upload has left the pinned buffer
-  std::memcpy(s->host_meta + dev_off, host, bytes);
-  TP_CUDA(cudaMemcpyAsync(s->meta + dev_off, s->host_meta + dev_off, bytes, cudaMemcpyHostToDevice, st));
+// Claim the next staging slot (waiting only if the stream has not yet executed
+// the upload that last used it); returns host + device addresses of the slot.
+int meta_slot(tp_stage* s, size_t bytes, char** host, char** dev, int* slot) {
+  TP_CHECK(bytes <= s->meta_bytes, TP_ESHAPE, "metadata exceeds stage staging buffer");
+  const int k = s->meta_next;
+  s->meta_next = (k + 1) % tp_stage::kMetaRing;
+  TP_CUDA(cudaEventSynchronize(s->meta_ev[k]));
+  *host = s->host_meta + (size_t)k * s->meta_bytes;
+  *dev = s->meta + (size_t)k * s->meta_bytes;
+  *slot = k;
+  return TP_OK;
+}
+
+int meta_push(tp_stage* s, int slot, size_t bytes, cudaStream_t st) {
+  const size_t off = (size_t)slot * s->meta_bytes;
+  TP_CUDA(cudaMemcpyAsync(s->meta + off, s->host_meta + off, bytes, cudaMemcpyHostToDevice, st));
   count_io((long long)bytes, 0);
-  TP_CUDA(cudaEventRecord(s->meta_done, st));
+  TP_CUDA(cudaEventRecord(s->meta_ev[slot], st));
+  return TP_OK;
+}
+
+int upload(tp_stage* s, const void* host, size_t bytes, cudaStream_t st, const char** dev_out) {
+  char *h, *d;
+  int k;
+  TP_TRY(meta_slot(s, bytes, &h, &d, &k));
+  std::memcpy(h, host, bytes);
+  TP_TRY(meta_push(s, k, bytes, st));
+  *dev_out = d;
   return TP_OK;
 }
 
@@ -108,8 +129,8 @@ int alloc_kv(tp_stage* s, int cap) {
   if (s->meta) cudaFree(s->meta);
   if (s->host_meta) cudaFreeHost(s->host_meta);
   s->meta_bytes = meta_capacity(s->m, cap, &s->max_words);
-  TP_CUDA(cudaMalloc((void**)&s->meta, s->meta_bytes));
-  TP_CUDA(cudaMallocHost((void**)&s->host_meta, s->meta_bytes));
+  TP_CUDA(cudaMalloc((void**)&s->meta, s->meta_bytes * tp_stage::kMetaRing));
+  TP_CUDA(cudaMallocHost((void**)&s->host_meta, s->meta_bytes * tp_stage::kMetaRing));
   return TP_OK;
 }
 
@@ -309,8 +330,11 @@ int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t cap
   }
   TP_CUDA(cudaMalloc((void**)&s->ws, s->ws_bytes));
   TP_CUDA(cudaMemset(s->ws, 0, s->ws_bytes));
-  TP_CUDA(cudaEventCreateWithFlags(&s->meta_done, cudaEventDisableTiming));
-  TP_CUDA(cudaEventRecord(s->meta_done, 0));
+  for (auto& ev : s->meta_ev) {
+    TP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TP_CUDA(cudaEventRecord(ev, 0));
+  }
+  TP_CUDA(cudaEventCreateWithFlags(&s->verify_ev, cudaEventDisableTiming));
   TP_CUDA(cudaMalloc((void**)&s->d_result, 16));
   TP_CUDA(cudaMallocHost((void**)&s->h_result, 16));
   TP_CUDA(cudaMalloc(&s->logits, (size_t)m->cfg.vocab * 8));
@@ -333,7 +357,9 @@ int tp_stage_destroy(tp_stage* s) {
   if (s->ws) cudaFree(s->ws);
   if (s->meta) cudaFree(s->meta);
   if (s->host_meta) cudaFreeHost(s->host_meta);
-  if (s->meta_done) cudaEventDestroy(s->meta_done);
+  for (auto ev : s->meta_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (s->verify_ev) cudaEventDestroy(s->verify_ev);
   if (s->d_result) cudaFree(s->d_result);
   if (s->h_result) cudaFreeHost(s->h_result);
   if (s->d_planes) cudaFree(s->d_planes);
@@ -392,17 +418,15 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   size_t off_tok = 0, off_pos = 4 * (size_t)n, off_pre = 8 * (size_t)n;
   size_t off_anc = ((12 * (size_t)n) + 7) & ~(size_t)7;
   size_t total = off_anc + 8 * (size_t)n * L->words;
-  TP_CHECK(total <= s->meta_bytes, TP_ESHAPE, "metadata exceeds stage staging buffer");
-  TP_CUDA(cudaEventSynchronize(s->meta_done));
-  char* h = s->host_meta;
+  char *h, *dm;
+  int slot;
+  TP_TRY(meta_slot(s, total, &h, &dm, &slot));
   if (L->tokens) std::memcpy(h + off_tok, L->tokens, 4 * (size_t)n);
   else std::memset(h + off_tok, 0, 4 * (size_t)n);
   std::memcpy(h + off_pos, L->positions, 4 * (size_t)n);
   std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
   if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
-  TP_CUDA(cudaMemcpyAsync(s->meta, h, total, cudaMemcpyHostToDevice, st));
-  count_io((long long)total, 0);
-  TP_CUDA(cudaEventRecord(s->meta_done, st));
+  TP_TRY(meta_push(s, slot, total, st));
   LevelDev lv;
   lv.n = n;
   lv.append = L->append;
@@ -417,10 +441,10 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   lv.layer_hi = all_layers ? s->hi : (no_layers ? s->lo : L->layer_hi);
   TP_CHECK(s->lo <= lv.layer_lo && lv.layer_lo <= lv.layer_hi && lv.layer_hi <= s->hi, TP_ESHAPE,
            "layer range not hosted by this stage");
-  lv.tokens = (const int32_t*)(s->meta + off_tok);
-  lv.positions = (const int32_t*)(s->meta + off_pos);
-  lv.prefix_rows = (const int32_t*)(s->meta + off_pre);
-  lv.anc = (const uint64_t*)(s->meta + off_anc);
+  lv.tokens = (const int32_t*)(dm + off_tok);
+  lv.positions = (const int32_t*)(dm + off_pos);
+  lv.prefix_rows = (const int32_t*)(dm + off_pre);
+  lv.anc = (const uint64_t*)(dm + off_anc);
   *out = lv;
   return TP_OK;
 }
@@ -477,8 +501,9 @@ int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64
     if ((keep_bits[j >> 6] >> (j & 63)) & 1ull) src.push_back(first_row + j);
   if (!src.empty()) {
     cudaStream_t st = (cudaStream_t)stream;
-    TP_TRY(upload(s, src.data(), src.size() * 4, 0, st));
-    TP_TRY(kv_compact(s, (const int32_t*)s->meta, (int)src.size(), first_row, s->d_planes, st));
+    const char* d;
+    TP_TRY(upload(s, src.data(), src.size() * 4, st, &d));
+    TP_TRY(kv_compact(s, (const int32_t*)d, (int)src.size(), first_row, s->d_planes, st));
   }
   s->rows = first_row + (int)src.size();
   return TP_OK;
@@ -529,21 +554,34 @@ int tp_model_logits(tp_model* m, tp_stage* ws, int32_t n, const void* hidden_dev
                    : llama_logits(m, ws, n, (const float*)hidden_dev, (float*)logits_dev, st);
 }
 
-int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
-                    int32_t n_children, int32_t* result_host, void* stream) {
+int tp_model_verify_async(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
+                          int32_t n_children, void* stream) {
   TP_CUDA(cudaSetDevice(m->cfg.device));
   TP_CHECK(ws && ws->m == m, TP_ECONFIG, "workspace stage must belong to the model");
   TP_CHECK(n_children >= 0 && n_children <= m->cfg.max_nodes, TP_ESHAPE, "too many children");
   cudaStream_t st = (cudaStream_t)stream;
   TP_TRY(tp_model_logits(m, ws, 1, hidden_dev, ws->logits, stream));
-  if (n_children) TP_TRY(upload(ws, child_tokens, 4 * (size_t)n_children, 0, st));
-  TP_TRY(argmax_match(ws->logits, is_toy(m), m->cfg.vocab, (const int32_t*)ws->meta, n_children, ws->d_result, st));
+  const char* d = nullptr;
+  if (n_children) TP_TRY(upload(ws, child_tokens, 4 * (size_t)n_children, st, &d));
+  TP_TRY(argmax_match(ws->logits, is_toy(m), m->cfg.vocab, (const int32_t*)d, n_children, ws->d_result, st));
   TP_CUDA(cudaMemcpyAsync(ws->h_result, ws->d_result, 8, cudaMemcpyDeviceToHost, st));
   count_io(0, 8);
-  TP_CUDA(cudaStreamSynchronize(st));
+  TP_CUDA(cudaEventRecord(ws->verify_ev, st));
+  return TP_OK;
+}
+
+int tp_model_verify_wait(tp_stage* ws, int32_t* result_host) {
+  TP_CHECK(ws, TP_ECONFIG, "null argument");
+  TP_CUDA(cudaEventSynchronize(ws->verify_ev));
   result_host[0] = ws->h_result[0];
   result_host[1] = ws->h_result[1];
   return TP_OK;
+}
+
+int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
+                    int32_t n_children, int32_t* result_host, void* stream) {
+  TP_TRY(tp_model_verify_async(m, ws, hidden_dev, child_tokens, n_children, stream));
+  return tp_model_verify_wait(ws, result_host);
 }
 
 int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t row_bytes, int32_t n_src,
@@ -555,8 +593,9 @@ int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t ro
   *n_out = (int32_t)idx.size();
   if (idx.empty()) return TP_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  TP_TRY(upload(ws, idx.data(), idx.size() * 4, 0, st));
-  return rows_compact(src_dev, dst_dev, row_bytes, (const int32_t*)ws->meta, (int)idx.size(), st);
+  const char* d;
+  TP_TRY(upload(ws, idx.data(), idx.size() * 4, st, &d));
+  return rows_compact(src_dev, dst_dev, row_bytes, (const int32_t*)d, (int)idx.size(), st);
 }
 
 }  // extern "C"

@@ -8,6 +8,7 @@ namespace tp {
 constexpr int kAttnChunk = 64;     // logical key slots per canonical chunk
 constexpr int kAttnMaxExtra = 64;  // speculative ancestor rows per node
 constexpr int kAttnHeadDim = 128;
+constexpr int kAttnMaxGroup = 8;   // stages per grouped launch
 
 struct AttnArgs {
   const __nv_bfloat16* q;  // [n][H*128]
@@ -19,7 +20,7 @@ struct AttnArgs {
   const __nv_bfloat16* vself;
   int H, KV;
   float scale;
-  float* pm;  // [n][H][max_chunks] per-chunk max
+  float* pm;  // [n][H][max_chunks] per-chunk max          (shared chunks only)
   float* pl;  // per-chunk sum
   float* po;  // [n][H][max_chunks][128] per-chunk unnormalised output
   int max_chunks;
@@ -27,6 +28,24 @@ struct AttnArgs {
   int out_stride;
 };
 
+// One grouped launch pair covers the same layer slot of several stages.
+struct AttnMember {
+  AttnArgs a;
+  LevelDev lv;
+  int c_shared;    // chunks inside every node's verified prefix
+  int zt;          // 64-node blocks
+  int cta_shared;  // first CTA of this member in the shared launch
+  int cta_tail;    // first CTA of this member in the tail launch
+};
+
+struct AttnGroup {
+  AttnMember m[kAttnMaxGroup];
+  int count;
+  int ctas_shared, ctas_tail;
+};
+
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
+// members[0..count) -> two launches (shared chunks, then per-node tail + ordered combine)
+int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st);
 
 }  // namespace tp

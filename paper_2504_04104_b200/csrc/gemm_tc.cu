@@ -490,10 +490,12 @@ int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st) {
   TP_CHECK(grp.max_npad == mx, TP_ECONFIG, "GemmGroup.max_npad must be the members' largest n_pad");
   const int stages = stages_for(mx);
   const size_t smem = smem_for(mx);
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
+  static size_t smem_set[64] = {0};  // per device
+  int dev = 0;
+  TP_CUDA(cudaGetDevice(&dev));
+  if (smem > smem_set[dev & 63]) {
     TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
+    smem_set[dev & 63] = smem;
   }
   ProfRec rec{};
   if (g_prof_on) {

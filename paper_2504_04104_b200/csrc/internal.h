@@ -32,13 +32,17 @@ struct tp_stage {
   // device workspace
   char* ws = nullptr;
   size_t ws_bytes = 0;
-  // device metadata block (tokens, positions, prefix rows, anc bits, extras)
-  char* meta = nullptr;
-  size_t meta_bytes = 0;
+  // metadata uploads (tokens, positions, prefix rows, anc bits, index lists) go
+  // through a ring of kMetaRing (pinned host, device) slot pairs, so the host
+  // only waits when it laps an upload the stream has not executed yet
+  static constexpr int kMetaRing = 8;
+  char* meta = nullptr;       // device: kMetaRing slots of meta_bytes
+  char* host_meta = nullptr;  // pinned host: same layout
+  size_t meta_bytes = 0;      // bytes per slot
   int max_words = 0;
-  // pinned host staging for metadata uploads
-  char* host_meta = nullptr;
-  cudaEvent_t meta_done = nullptr;
+  cudaEvent_t meta_ev[kMetaRing] = {nullptr};
+  int meta_next = 0;
+  cudaEvent_t verify_ev = nullptr;  // async verify: result landed in h_result
   // verify result staging
   int32_t* d_result = nullptr;
   int32_t* h_result = nullptr;

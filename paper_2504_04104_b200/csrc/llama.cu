@@ -423,30 +423,33 @@ int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* co
       TP_CUDA(cudaGetLastError());
     }
     TP_TRY(sk_gemm_group(gq, pqkv, st));
+    AttnArgs aa[kMaxGroup];
+    LevelDev al[kMaxGroup];
     for (int a = 0; a < na; ++a) {
       const int g = idx[a];
       tp_stage* s = ss[g];
       const LevelDev& lv = lvs[g];
       LlamaStageExt* e = sext(s);
-      AttnArgs aa;
-      aa.q = e->Xq;
-      aa.q_stride = q;
-      aa.cap = s->cap;
-      aa.kself = lv.append ? nullptr : e->kself;
-      aa.vself = lv.append ? nullptr : e->vself;
-      aa.H = H;
-      aa.KV = KV;
-      aa.scale = (float)(1.0 / std::sqrt(128.0));
-      aa.pm = e->pm;
-      aa.pl = e->pl;
-      aa.po = e->po;
-      aa.max_chunks = e->max_chunks;
-      aa.out = e->Xo;
-      aa.out_stride = q;
-      aa.k = gq.m[a].e.kc;
-      aa.v = gq.m[a].e.vc;
-      TP_TRY(attn_tree(aa, lv, st));
+      AttnArgs& x = aa[a];
+      x.q = e->Xq;
+      x.q_stride = q;
+      x.cap = s->cap;
+      x.kself = lv.append ? nullptr : e->kself;
+      x.vself = lv.append ? nullptr : e->vself;
+      x.H = H;
+      x.KV = KV;
+      x.scale = (float)(1.0 / std::sqrt(128.0));
+      x.pm = e->pm;
+      x.pl = e->pl;
+      x.po = e->po;
+      x.max_chunks = e->max_chunks;
+      x.out = e->Xo;
+      x.out_stride = q;
+      x.k = gq.m[a].e.kc;
+      x.v = gq.m[a].e.vc;
+      al[a] = lv;
     }
+    TP_TRY(attn_tree_group(aa, al, na, st));
     TP_TRY(sk_gemm_group(go, po, st));
     ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
     TP_CUDA(cudaGetLastError());

@@ -235,3 +235,31 @@ def test_grouped_gemm_nine_stages_chunks():
     res = tp.run(m, tp.PipelineConfig(num_stages=9), tp.BeamConfig(w=3, k=3), draft, prompt, 20,
                  collect_trace=False)
     assert res.tokens == ref[:20]
+
+
+def test_llama_long_context_invariance_and_oracle():
+    """> 32 canonical chunks (2.2k-token prefix): siblings together == alone, a
+    chain == sequential prefill (bitwise), and outputs within TOL of the oracle."""
+    cfg, m, o = tiny_model()
+    rng = np.random.default_rng(21)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, 2200)]
+    base = KvCache(cfg.layers, cfg.hidden, capacity=2304)
+    tp.model.prefill_rows(m, base, prompt)
+
+    def fresh():
+        c = KvCache(cfg.layers, cfg.hidden, capacity=2304)
+        tp.model.prefill_rows(m, c, prompt)
+        return c
+
+    P = len(prompt)
+    nodes = [(10 + i, int(rng.integers(cfg.vocab)), P, frozenset({10 + i})) for i in range(6)]
+    together = forward_tree(m, fresh(), nodes).cpu()
+    for i, nd in enumerate(nodes[:3]):
+        alone = forward_tree(m, fresh(), [nd]).cpu()
+        assert torch.equal(alone[0], together[i]), i
+    okv = o.new_kv()
+    x = None
+    for pos, tok in enumerate(prompt + [nodes[0][1]]):
+        x = o.run_position(o.embed(tok, pos), okv, list(range(len(okv))), pos=pos, prefix=True)
+    got = together[0].numpy()
+    assert float(np.abs(got - x).max()) <= TOL * max(1.0, float(np.abs(x).max()))

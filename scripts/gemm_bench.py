@@ -23,12 +23,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="7b")
 ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--n", default="1,16,48,64")
+ap.add_argument("--shapes", default="", help="comma list of shape names to run (default all)")
 args = ap.parse_args()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.
 lib = _lib.lib()
 st = torch.cuda.current_stream().cuda_stream
 for name, n_out, k in SHAPES[args.model]:
+    if args.shapes and name not in args.shapes.split(","):
+        continue
     w = (torch.randn(n_out, k, device="cuda") * 0.02).to(torch.bfloat16)
     for n in [int(x) for x in args.n.split(",")]:
         x = torch.randn(n, k, device="cuda").to(torch.bfloat16)

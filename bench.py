@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-steps", type=int, default=16)
+    ap.add_argument("--profile-steps", type=int, default=24)
     return ap.parse_args()
 
 
@@ -276,24 +276,57 @@ def run_ours(args, rank, world):
     sync_all()
     tok0 = len(replay.emitted)
     node_layers = 0
+    step_bytes = 0.0  # SURVEY §8d algorithmic bytes of the timed steps
+    q_, kv_ = cfg.heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
+    layer_w = 2.0 * (cfg.hidden * (q_ + 2 * kv_) + q_ * cfg.hidden + 3 * cfg.hidden * cfg.ffn)
+    head_w = 2.0 * cfg.vocab * cfg.hidden
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    replay.host_s = {k: 0.0 for k in replay.host_s}
+    th = time.perf_counter()
     e0.record(streams[0])
     for ch in children[args.warmup : args.warmup + args.steps]:
         node_layers += sum(len(s.resident) * (s.layer_range[1] - s.layer_range[0])
                            for s in replay.stages if s.resident is not None)
         resident.append([len(s.resident) if s.resident is not None else 0 for s in replay.stages])
+        for s in replay.stages:
+            if s.resident is None:
+                continue
+            nl, ns = s.layer_range[1] - s.layer_range[0], len(s.resident)
+            ctx = len(s.kv)  # rows streamed once per layer (prefix + speculative)
+            step_bytes += nl * (layer_w + ctx * 2 * kv_ * 2 + ns * 2 * kv_ * 2)
+            if s.layer_range[0] == 0:
+                step_bytes += ns * cfg.hidden * 2
+            if s is replay.stages[-1]:
+                step_bytes += head_w
         replay.step(ch)
     e1.record(streams[0])
+    host_loop_s = time.perf_counter() - th
     sync_all()
+    host_diag = {k: round(v * 1e3 / args.steps, 4) for k, v in replay.host_s.items()}
+    host_diag["loop_wall"] = round(host_loop_s * 1e3 / args.steps, 4)
     value_tokens = len(replay.emitted) - tok0
     value_ms = e0.elapsed_time(e1) / max(1, value_tokens)
     assert replay.emitted == ref[: len(replay.emitted)]
+
+    # ---- GPU phase timeline of a few steps (diagnostic, separate from the timed run) -----
+    replay.phase_events = []
+    for ch in children[args.warmup + args.steps : args.warmup + args.steps + 8]:
+        replay.step(ch)
+    sync_all()
+    phases: dict[str, float] = {}
+    evs = replay.phase_events
+    for (ta, ea), (tb, eb) in zip(evs, evs[1:]):
+        key = f"{ta}->{tb}"
+        phases[key] = phases.get(key, 0.0) + ea.elapsed_time(eb)
+    nsteps = max(1, sum(1 for t, _ in evs if t == "end"))
+    phase_diag = {k: round(v / nsteps, 4) for k, v in phases.items()}
+    replay.phase_events = None
 
     # ---- roofline: profiled replay of the next steps -------------------------------------
     _lib.profile_enable(True)
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pe0.record(streams[0])
-    for ch in children[args.warmup + args.steps :]:
+    for ch in children[args.warmup + args.steps + 8 :]:
         replay.step(ch)
     pe1.record(streams[0])
     sync_all()
@@ -319,6 +352,14 @@ def run_ours(args, rank, world):
                      "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
                      "gemm_share_of_step": round(gemm_ms / prof_total_ms, 4) if prof_total_ms else None,
                      "gemm_launches": gemm_n, "bytes_per_launch": round(gemm_bytes / max(1, gemm_n))},
+        "step_roofline": {"bound": "hbm", "algorithmic_bytes_per_step": round(step_bytes / max(1, len(resident))),
+                          "ideal_ms_per_step": round(step_bytes / max(1, len(resident)) / (peak * 1e6), 4),
+                          "achieved": round(step_bytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1),
+                          "frac": round(step_bytes / (e0.elapsed_time(e1) * 1e-3) / 1e9 / peak, 4),
+                          "unit": "GB/s", "note": "whole engine step (all kernels + host gaps) vs weights of the "
+                                                  "occupied stages + KV rows + LM head, per SURVEY 8d"},
+        "host_ms_per_step": host_diag,
+        "gpu_phase_ms_per_step": phase_diag,
         "clocks": clocks.summary(),
         "steps_per_token": round(steps_per_token, 4), "hit_rate": round(hit_rate, 4),
         "mean_resident_nodes": [round(float(x), 2) for x in np.mean(np.asarray(resident), axis=0)] if resident else None,

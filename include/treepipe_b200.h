@@ -158,6 +158,13 @@ int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_dev, int32_t 
 int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, int32_t n, int32_t n_out, int32_t k,
                         void* out_dev, int32_t iters, float* ms_per_launch, void* stream);
 
+/* Grouped variant: `count` (<= 8) same-shape GEMMs in one launch, as phase 1 runs them. */
+int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
+                              const int32_t* n, int32_t n_out, int32_t k, void* const* out_dev, int32_t iters,
+                              float* ms_per_launch, void* stream);
+/* Tuning knobs of K2 (0: ring depth cap, 1: smem budget in KB); process-wide. */
+int tp_debug_gemm_knob(int32_t knob, int32_t value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,8 @@ _SIGS = {
     "tp_rows_compact": (C.c_int, [_P, _P, _P, C.c_int64, _I, _P, C.POINTER(C.c_int32), _P]),
     "tp_debug_gemm": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _P]),
     "tp_debug_gemm_timed": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _I, _P, _P]),
+    "tp_debug_gemm_group_timed": (C.c_int, [_I, _I, _P, _P, _P, _I, _I, _P, _I, _P, _P]),
+    "tp_debug_gemm_knob": (C.c_int, [_I, _I]),
     "tp_launch_count": (C.c_int, [C.POINTER(C.c_int64)]),
     "tp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tp_profile_enable": (C.c_int, [_I]),

@@ -43,7 +43,8 @@ namespace tp {
 using namespace sm100;
 
 constexpr int kBM = 128, kBK = 64;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;
+constexpr int kMaxTmemBufs = 4;  // accumulator buffers: the MMA may run this many segments ahead
 constexpr int kThreads = 192;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kXchNodes = 32;           // epilogue exchange tile: 32 nodes x 128 features
@@ -103,13 +104,17 @@ SkPlan sk_plan(int n_out, int k, int n) {
   return p;
 }
 
+// Tuning knobs (tp_debug_gemm_knob): ring depth cap and smem budget.
+static int g_knob_max_stages = 8;
+static int g_knob_smem_kb = 200;
+
 static int stages_for(int n_pad) {
   const int per = kABytes + n_pad * 128;
-  return std::min(kMaxStages, (200 * 1024 - kXchBytes) / per);
+  return std::min(std::min(kMaxStages, g_knob_max_stages), (g_knob_smem_kb * 1024 - kXchBytes - 1024 - 512) / per);
 }
 
 static size_t smem_for(int n_pad) {
-  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + 256 /*barriers*/;
+  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + 512 /*barriers*/;  // 2*16 + 2*4 mbarriers + holder
 }
 
 // ---- device --------------------------------------------------------------------
@@ -263,7 +268,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // the TMA producer, the MMA issuer and the epilogue warps walk the same
 // sequence, the smem ring and the TMEM double buffer continuing across members.
 __global__ void __launch_bounds__(kThreads, 1)
-    sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages) {
+    sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages, int nbuf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
@@ -275,18 +280,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + kXchBytes);
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + kMaxTmemBufs;
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + kMaxTmemBufs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ncols = 32;
-  while (ncols < (uint32_t)(2 * grp.max_npad)) ncols <<= 1;
+  while (ncols < (uint32_t)(nbuf * grp.max_npad)) ncols <<= 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nbuf; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
@@ -351,8 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (t < t1) {
           const int mt = t / p.KB;
           const int seg_start = t, seg_end = min(t1, (mt + 1) * p.KB);
-          const int buf = seg & 1;
-          const uint32_t bphase = (seg >> 1) & 1;
+          const int buf = seg % nbuf;
+          const uint32_t bphase = (seg / nbuf) & 1;
           mbar_wait(&tempty[buf], bphase ^ 1);
           tc_fence_after();
           const uint32_t d = taddr + buf * grp.max_npad;
@@ -390,8 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (t < t1) {
         const int mt = t / p.KB;
         const int seg_end = min(t1, (mt + 1) * p.KB);
-        const int buf = seg & 1;
-        const uint32_t bphase = (seg >> 1) & 1;
+        const int buf = seg % nbuf;
+        const uint32_t bphase = (seg / nbuf) & 1;
         const int cfirst = sk_cta_of(p, mt * p.KB);
         const int clast = sk_cta_of(p, (mt + 1) * p.KB - 1);
         const int cnt = clast - cfirst + 1;
@@ -434,10 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           // ... and, if this segment ends the CTA's range of this member, reduce a
           // slice of the tile's nodes once every partial is in.  The contributors
           // whose ranges end inside the tile finish together; splitting the nodes
-          // among them keeps the fix-up short.  The tile's other contributor (at
-          // most one: the CTA whose range *starts* in the tile) published early in
-          // its pass over this member.  Waits only ever point at an earlier
-          // (member, position), so the chain cannot cycle.
+          // among them keeps the fix-up short (one CTA reducing a whole tile was
+          // measured 2x slower on the o / down projections).  The tile's other
+          // contributor (at most one: the CTA whose range *starts* in the tile)
+          // published early in its pass over this member.  Waits only ever point
+          // at an earlier (member, position), so the chain cannot cycle.
           if (t1 <= (mt + 1) * p.KB) {
             const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
             const int E = cend - cfirst + 1, rank = c - cfirst;
@@ -490,10 +496,11 @@ int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st) {
   TP_CHECK(grp.max_npad == mx, TP_ECONFIG, "GemmGroup.max_npad must be the members' largest n_pad");
   const int stages = stages_for(mx);
   const size_t smem = smem_for(mx);
+  const int nbuf = std::min(kMaxTmemBufs, 512 / mx);
   static size_t smem_set[64] = {0};  // per device
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
-  if (smem > smem_set[dev & 63]) {
+  if (smem != smem_set[dev & 63]) {
     TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set[dev & 63] = smem;
   }
@@ -517,7 +524,7 @@ int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ::tp::count_launch();
-  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, grp, p, stages));
+  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, grp, p, stages, nbuf));
   if (g_prof_on) {
     TP_CUDA(cudaEventRecord(rec.b, st));
     std::lock_guard<std::mutex> g(g_prof_mu);
@@ -561,6 +568,64 @@ extern "C" int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* lau
   *gemm_bytes = bytes;
   *launches = (int64_t)tp::g_prof.size();
   tp::g_prof.clear();
+  return TP_OK;
+}
+
+extern "C" int tp_debug_gemm_knob(int32_t knob, int32_t value) {
+  if (knob == 0) tp::g_knob_max_stages = value;
+  else if (knob == 1) tp::g_knob_smem_kb = value;
+  else return TP_ECONFIG;
+  return TP_OK;
+}
+
+// Grouped GEMM timing (count members: distinct weights / node rows / outputs).
+extern "C" int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* w_dev,
+                                         const void* const* x_dev, const int32_t* n, int32_t n_out, int32_t k,
+                                         void* const* out_dev, int32_t iters, float* ms_per_launch, void* stream) {
+  using namespace tp;
+  TP_CUDA(cudaSetDevice(device));
+  TP_CHECK(count >= 1 && count <= kMaxGroup && n_out % 128 == 0 && k % 64 == 0 && iters >= 1, TP_ESHAPE,
+           "debug GEMM shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  SkPlan p = sk_plan(n_out, k, 1);
+  GemmGroup grp;
+  grp.count = count;
+  grp.max_npad = 16;
+  std::vector<void*> bufs;
+  for (int g = 0; g < count; ++g) {
+    TP_CHECK(n[g] >= 1 && n[g] <= 256, TP_ESHAPE, "debug GEMM node count");
+    GemmMember& m = grp.m[g];
+    TP_TRY(make_tmap_kmajor(&m.a, w_dev[g], n_out, k, 128));
+    TP_TRY(make_tmap_kmajor(&m.b, x_dev[g], n[g], k, 16));
+    m.n = n[g];
+    m.n_pad = std::max(16, (n[g] + 15) / 16 * 16);
+    grp.max_npad = std::max(grp.max_npad, m.n_pad);
+    m.e = GemmEpi();
+    m.e.op = kOpStore;
+    m.e.out = (float*)out_dev[g];
+    m.e.out_ld = n_out;
+    SkPlan pg = p;
+    pg.n = n[g];
+    TP_CUDA(cudaMalloc((void**)&m.e.part, sk_part_floats(pg) * 4));
+    TP_CUDA(cudaMalloc((void**)&m.e.counters, 2 * p.mtiles * 4));
+    TP_CUDA(cudaMemsetAsync(m.e.counters, 0, 2 * p.mtiles * 4, st));
+    bufs.push_back(m.e.part);
+    bufs.push_back(m.e.counters);
+  }
+  TP_TRY(sk_gemm_group(grp, p, st));  // warm-up
+  cudaEvent_t a, b;
+  TP_CUDA(cudaEventCreate(&a));
+  TP_CUDA(cudaEventCreate(&b));
+  TP_CUDA(cudaEventRecord(a, st));
+  for (int i = 0; i < iters; ++i) TP_TRY(sk_gemm_group(grp, p, st));
+  TP_CUDA(cudaEventRecord(b, st));
+  TP_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  TP_CUDA(cudaEventElapsedTime(&ms, a, b));
+  *ms_per_launch = ms / iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  for (void* q : bufs) cudaFree(q);
   return TP_OK;
 }
 

@@ -105,6 +105,11 @@ int tp_model_verify(tp_model* m, tp_stage* ws, const void* hidden_dev, const int
 int tp_model_verify_async(tp_model* m, tp_stage* ws, const void* hidden_dev, const int32_t* child_tokens,
                           int32_t n_children, void* stream);
 int tp_model_verify_wait(tp_stage* ws, int32_t* result_host);
+/* greedy_token of n rows at once (one per request in a SpecPipe-DB tick):
+ * _async enqueues final norm + LM head (one GEMM for all rows) + per-row first
+ * argmax + the D2H; _wait returns the n tokens.                              */
+int tp_model_greedy_rows_async(tp_model* m, tp_stage* ws, int32_t n, const void* hidden_dev, void* stream);
+int tp_model_greedy_rows_wait(tp_model* m, int32_t n, int32_t* tokens_host);
 
 /* ---- stage: replaces KvCache (model.py:105-204) + forward_tree (:312-349) - */
 int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t capacity_rows,
@@ -122,6 +127,21 @@ int tp_stage_forward(tp_stage* s, const tp_level* level, const void* hidden_in, 
  * tp_stage_forward calls.  Stages must be distinct and share device + arch.   */
 int tp_stages_forward(int32_t count, tp_stage* const* stages, const tp_level* levels, const void* const* hidden_in,
                       void* const* hidden_out, void* stream);
+/* Ragged multi-request form (SpecPipe-DB combined step, batching.py:226-264):
+ * every item is one request's level on one of its stage caches; items with the
+ * same `member` (same layers, same model object) are concatenated into one
+ * ragged batch — one GEMM over all their node rows (weights streamed once per
+ * tick, not once per request), K/V scattered into each request's own cache,
+ * attention per request (block-diagonal by construction, batching.py:90-126).
+ * member_hidden_out[g] is the [sum_n, hidden] fp32 residual stream of member g,
+ * items in their order; member ids must be first-use ordered from 0.          */
+typedef struct tp_item {
+  tp_stage* stage;
+  tp_level level;
+  const void* hidden_in; /* device [n, hidden] rows, or NULL to embed level.tokens */
+  int32_t member;
+} tp_item;
+int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_hidden_out, void* stream);
 /* Pruning propagation (KvCache.promote/prune/_restrict/drop_speculative,
  * model.py:169-194): rows < first_row stay; of rows [first_row, first_row+count)
  * those with keep bit set are compacted stably to follow them; the rest and

@@ -47,6 +47,10 @@ class Level(C.Structure):
     ]
 
 
+class Item(C.Structure):
+    _fields_ = [("stage", C.c_void_p), ("level", Level), ("hidden_in", C.c_void_p), ("member", C.c_int32)]
+
+
 _P = C.c_void_p
 _I = C.c_int32
 _SIGS = {
@@ -70,6 +74,9 @@ _SIGS = {
     "tp_stage_reserve": (C.c_int, [_P, _I]),
     "tp_stage_forward": (C.c_int, [_P, C.POINTER(Level), _P, _P, _P]),
     "tp_stages_forward": (C.c_int, [_I, _P, _P, _P, _P, _P]),
+    "tp_items_forward": (C.c_int, [_I, _P, _P, _P]),
+    "tp_model_greedy_rows_async": (C.c_int, [_P, _P, _I, _P, _P]),
+    "tp_model_greedy_rows_wait": (C.c_int, [_P, _I, _P]),
     "tp_stage_compact": (C.c_int, [_P, _I, _I, _P, _P]),
     "tp_stage_truncate": (C.c_int, [_P, _I]),
     "tp_stage_read_kv": (C.c_int, [_P, _I, _I, _I, _I, _P]),

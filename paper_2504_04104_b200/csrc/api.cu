@@ -36,32 +36,7 @@ extern "C" int tp_io_bytes(int64_t* h2d, int64_t* d2h) {
 
 using namespace tp;
 
-namespace {
-
-struct ToyTensorSpec {
-  int64_t rows, cols;
-};
-
-// toy per-layer tensors in generation order (model.py:224-233)
-ToyTensorSpec toy_spec(int d, int which) {
-  switch (which) {
-    case 1: case 2: case 3: case 4: return {d, d};
-    case 5: return {d, 2 * d};
-    case 6: return {2 * d, d};
-  }
-  return {0, 0};
-}
-
-size_t meta_capacity(const tp_model* m, int cap, int* words) {
-  *words = (cap + 64) / 64 + 1;
-  size_t n = (size_t)std::max(m->cfg.max_nodes, 64);
-  size_t bytes = n * 4 * 4                       // tokens, positions, prefix rows, children
-                 + n * (size_t)(*words) * 8      // anc bits
-                 + (size_t)(cap + 64) * 4        // compaction / gather index lists
-                 + 256;
-  return (bytes + 255) & ~(size_t)255;
-}
-
+namespace tp {
 // Claim the next staging slot (waiting only if the stream has not yet executed
 // the upload that last used it); returns host + device addresses of the slot.
 int meta_slot(tp_stage* s, size_t bytes, char** host, char** dev, int* slot) {
@@ -91,6 +66,34 @@ int upload(tp_stage* s, const void* host, size_t bytes, cudaStream_t st, const c
   TP_TRY(meta_push(s, k, bytes, st));
   *dev_out = d;
   return TP_OK;
+}
+
+}  // namespace tp
+
+namespace {
+
+struct ToyTensorSpec {
+  int64_t rows, cols;
+};
+
+// toy per-layer tensors in generation order (model.py:224-233)
+ToyTensorSpec toy_spec(int d, int which) {
+  switch (which) {
+    case 1: case 2: case 3: case 4: return {d, d};
+    case 5: return {d, 2 * d};
+    case 6: return {2 * d, d};
+  }
+  return {0, 0};
+}
+
+size_t meta_capacity(const tp_model* m, int cap, int* words) {
+  *words = (cap + 64) / 64 + 1;
+  size_t n = (size_t)std::max(m->cfg.max_nodes, 64);
+  size_t bytes = n * 4 * 4                       // tokens, positions, prefix rows, children
+                 + n * (size_t)(*words) * 8      // anc bits
+                 + (size_t)(cap + 64) * 4        // compaction / gather index lists
+                 + 256;
+  return (bytes + 255) & ~(size_t)255;
 }
 
 int alloc_kv(tp_stage* s, int cap) {
@@ -338,6 +341,7 @@ int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t cap
   TP_CUDA(cudaMalloc((void**)&s->d_result, 16));
   TP_CUDA(cudaMallocHost((void**)&s->h_result, 16));
   TP_CUDA(cudaMalloc(&s->logits, (size_t)m->cfg.vocab * 8));
+  s->logits_rows = 1;
   if (!is_toy(m)) {
     rc = llama_stage_init(s);
     if (rc != TP_OK) {
@@ -467,28 +471,69 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
 int tp_stages_forward(int32_t count, tp_stage* const* stages, const tp_level* levels, const void* const* hidden_in,
                       void* const* hidden_out, void* stream) {
   TP_CHECK(count >= 1 && stages && levels && hidden_in && hidden_out, TP_ECONFIG, "null argument");
-  const int dev = stages[0]->m->cfg.device;
-  for (int g = 0; g < count; ++g) {
-    TP_CHECK(stages[g] && stages[g]->m->cfg.device == dev, TP_ECONFIG, "grouped stages must share one device");
-    TP_CHECK(stages[g]->m->cfg.arch == stages[0]->m->cfg.arch, TP_ECONFIG, "grouped stages must share the arch");
-    for (int h = 0; h < g; ++h) TP_CHECK(stages[h] != stages[g], TP_ECONFIG, "a stage appears twice in the group");
+  std::vector<tp_item> items(count);
+  for (int g = 0; g < count; ++g) items[g] = tp_item{stages[g], levels[g], hidden_in[g], g};
+  return tp_items_forward(count, items.data(), hidden_out, stream);
+}
+
+int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_hidden_out, void* stream) {
+  TP_CHECK(n_items >= 1 && items && member_hidden_out, TP_ECONFIG, "null argument");
+  tp_model* m0 = items[0].stage ? items[0].stage->m : nullptr;
+  TP_CHECK(m0, TP_ECONFIG, "null stage");
+  const int dev = m0->cfg.device;
+  int n_members = 0;
+  for (int i = 0; i < n_items; ++i) {
+    const tp_item& it = items[i];
+    TP_CHECK(it.stage && it.stage->m->cfg.device == dev, TP_ECONFIG, "forward items must share one device");
+    TP_CHECK(it.stage->m->cfg.arch == m0->cfg.arch, TP_ECONFIG, "forward items must share the arch");
+    TP_CHECK(it.member >= 0 && it.member <= i, TP_ECONFIG, "member ids must be first-use ordered from 0");
+    n_members = std::max(n_members, it.member + 1);
+    for (int h = 0; h < i; ++h) TP_CHECK(items[h].stage != it.stage, TP_ECONFIG, "a stage appears twice");
   }
   TP_CUDA(cudaSetDevice(dev));
   cudaStream_t st = (cudaStream_t)stream;
-  std::vector<LevelDev> lv(count);
-  for (int g = 0; g < count; ++g)
-    TP_TRY(prepare_level(stages[g], &levels[g], hidden_in[g], hidden_out[g], st, &lv[g]));
-  if (is_toy(stages[0]->m)) {
-    for (int g = 0; g < count; ++g) TP_TRY(toy_forward(stages[g], lv[g], hidden_in[g], hidden_out[g], st));
+  std::vector<LevelDev> lv(n_items);
+  for (int i = 0; i < n_items; ++i)
+    TP_TRY(prepare_level(items[i].stage, &items[i].level, items[i].hidden_in, member_hidden_out[items[i].member],
+                         st, &lv[i]));
+  if (is_toy(m0)) {
+    TP_CHECK(n_members == n_items, TP_ECONFIG, "toy arch: one item per member");
+    for (int i = 0; i < n_items; ++i)
+      TP_TRY(toy_forward(items[i].stage, lv[i], items[i].hidden_in, member_hidden_out[items[i].member], st));
   } else {
-    for (int g0 = 0; g0 < count; g0 += kMaxGroup) {
-      const int cnt = std::min(kMaxGroup, count - g0);
-      TP_TRY(llama_forward_group(stages + g0, lv.data() + g0, hidden_in + g0, hidden_out + g0, cnt, st));
-    }
+    std::vector<std::vector<FwdItem>> per(n_members);
+    for (int i = 0; i < n_items; ++i)
+      per[items[i].member].push_back(FwdItem{items[i].stage, lv[i], items[i].hidden_in});
+    std::vector<FwdMember> mem(n_members);
+    for (int g = 0; g < n_members; ++g)
+      mem[g] = FwdMember{per[g].data(), (int)per[g].size(), (float*)member_hidden_out[g]};
+    for (int g0 = 0; g0 < n_members; g0 += kMaxGroup)
+      TP_TRY(llama_forward_members(mem.data() + g0, std::min(kMaxGroup, n_members - g0), st));
   }
-  for (int g = 0; g < count; ++g)
-    if (levels[g].append) stages[g]->rows += levels[g].n;
+  for (int i = 0; i < n_items; ++i)
+    if (items[i].level.append) items[i].stage->rows += items[i].level.n;
   return TP_OK;
+}
+
+int tp_model_greedy_rows_async(tp_model* m, tp_stage* ws, int32_t n, const void* hidden_dev, void* stream) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  TP_CHECK(!is_toy(m), TP_ECONFIG, "multi-row verify is the llama path");
+  TP_CHECK(ws && ws->m == m, TP_ECONFIG, "workspace stage must belong to the model");
+  TP_CHECK(n >= 1 && n <= m->cfg.max_nodes, TP_ESHAPE, "rows outside [1, max_nodes]");
+  if (ws->logits_rows < n) {
+    TP_CUDA(cudaDeviceSynchronize());
+    if (ws->logits) cudaFree(ws->logits);
+    TP_CUDA(cudaMalloc(&ws->logits, (size_t)m->cfg.vocab * 8 * n));
+    ws->logits_rows = n;
+  }
+  TP_TRY(llama_greedy_rows_async(m, n, (const float*)hidden_dev, (float*)ws->logits, (cudaStream_t)stream));
+  count_io(0, 4LL * n);
+  return TP_OK;
+}
+
+int tp_model_greedy_rows_wait(tp_model* m, int32_t n, int32_t* tokens_host) {
+  TP_CUDA(cudaSetDevice(m->cfg.device));
+  return llama_greedy_rows_wait(m, n, tokens_host);
 }
 
 int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64_t* keep_bits, void* stream) {

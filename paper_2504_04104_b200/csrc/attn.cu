@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
 }
 
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
-  TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 8]");
+  TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 64]");
   AttnGroup G;
   G.count = count;
   int cs = 0, ct = 0;

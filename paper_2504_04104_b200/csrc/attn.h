@@ -8,7 +8,7 @@ namespace tp {
 constexpr int kAttnChunk = 64;     // logical key slots per canonical chunk
 constexpr int kAttnMaxExtra = 64;  // speculative ancestor rows per node
 constexpr int kAttnHeadDim = 128;
-constexpr int kAttnMaxGroup = 8;   // stages per grouped launch
+constexpr int kAttnMaxGroup = 64;  // (request, stage) items per grouped launch (large kernel params)
 
 struct AttnArgs {
   const __nv_bfloat16* q;  // [n][H*128]

@@ -196,10 +196,18 @@ __device__ __forceinline__ void epi_finish(const GemmEpi& e, int mt, int lane, i
       } else {
         const bool is_k = mt < e.H + e.KV;
         const int kh = is_k ? mt - e.H : mt - e.H - e.KV;
-        if (e.append)
+        if (e.items) {
+          const QkvItem& it = e.items[e.node_item[c]];
+          if (it.append)
+            dst = static_cast<__nv_bfloat16*>(it.planes[2 * (e.layer - it.lo) + (is_k ? 0 : 1)]) +
+                  ((size_t)kh * it.cap + it.row0 + (c - it.off)) * kBM;
+          else
+            dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
+        } else if (e.append) {
           dst = (is_k ? e.kc : e.vc) + ((size_t)kh * e.cap + e.row0 + c) * kBM;
-        else
+        } else {
           dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
+        }
       }
       st_bf16x4(dst + f, o.x, o.y, o.z, o.w);
     }

@@ -30,6 +30,14 @@ enum GemmOp : int {
   kOpSwiglu = 3,  // tile = 64 gate rows | 64 up rows: xf[node][mt*64 + i] = bf16(silu(g) * u)
 };
 
+// Per-request KV destination of a ragged (multi-request) QKV member: node c of
+// item it = items[node_item[c]] writes its K/V rows to that request's cache.
+struct QkvItem {
+  void* const* planes;  // the request-stage's [2*layers] K/V plane pointers (device)
+  int lo;               // first layer hosted by that stage
+  int cap, row0, append, off;  // plane rows, first appended row, append flag, first node of the item
+};
+
 struct GemmEpi {
   int op = kOpStore;
   float* out = nullptr;
@@ -38,6 +46,9 @@ struct GemmEpi {
   int H = 0, KV = 0, cap = 0, row0 = 0, append = 0;
   const float* rope = nullptr;  // [n][64][2] (cos, sin) per node position
   __nv_bfloat16 *xq = nullptr, *kc = nullptr, *vc = nullptr, *kself = nullptr, *vself = nullptr;
+  const QkvItem* items = nullptr;      // ragged member (nullptr: single request, fields above)
+  const int32_t* node_item = nullptr;  // [n]
+  int layer = 0;
   // kOpSwiglu
   __nv_bfloat16* xf = nullptr;
   int f = 0;

@@ -47,7 +47,8 @@ struct tp_stage {
   int32_t* d_result = nullptr;
   int32_t* h_result = nullptr;
   void** d_planes = nullptr;  // [2*layers] K/V plane bases for kv_compact
-  void* logits = nullptr;     // [vocab] verify scratch (f64 toy / f32 llama)
+  void* logits = nullptr;     // [logits_rows][vocab] verify scratch (f64 toy / f32 llama)
+  int logits_rows = 0;
   void* ext = nullptr;        // arch-specific state (llama: tensor maps, attention partials)
 };
 
@@ -83,8 +84,24 @@ int toy_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);
 // llama arch (llama.cu)
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out,
                   cudaStream_t st);
-int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* const* hidden_in,
-                        void* const* hidden_out, int count, cudaStream_t st);
+// One item = one request's level on one stage; a member = items sharing layers
+// (a ragged batch: rows concatenated in x, one GEMM member).
+struct FwdItem {
+  tp_stage* s;
+  LevelDev lv;
+  const void* hin;  // device rows or nullptr (embed tokens)
+};
+struct FwdMember {
+  const FwdItem* items;
+  int count;
+  float* x;  // [sum n, hidden] residual stream of the member
+};
+int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st);
+int llama_greedy_rows_async(tp_model* m, int n, const float* x, float* logits, cudaStream_t st);
+int llama_greedy_rows_wait(tp_model* m, int n, int32_t* out);
+int argmax_rows(const void* logits_f32, int vocab, int n, int32_t* d_out, cudaStream_t st);
+// metadata upload through a stage's staging ring (api.cu)
+int upload(tp_stage* s, const void* host, size_t bytes, cudaStream_t st, const char** dev_out);
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st);
 int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st);
 int llama_workspace_bytes(const tp_model* m, int max_nodes, size_t* bytes);

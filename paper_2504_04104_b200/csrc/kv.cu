@@ -144,4 +144,52 @@ int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_chi
   return TP_OK;
 }
 
+// One CTA per row: first argmax (lowest id wins ties) of n rows of fp32 logits.
+__global__ void __launch_bounds__(1024) argmax_rows_kernel(const float* __restrict__ logits, int V,
+                                                           int32_t* __restrict__ out) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* row = logits + (size_t)blockIdx.x * V;
+  float best = row[0];
+  int bi = 0;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float x = row[v];
+    if (better(x, v, best, bi)) {
+      best = x;
+      bi = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, best, bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = sv[0];
+    int ib = si[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (better(sv[k], si[k], b, ib)) {
+        b = sv[k];
+        ib = si[k];
+      }
+    out[blockIdx.x] = ib;
+  }
+}
+
+int argmax_rows(const void* logits_f32, int vocab, int n, int32_t* d_out, cudaStream_t st) {
+  ::tp::count_launch(), argmax_rows_kernel<<<n, 1024, 0, st>>>((const float*)logits_f32, vocab, d_out);
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
 }  // namespace tp

@@ -19,6 +19,7 @@
 // output, then rounded to bf16 for the cache / attention; softmax fp32.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 
 #include "attn.h"
 #include "gemm_tc.h"
@@ -28,12 +29,11 @@ namespace tp {
 
 enum { kCtrQkv = 0, kCtrO, kCtrGu, kCtrDown, kCtrHead, kCtrKinds };
 
-struct LlamaModelExt {
-  std::vector<CUtensorMap> qkv, o, gu, down;
-  CUtensorMap head;
-};
-
-struct LlamaStageExt {
+// Transient scratch of one member of a (grouped) forward: node-row operands of
+// the GEMMs, stream-K partials / counters, RoPE table, attention partials.
+// Owned by the model (a small pool, one per member slot of a grouped launch),
+// not by the stages, so hundreds of request caches carry no scratch.
+struct LlamaWs {
   int np = 0;  // padded node rows (multiple of 16)
   __nv_bfloat16 *Xd = nullptr, *Xo = nullptr, *Xf = nullptr, *Xq = nullptr;
   __nv_bfloat16 *kself = nullptr, *vself = nullptr;
@@ -47,8 +47,17 @@ struct LlamaStageExt {
   int max_chunks = 0;
 };
 
+struct LlamaModelExt {
+  std::vector<CUtensorMap> qkv, o, gu, down;
+  CUtensorMap head;
+  std::vector<LlamaWs*> ws;  // member workspaces
+  std::mutex mu;             // host-side enqueue of one forward at a time (worker threads)
+  int32_t* d_tok = nullptr;  // greedy tokens of a multi-row verify
+  int32_t* h_tok = nullptr;  // pinned
+  cudaEvent_t tok_ev = nullptr;
+};
+
 static LlamaModelExt* mext(tp_model* m) { return reinterpret_cast<LlamaModelExt*>(m->tma_cache); }
-static LlamaStageExt* sext(tp_stage* s) { return reinterpret_cast<LlamaStageExt*>(s->ext); }
 
 // ---- kernels --------------------------------------------------------------------
 
@@ -140,13 +149,27 @@ static int build_model_ext(tp_model* m) {
   return TP_OK;
 }
 
+static void ws_free(LlamaWs* e) {
+  if (!e) return;
+  for (void* p : {(void*)e->Xd, (void*)e->Xo, (void*)e->Xf, (void*)e->Xq, (void*)e->kself, (void*)e->vself,
+                  (void*)e->part, (void*)e->counters, (void*)e->rope, (void*)e->pm, (void*)e->pl, (void*)e->po})
+    if (p) cudaFree(p);
+  delete e;
+}
+
 void llama_model_free(tp_model* m) {
-  delete mext(m);
+  LlamaModelExt* me = mext(m);
+  if (!me) return;
+  for (LlamaWs* e : me->ws) ws_free(e);
+  if (me->d_tok) cudaFree(me->d_tok);
+  if (me->h_tok) cudaFreeHost(me->h_tok);
+  if (me->tok_ev) cudaEventDestroy(me->tok_ev);
+  delete me;
   m->tma_cache = nullptr;
 }
 
 int llama_workspace_bytes(const tp_model*, int, size_t* bytes) {
-  *bytes = 256;  // llama state lives in LlamaStageExt
+  *bytes = 256;  // llama scratch lives in the model workspace pool (llama.cu)
   return TP_OK;
 }
 
@@ -181,14 +204,14 @@ int llama_init_weights(tp_model* m, uint64_t seed, cudaStream_t st) {
   return build_model_ext(m);
 }
 
-int llama_stage_init(tp_stage* s) {
-  tp_model* m = s->m;
+// Workspace g of the model's pool, grown to hold `min_chunks` attention chunks.
+static int ws_get(tp_model* m, int g, int min_chunks, LlamaWs** out) {
+  LlamaModelExt* me = mext(m);
   const tp_model_config& c = m->cfg;
-  TP_TRY(build_model_ext(m));
-  LlamaStageExt* e = sext(s);
+  while ((int)me->ws.size() <= g) me->ws.push_back(nullptr);
+  LlamaWs*& e = me->ws[g];
   if (e == nullptr) {
-    e = new LlamaStageExt();
-    s->ext = e;
+    e = new LlamaWs();
     const int64_t d = c.hidden, q = (int64_t)c.heads * 128, kv = (int64_t)c.kv_heads * 128, f = c.ffn;
     e->np = (c.max_nodes + 15) / 16 * 16;
     const int64_t np = e->np;
@@ -224,30 +247,28 @@ int llama_stage_init(tp_stage* s) {
     TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
     TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));
   }
-  // attention chunk partials follow the KV capacity (+ ancestors + self)
-  const int chunks = (s->cap + kAttnMaxExtra + 1 + kAttnChunk - 1) / kAttnChunk;
-  if (chunks > e->max_chunks) {
+  if (min_chunks > e->max_chunks) {
+    // grows with the largest KV capacity seen (rare): drain in-flight users first
+    TP_CUDA(cudaDeviceSynchronize());
     if (e->pm) cudaFree(e->pm);
     if (e->pl) cudaFree(e->pl);
     if (e->po) cudaFree(e->po);
+    const int chunks = std::max(min_chunks, 2 * e->max_chunks);
     const size_t cells = (size_t)e->np * c.heads * chunks;
     TP_CUDA(cudaMalloc(&e->pm, cells * 4));
     TP_CUDA(cudaMalloc(&e->pl, cells * 4));
     TP_CUDA(cudaMalloc(&e->po, cells * 128 * 4));
     e->max_chunks = chunks;
   }
+  *out = e;
   return TP_OK;
 }
 
-void llama_stage_free(tp_stage* s) {
-  LlamaStageExt* e = sext(s);
-  if (!e) return;
-  for (void* p : {(void*)e->Xd, (void*)e->Xo, (void*)e->Xf, (void*)e->Xq, (void*)e->kself, (void*)e->vself,
-                  (void*)e->part, (void*)e->counters, (void*)e->rope, (void*)e->pm, (void*)e->pl, (void*)e->po})
-    if (p) cudaFree(p);
-  delete e;
-  s->ext = nullptr;
-}
+static int chunks_for_cap(int cap) { return (cap + kAttnMaxExtra + 1 + kAttnChunk - 1) / kAttnChunk; }
+
+int llama_stage_init(tp_stage* s) { return build_model_ext(s->m); }
+
+void llama_stage_free(tp_stage*) {}
 
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st) {
   TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
@@ -257,17 +278,18 @@ int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStr
   return TP_OK;
 }
 
-static GemmEpi epi_base(LlamaStageExt* e, int kind) {
+static GemmEpi epi_base(LlamaWs* e, int kind) {
   GemmEpi g;
   g.part = e->part;
   g.counters = e->counters + (size_t)kind * e->ctr_stride;
   return g;
 }
 
-int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits, cudaStream_t st) {
+static int logits_locked(tp_model* m, int n, const float* x, float* logits, cudaStream_t st) {
   TP_CHECK(m->head, TP_ECONFIG, "model has no LM head");
-  TP_TRY(llama_stage_init(ws));
-  LlamaStageExt* e = sext(ws);
+  TP_TRY(build_model_ext(m));
+  LlamaWs* e;
+  TP_TRY(ws_get(m, 0, 1, &e));
   const int d = m->cfg.hidden, V = m->cfg.vocab;
   ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
   TP_CUDA(cudaGetLastError());
@@ -276,6 +298,36 @@ int llama_logits(tp_model* m, tp_stage* ws, int n, const float* x, float* logits
   g.out = logits;
   g.out_ld = V;
   return sk_gemm(&mext(m)->head, &e->mXd, sk_plan(V, d, n), g, st);
+}
+
+int llama_logits(tp_model* m, tp_stage*, int n, const float* x, float* logits, cudaStream_t st) {
+  TP_TRY(build_model_ext(m));
+  std::lock_guard<std::mutex> lk(mext(m)->mu);
+  return logits_locked(m, n, x, logits, st);
+}
+
+int llama_greedy_rows_async(tp_model* m, int n, const float* x, float* logits, cudaStream_t st) {
+  TP_TRY(build_model_ext(m));
+  LlamaModelExt* me = mext(m);
+  std::lock_guard<std::mutex> lk(me->mu);
+  if (!me->d_tok) {
+    TP_CUDA(cudaMalloc(&me->d_tok, 4 * (size_t)std::max(64, m->cfg.max_nodes)));
+    TP_CUDA(cudaMallocHost(&me->h_tok, 4 * (size_t)std::max(64, m->cfg.max_nodes)));
+    TP_CUDA(cudaEventCreateWithFlags(&me->tok_ev, cudaEventDisableTiming));
+  }
+  TP_TRY(logits_locked(m, n, x, logits, st));
+  TP_TRY(argmax_rows(logits, m->cfg.vocab, n, me->d_tok, st));
+  TP_CUDA(cudaMemcpyAsync(me->h_tok, me->d_tok, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  TP_CUDA(cudaEventRecord(me->tok_ev, st));
+  return TP_OK;
+}
+
+int llama_greedy_rows_wait(tp_model* m, int n, int32_t* out) {
+  LlamaModelExt* me = mext(m);
+  TP_CHECK(me && me->tok_ev, TP_ECONFIG, "no multi-row verify in flight");
+  TP_CUDA(cudaEventSynchronize(me->tok_ev));
+  std::memcpy(out, me->h_tok, 4 * (size_t)n);
+  return TP_OK;
 }
 
 // Grouped rmsnorm: one CTA per (node row, member).
@@ -315,89 +367,136 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __gri
 }
 
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
-  tp_stage* ss[1] = {s};
-  const void* hin[1] = {hidden_in};
-  void* hout[1] = {hidden_out};
-  return llama_forward_group(ss, &lv, hin, hout, 1, st);
+  FwdItem it{s, lv, hidden_in};
+  FwdMember mb{&it, 1, (float*)hidden_out};
+  return llama_forward_members(&mb, 1, st);
 }
 
-// Several stages' levels on one device, layer slot by layer slot: slot j runs
-// layer lo_g + j of every member g that has one, each GEMM as ONE grouped
-// launch over the members (same segment boundaries as ungrouped launches, so
-// every member's bits equal its stand-alone forward).
-int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* const* hin, void* const* hout,
-                        int count, cudaStream_t st) {
-  TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "stage group size outside [1, 8]");
-  tp_model* m0 = ss[0]->m;
+// Members of a grouped forward run layer slot by layer slot: slot j runs layer
+// lo_g + j of every member g that has one, each GEMM as ONE grouped launch over
+// the members (same segment boundaries as ungrouped launches, so every member's
+// bits equal its stand-alone forward).  A member is a ragged batch of items —
+// one request each (SpecPipe-DB) — that share the member's layers: their node
+// rows are concatenated for the GEMMs (weights streamed once for all requests),
+// K/V rows are scattered to each request's cache, and attention runs per item.
+int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
+  TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "member group size outside [1, 8]");
+  tp_model* m0 = mem[0].items[0].s->m;
+  TP_TRY(build_model_ext(m0));
+  LlamaModelExt* me = mext(m0);
+  std::lock_guard<std::mutex> lk(me->mu);
   const tp_model_config& c = m0->cfg;
   const int d = c.hidden, H = c.heads, KV = c.kv_heads, f = c.ffn;
   const int q = H * 128, kvd = KV * 128;
+  LlamaWs* ws[kMaxGroup];
+  std::vector<int> offs[kMaxGroup];
+  int ntot[kMaxGroup], lo[kMaxGroup], hi[kMaxGroup];
   int slots = 0;
   for (int g = 0; g < count; ++g) {
-    tp_stage* s = ss[g];
-    const tp_model_config& cg = s->m->cfg;
-    TP_CHECK(cg.hidden == d && cg.heads == H && cg.kv_heads == KV && cg.ffn == f && cg.device == c.device,
-             TP_ECONFIG, "grouped stages must share the model shape and device");
-    TP_TRY(llama_stage_init(s));
-    const LevelDev& lv = lvs[g];
-    float* x = (float*)hout[g];
-    if (hin[g]) {
-      if (hin[g] != hout[g])
-        TP_CUDA(cudaMemcpyAsync(x, hin[g], (size_t)lv.n * d * 4, cudaMemcpyDeviceToDevice, st));
-    } else {
-      TP_TRY(llama_embed(s->m, lv.n, lv.tokens, x, st));
+    const FwdMember& M = mem[g];
+    TP_CHECK(M.count >= 1 && M.x, TP_ECONFIG, "empty forward member");
+    int cap_max = 1, n = 0;
+    lo[g] = M.items[0].lv.layer_lo;
+    hi[g] = M.items[0].lv.layer_hi;
+    for (int r = 0; r < M.count; ++r) {
+      const FwdItem& it = M.items[r];
+      TP_CHECK(it.s->m == m0, TP_ECONFIG, "grouped stages must share one model object");
+      TP_CHECK(it.lv.layer_lo == lo[g] && it.lv.layer_hi == hi[g], TP_ECONFIG,
+               "items of a member must run the same layers");
+      cap_max = std::max(cap_max, it.s->cap);
+      offs[g].push_back(n);
+      n += it.lv.n;
     }
-    slots = std::max(slots, lv.layer_hi - lv.layer_lo);
+    TP_CHECK(n <= c.max_nodes, TP_ESHAPE, "ragged member exceeds max_nodes");
+    ntot[g] = n;
+    TP_TRY(ws_get(m0, g, chunks_for_cap(cap_max), &ws[g]));
+    for (int r = 0; r < M.count; ++r) {
+      const FwdItem& it = M.items[r];
+      float* x = M.x + (size_t)offs[g][r] * d;
+      if (it.hin) {
+        if (it.hin != x) TP_CUDA(cudaMemcpyAsync(x, it.hin, (size_t)it.lv.n * d * 4, cudaMemcpyDeviceToDevice, st));
+      } else {
+        TP_TRY(llama_embed(m0, it.lv.n, it.lv.tokens, x, st));
+      }
+    }
+    slots = std::max(slots, hi[g] - lo[g]);
   }
   if (slots == 0) return TP_OK;
-  int maxn = 0;
+  // per-request KV destinations of ragged members (one small upload each)
+  const QkvItem* qitems[kMaxGroup] = {nullptr};
+  const int32_t* qnode[kMaxGroup] = {nullptr};
   for (int g = 0; g < count; ++g) {
-    const LevelDev& lv = lvs[g];
-    if (lv.layer_hi == lv.layer_lo) continue;
-    maxn = std::max(maxn, lv.n);
-    ::tp::count_launch(), rope_table_kernel<<<lv.n, 64, 0, st>>>(lv.positions, (double)c.rope_theta,
-                                                                  sext(ss[g])->rope);
-    TP_CUDA(cudaGetLastError());
+    const FwdMember& M = mem[g];
+    if (hi[g] == lo[g]) continue;
+    for (int r = 0; r < M.count; ++r) {
+      const FwdItem& it = M.items[r];
+      ::tp::count_launch(), rope_table_kernel<<<it.lv.n, 64, 0, st>>>(it.lv.positions, (double)c.rope_theta,
+                                                                     ws[g]->rope + (size_t)offs[g][r] * 128);
+      TP_CUDA(cudaGetLastError());
+    }
+    if (M.count > 1) {
+      std::vector<char> blob(sizeof(QkvItem) * M.count + 4 * (size_t)ntot[g]);
+      QkvItem* qi = reinterpret_cast<QkvItem*>(blob.data());
+      int32_t* ni = reinterpret_cast<int32_t*>(blob.data() + sizeof(QkvItem) * M.count);
+      for (int r = 0; r < M.count; ++r) {
+        const FwdItem& it = M.items[r];
+        qi[r] = QkvItem{it.s->d_planes, it.s->lo, it.s->cap, it.lv.row0, it.lv.append, offs[g][r]};
+        for (int i = 0; i < it.lv.n; ++i) ni[offs[g][r] + i] = r;
+      }
+      const char* dptr;
+      TP_TRY(upload(M.items[0].s, blob.data(), blob.size(), st, &dptr));
+      qitems[g] = reinterpret_cast<const QkvItem*>(dptr);
+      qnode[g] = reinterpret_cast<const int32_t*>(dptr + sizeof(QkvItem) * M.count);
+    }
   }
   const SkPlan pqkv = sk_plan(q + 2 * kvd, d, 1), po = sk_plan(d, q, 1), pgu = sk_plan(2 * f, d, 1),
                pdn = sk_plan(d, f, 1);
+  std::vector<AttnArgs> aa;
+  std::vector<LevelDev> al;
   for (int j = 0; j < slots; ++j) {
     int idx[kMaxGroup], na = 0;
     for (int g = 0; g < count; ++g)
-      if (lvs[g].layer_lo + j < lvs[g].layer_hi) idx[na++] = g;
+      if (lo[g] + j < hi[g]) idx[na++] = g;
     NormGroup ng;
     GemmGroup gq, go, ggu, gdn;
     gq.count = go.count = ggu.count = gdn.count = na;
-    int mx = 16;
+    int mx = 16, maxn = 0;
+    aa.clear();
+    al.clear();
     for (int a = 0; a < na; ++a) {
       const int g = idx[a];
-      tp_stage* s = ss[g];
-      const LevelDev& lv = lvs[g];
-      LlamaStageExt* e = sext(s);
-      LlamaModelExt* me = mext(s->m);
-      const int layer = lv.layer_lo + j, li = layer - s->m->cfg.layer_lo;
-      const int n = lv.n, npad = std::max(16, (n + 15) / 16 * 16);
+      const FwdMember& M = mem[g];
+      LlamaWs* e = ws[g];
+      const int layer = lo[g] + j, li = layer - c.layer_lo;
+      const int n = ntot[g], npad = std::max(16, (n + 15) / 16 * 16);
       mx = std::max(mx, npad);
-      float* x = (float*)hout[g];
-      ng.x[a] = x;
+      maxn = std::max(maxn, n);
+      ng.x[a] = M.x;
       ng.xd[a] = e->Xd;
       ng.n[a] = n;
+      const FwdItem& i0 = M.items[0];
       GemmEpi eq = epi_base(e, kCtrQkv);
       eq.op = kOpQkv;
       eq.H = H;
       eq.KV = KV;
-      eq.cap = s->cap;
-      eq.row0 = lv.row0;
-      eq.append = lv.append;
       eq.rope = e->rope;
       eq.xq = e->Xq;
       eq.kself = e->kself;
       eq.vself = e->vself;
-      eq.kc = (__nv_bfloat16*)s->k[layer - s->lo];
-      eq.vc = (__nv_bfloat16*)s->v[layer - s->lo];
+      eq.layer = layer;
+      if (M.count == 1) {
+        eq.cap = i0.s->cap;
+        eq.row0 = i0.lv.row0;
+        eq.append = i0.lv.append;
+        eq.kc = (__nv_bfloat16*)i0.s->k[layer - i0.s->lo];
+        eq.vc = (__nv_bfloat16*)i0.s->v[layer - i0.s->lo];
+      } else {
+        eq.items = qitems[g];
+        eq.node_item = qnode[g];
+      }
       GemmEpi er = epi_base(e, kCtrO);
       er.op = kOpResid;
-      er.out = x;
+      er.out = M.x;
       er.out_ld = d;
       GemmEpi ed = er;
       ed.counters = e->counters + (size_t)kCtrDown * e->ctr_stride;
@@ -416,6 +515,29 @@ int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* co
       set(go, me->o[li], e->mXo, er);
       set(ggu, me->gu[li], e->mXd, eg);
       set(gdn, me->down[li], e->mXf, ed);
+      for (int r = 0; r < M.count; ++r) {
+        const FwdItem& it = M.items[r];
+        const size_t off = offs[g][r];
+        AttnArgs x;
+        x.q = e->Xq + off * q;
+        x.q_stride = q;
+        x.k = (const __nv_bfloat16*)it.s->k[layer - it.s->lo];
+        x.v = (const __nv_bfloat16*)it.s->v[layer - it.s->lo];
+        x.cap = it.s->cap;
+        x.kself = it.lv.append ? nullptr : e->kself + off * kvd;
+        x.vself = it.lv.append ? nullptr : e->vself + off * kvd;
+        x.H = H;
+        x.KV = KV;
+        x.scale = (float)(1.0 / std::sqrt(128.0));
+        x.pm = e->pm + off * H * e->max_chunks;
+        x.pl = e->pl + off * H * e->max_chunks;
+        x.po = e->po + off * H * e->max_chunks * 128;
+        x.max_chunks = e->max_chunks;
+        x.out = e->Xo + off * q;
+        x.out_stride = q;
+        aa.push_back(x);
+        al.push_back(it.lv);
+      }
     }
     gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
     if (j == 0) {
@@ -423,44 +545,20 @@ int llama_forward_group(tp_stage* const* ss, const LevelDev* lvs, const void* co
       TP_CUDA(cudaGetLastError());
     }
     TP_TRY(sk_gemm_group(gq, pqkv, st));
-    AttnArgs aa[kMaxGroup];
-    LevelDev al[kMaxGroup];
-    for (int a = 0; a < na; ++a) {
-      const int g = idx[a];
-      tp_stage* s = ss[g];
-      const LevelDev& lv = lvs[g];
-      LlamaStageExt* e = sext(s);
-      AttnArgs& x = aa[a];
-      x.q = e->Xq;
-      x.q_stride = q;
-      x.cap = s->cap;
-      x.kself = lv.append ? nullptr : e->kself;
-      x.vself = lv.append ? nullptr : e->vself;
-      x.H = H;
-      x.KV = KV;
-      x.scale = (float)(1.0 / std::sqrt(128.0));
-      x.pm = e->pm;
-      x.pl = e->pl;
-      x.po = e->po;
-      x.max_chunks = e->max_chunks;
-      x.out = e->Xo;
-      x.out_stride = q;
-      x.k = gq.m[a].e.kc;
-      x.v = gq.m[a].e.vc;
-      al[a] = lv;
+    for (size_t a0 = 0; a0 < aa.size(); a0 += kAttnMaxGroup) {
+      const int cnt = (int)std::min<size_t>(kAttnMaxGroup, aa.size() - a0);
+      TP_TRY(attn_tree_group(aa.data() + a0, al.data() + a0, cnt, st));
     }
-    TP_TRY(attn_tree_group(aa, al, na, st));
     TP_TRY(sk_gemm_group(go, po, st));
     ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
     TP_CUDA(cudaGetLastError());
     TP_TRY(sk_gemm_group(ggu, pgu, st));
     TP_TRY(sk_gemm_group(gdn, pdn, st));
     // input norm of the next slot, for the members that continue
-    int nc = 0;
+    int nc = 0, maxc = 0;
     NormGroup nn;
-    int maxc = 0;
     for (int a = 0; a < na; ++a)
-      if (lvs[idx[a]].layer_lo + j + 1 < lvs[idx[a]].layer_hi) {
+      if (lo[idx[a]] + j + 1 < hi[idx[a]]) {
         nn.x[nc] = ng.x[a];
         nn.xd[nc] = ng.xd[a];
         nn.n[nc] = ng.n[a];

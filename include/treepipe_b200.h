@@ -159,6 +159,17 @@ int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t ro
 /* Grow the KV capacity (reference KvCache grow-by-doubling, model.py:141-148). */
 int tp_stage_reserve(tp_stage* s, int32_t capacity_rows);
 
+/* ---- host control: synthetic draft (token_source.py:73-111), pure host code ---
+ * Bit-exact restatement of the numpy draws of one synthetic_draft call
+ * (SeedSequence([seed, call_index]) -> PCG64 -> random / geometric / choice).
+ * oracle_next < 0 = no bound continuation.  TP_ECONFIG = a numpy branch not
+ * restated here (geometric with p < 1/3, tail-shuffle choice): use numpy.     */
+int tp_synthetic_draft(uint64_t seed, int64_t call_index, int32_t oracle_next, double top1_hit, double rank_decay,
+                       double miss_prob, int32_t k, int32_t vocab, int32_t* tokens_out, int32_t* n_out);
+int tp_synthetic_draft_batch(int32_t count, uint64_t seed, int64_t call_index0, const int32_t* oracle_next,
+                             double top1_hit, double rank_decay, double miss_prob, int32_t k, int32_t vocab,
+                             int32_t* tokens_out, int32_t* n_out);
+
 /* ---- instrumentation (no reference counterpart; used by bench.py) ---------- */
 /* Kernels launched by this library since load (every launch site counts). */
 int tp_launch_count(int64_t* out);

@@ -112,3 +112,54 @@ def test_bits_match_parent_pointers_and_roundtrip(seed):
     pruned, surv = tp.to_subtree_prune(t, r)
     tp.validate(pruned)
     assert np.array_equal(pruned.mask, t.mask[np.ix_(surv.indices(), surv.indices())])
+
+
+def test_native_synthetic_draft_bit_exact():
+    """The native restatement of numpy's SeedSequence/PCG64/choice draws equals
+    synthetic_draft (itself pinned to the reference by the golden fixtures)."""
+    import ctypes as C
+
+    from paper_2504_04104_b200 import _lib
+    from paper_2504_04104_b200.token_source import SyntheticDraftConfig, synthetic_draft
+
+    lib = _lib.load()
+    rng = np.random.default_rng(99)
+    checked = 0
+    for _ in range(3000):
+        V = int(rng.choice([16, 64, 512, 32000]))
+        k = int(rng.integers(1, min(V - 1, 33)))
+        miss = float(rng.choice([0.0, 0.01, 0.2]))
+        cfg = SyntheticDraftConfig(top1_hit=min(float(rng.choice([0.0, 0.62, 1.0])), 1 - miss),
+                                   rank_decay=float(rng.choice([0.0, 0.5, 0.6])), miss_prob=miss,
+                                   seed=int(rng.choice([0, 3, 2**35 + 1])))
+        idx = int(rng.integers(0, 1 << 30))
+        nxt = None if rng.random() < 0.2 else int(rng.integers(0, V))
+        want = [t for t, _ in synthetic_draft(cfg, nxt, k, idx, V)]
+        out = np.zeros(k, np.int32)
+        n = C.c_int32()
+        rc = lib.tp_synthetic_draft(cfg.seed, idx, -1 if nxt is None else nxt, cfg.top1_hit, cfg.rank_decay,
+                                    cfg.miss_prob, k, V, out.ctypes.data, C.byref(n))
+        assert rc == 0
+        assert out[: n.value].tolist() == want
+        checked += 1
+    assert checked == 3000
+
+
+@pytest.mark.parametrize("w,k,levels", [(64, 16, 6), (8, 4, 4), (3, 3, 7), (1, 2, 5)])
+def test_batched_expand_equals_per_node(w, k, levels):
+    """expand_fixed_width's native batched path == the per-node reference loop."""
+    V = 32000
+    truth = tuple(int(t) for t in np.random.default_rng(w * 7 + k).integers(0, V, 900))
+    ctx = truth[:300]
+    fast_d = tp.SyntheticDraft(tp.SyntheticDraftConfig(seed=4), V)
+    slow_d = tp.RecordingDraft(tp.SyntheticDraft(tp.SyntheticDraftConfig(seed=4), V))  # no propose_batch
+    fast_d.bind_reference(truth)
+    slow_d.bind_reference(truth)
+    beam = tp.BeamConfig(w=w, k=k)
+    tree = tp.new_root(ctx[-1], V)
+    for _ in range(levels):
+        a = tp.expand_fixed_width(tree, beam, fast_d, ctx)
+        b = tp.expand_fixed_width(tree, beam, slow_d, ctx)
+        assert a == b
+        tree = tp.layer_append(tree, a)
+    assert fast_d._calls == slow_d.inner._calls

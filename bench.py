@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=24)
+    ap.add_argument("--db-model", default="13b", choices=["7b", "13b", "70b", "tiny"])
+    ap.add_argument("--db-batches", default="1,16", help="SpecPipe-DB batch sizes (empty: skip)")
+    ap.add_argument("--db-new", type=int, default=24)
     return ap.parse_args()
 
 
@@ -83,26 +86,51 @@ def workload(args):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING a timed region, in-process
+    through NVML (nvidia-ml-py; an nvidia-smi subprocess per sample perturbed
+    the host loop it was measuring).  Falls back to nvidia-smi if NVML fails."""
 
-    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, gpu=0):
-        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
+    def __init__(self, gpu=0, period=0.05):
+        self.gpu, self.period, self.samples, self._stop = gpu, period, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            self._nvml = None
+            self.max_mhz = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            sm = float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            reasons = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+            return sm, reasons
+        out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        sm, mx = (float(x) for x in out.stdout.strip().split(","))
+        self.max_mhz = mx
+        return sm, 0
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                self.samples.append(self._sample())
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
+        self._stop.clear()
+        self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
@@ -112,13 +140,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def peaks():
@@ -283,6 +309,7 @@ def run_ours(args, rank, world):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     replay.host_s = {k: 0.0 for k in replay.host_s}
     th = time.perf_counter()
+    clocks.__enter__()
     e0.record(streams[0])
     for ch in children[args.warmup : args.warmup + args.steps]:
         node_layers += sum(len(s.resident) * (s.layer_range[1] - s.layer_range[0])
@@ -302,6 +329,7 @@ def run_ours(args, rank, world):
     e1.record(streams[0])
     host_loop_s = time.perf_counter() - th
     sync_all()
+    clocks.__exit__()
     host_diag = {k: round(v * 1e3 / args.steps, 4) for k, v in replay.host_s.items()}
     host_diag["loop_wall"] = round(host_loop_s * 1e3 / args.steps, 4)
     value_tokens = len(replay.emitted) - tok0
@@ -310,9 +338,13 @@ def run_ours(args, rank, world):
 
     # ---- GPU phase timeline of a few steps (diagnostic, separate from the timed run) -----
     replay.phase_events = []
+    _lib.timeline_enable(True)
+    _lib.timeline_read()
     for ch in children[args.warmup + args.steps : args.warmup + args.steps + 8]:
         replay.step(ch)
     sync_all()
+    _lib.timeline_enable(False)
+    kernel_tl = {k: round(v / 8, 4) for k, v in sorted(_lib.timeline_read().items(), key=lambda kv: -kv[1])}
     phases: dict[str, float] = {}
     evs = replay.phase_events
     for (ta, ea), (tb, eb) in zip(evs, evs[1:]):
@@ -360,6 +392,7 @@ def run_ours(args, rank, world):
                                                   "occupied stages + KV rows + LM head, per SURVEY 8d"},
         "host_ms_per_step": host_diag,
         "gpu_phase_ms_per_step": phase_diag,
+        "gpu_kernel_ms_per_step": kernel_tl,
         "clocks": clocks.summary(),
         "steps_per_token": round(steps_per_token, 4), "hit_rate": round(hit_rate, 4),
         "mean_resident_nodes": [round(float(x), 2) for x in np.mean(np.asarray(resident), axis=0)] if resident else None,
@@ -370,7 +403,32 @@ def run_ours(args, rank, world):
         ms, info = cpu_step_estimate(cfg, node_layers / max(1, len(resident)), 1.0, args.prompt_len)
         line["cpu_baseline"] = {"value": round(ms * steps_per_token, 2), "unit": UNIT, "cores": os.cpu_count(),
                                 "kind": "port", "sample": info["sample"]}
+    if rank == 0 and ngpu == 1 and args.db_batches:
+        line["specpipe_db"] = run_db(args)
     print(json.dumps(line), flush=True)
+
+
+def run_db(args):
+    """SpecPipe-DB (BASELINE config 5) on the same GPU: 13B-shape target, 8 stages,
+    total tree width 64, FIFO requests all arriving at tick 0; steady-state
+    tokens/s over the ticks where the whole batch is active (wall clock,
+    synchronised; host scheduling included)."""
+    import gc
+
+    import torch
+
+    from paper_2504_04104_b200.model import LlamaModel
+    from scripts.bench_db import measure_db
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    model = LlamaModel(model_cfg(args.db_model), max_nodes=64)
+    out = {"metric": "SpecPipe-DB tokens/s", "model": f"llama2-{args.db_model}-shape", "stages": 8,
+           "total_width": 64, "k": 16, "prompt_len": args.prompt_len, "new_tokens": args.db_new, "results": []}
+    for b in [int(x) for x in args.db_batches.split(",") if x]:
+        out["results"].append(measure_db(model, b, args.prompt_len, args.db_new))
+    del model
+    return out
 
 
 def main():

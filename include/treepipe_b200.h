@@ -193,6 +193,11 @@ int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, in
 int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
                               const int32_t* n, int32_t n_out, int32_t k, void* const* out_dev, int32_t iters,
                               float* ms_per_launch, void* stream);
+/* GPU timeline (diagnostics): while enabled, CUDA events between kernel groups;
+ * _read returns "tag=ms;..." (GPU time since the previous mark on the stream,
+ * summed per tag) and resets.                                                 */
+int tp_timeline_enable(int32_t on);
+int tp_timeline_read(char* buf, int32_t len);
 /* Tuning knobs of K2 (0: ring depth cap, 1: smem budget in KB); process-wide. */
 int tp_debug_gemm_knob(int32_t knob, int32_t value);
 

@@ -89,6 +89,8 @@ _SIGS = {
                                       _P, _P]),
     "tp_synthetic_draft_batch": (C.c_int, [_I, C.c_uint64, C.c_int64, _P, C.c_double, C.c_double, C.c_double,
                                             _I, _I, _P, _P]),
+    "tp_timeline_enable": (C.c_int, [_I]),
+    "tp_timeline_read": (C.c_int, [C.c_char_p, _I]),
     "tp_launch_count": (C.c_int, [C.POINTER(C.c_int64)]),
     "tp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tp_profile_enable": (C.c_int, [_I]),
@@ -116,6 +118,21 @@ def profile_read() -> tuple[float, float, int]:
     ms, by, n = C.c_double(), C.c_double(), C.c_int64()
     check(load().tp_profile_read(C.byref(ms), C.byref(by), C.byref(n)))
     return ms.value, by.value, n.value
+
+def timeline_enable(on: bool) -> None:
+    check(load().tp_timeline_enable(int(on)))
+
+
+def timeline_read() -> dict[str, float]:
+    buf = C.create_string_buffer(1 << 16)
+    check(load().tp_timeline_read(buf, len(buf)))
+    out = {}
+    for part in buf.value.decode().split(";"):
+        if part:
+            k, v = part.split("=")
+            out[k] = float(v)
+    return out
+
 
 EXPORTED = tuple(_SIGS)
 

@@ -23,6 +23,61 @@ static void count_io(long long h2d, long long d2h) {
 }
 }  // namespace tp
 
+// ---- optional GPU timeline: events between kernel groups, aggregated per tag ----
+namespace tp {
+struct TlRec {
+  const char* tag;
+  cudaEvent_t ev;
+  cudaStream_t st;
+};
+static std::vector<TlRec> g_tl;
+static bool g_tl_on = false;
+static std::mutex g_tl_mu;
+void timeline_mark(const char* tag, cudaStream_t st) {
+  if (!g_tl_on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  std::lock_guard<std::mutex> g(g_tl_mu);
+  g_tl.push_back({tag, e, st});
+}
+}  // namespace tp
+
+extern "C" int tp_timeline_enable(int32_t on) {
+  tp::g_tl_on = on != 0;
+  return TP_OK;
+}
+
+// "tag=ms;tag=ms;..." : GPU time from the previous mark on the same stream to
+// each mark, summed per tag; resets the record.
+extern "C" int tp_timeline_read(char* buf, int32_t len) {
+  std::lock_guard<std::mutex> g(tp::g_tl_mu);
+  std::vector<std::pair<std::string, double>> acc;
+  for (size_t i = 0; i < tp::g_tl.size(); ++i) {
+    auto& r = tp::g_tl[i];
+    cudaEventSynchronize(r.ev);
+    for (size_t j = i; j-- > 0;)
+      if (tp::g_tl[j].st == r.st) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tp::g_tl[j].ev, r.ev);
+        bool found = false;
+        for (auto& a : acc)
+          if (a.first == r.tag) {
+            a.second += ms;
+            found = true;
+          }
+        if (!found) acc.push_back({r.tag, ms});
+        break;
+      }
+  }
+  for (auto& r : tp::g_tl) cudaEventDestroy(r.ev);
+  tp::g_tl.clear();
+  std::string out;
+  for (auto& a : acc) out += a.first + "=" + std::to_string(a.second) + ";";
+  std::snprintf(buf, (size_t)len, "%s", out.c_str());
+  return TP_OK;
+}
+
 extern "C" int tp_launch_count(int64_t* out) {
   *out = tp::g_launches.load();
   return TP_OK;
@@ -400,6 +455,7 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   TP_CHECK(hidden_in || (L->tokens && m->embed), TP_ECONFIG, "need hidden_in or tokens + embedding");
   TP_CHECK(L->words >= 0 && L->words <= s->max_words, TP_ESHAPE, "too many mask words for this stage");
   TP_CHECK(!L->append || s->rows + n <= s->cap, TP_ESHAPE, "KV capacity exceeded (reserve first)");
+  timeline_mark("host_gap", st);  // GPU time since the previous mark: idle or other work
   const int visible = s->rows + (L->append ? n : 0);
   int max_t = 0;
   for (int i = 0; i < n; ++i) {
@@ -549,6 +605,7 @@ int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64
     const char* d;
     TP_TRY(upload(s, src.data(), src.size() * 4, st, &d));
     TP_TRY(kv_compact(s, (const int32_t*)d, (int)src.size(), first_row, s->d_planes, st));
+    timeline_mark("kv_compact", st);
   }
   s->rows = first_row + (int)src.size();
   return TP_OK;
@@ -611,6 +668,7 @@ int tp_model_verify_async(tp_model* m, tp_stage* ws, const void* hidden_dev, con
   TP_TRY(argmax_match(ws->logits, is_toy(m), m->cfg.vocab, (const int32_t*)d, n_children, ws->d_result, st));
   TP_CUDA(cudaMemcpyAsync(ws->h_result, ws->d_result, 8, cudaMemcpyDeviceToHost, st));
   count_io(0, 8);
+  timeline_mark("verify_head", st);
   TP_CUDA(cudaEventRecord(ws->verify_ev, st));
   return TP_OK;
 }
@@ -640,7 +698,9 @@ int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t ro
   cudaStream_t st = (cudaStream_t)stream;
   const char* d;
   TP_TRY(upload(ws, idx.data(), idx.size() * 4, st, &d));
-  return rows_compact(src_dev, dst_dev, row_bytes, (const int32_t*)d, (int)idx.size(), st);
+  TP_TRY(rows_compact(src_dev, dst_dev, row_bytes, (const int32_t*)d, (int)idx.size(), st));
+  timeline_mark("rows_compact", st);
+  return TP_OK;
 }
 
 }  // extern "C"

@@ -99,6 +99,7 @@ struct FwdMember {
 int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st);
 int llama_greedy_rows_async(tp_model* m, int n, const float* x, float* logits, cudaStream_t st);
 int llama_greedy_rows_wait(tp_model* m, int n, int32_t* out);
+void timeline_mark(const char* tag, cudaStream_t st);  // no-op unless enabled
 int argmax_rows(const void* logits_f32, int vocab, int n, int32_t* d_out, cudaStream_t st);
 // metadata upload through a stage's staging ring (api.cu)
 int upload(tp_stage* s, const void* host, size_t bytes, cudaStream_t st, const char** dev_out);

@@ -317,6 +317,7 @@ int llama_greedy_rows_async(tp_model* m, int n, const float* x, float* logits, c
   }
   TP_TRY(logits_locked(m, n, x, logits, st));
   TP_TRY(argmax_rows(logits, m->cfg.vocab, n, me->d_tok, st));
+  timeline_mark("verify_head", st);
   TP_CUDA(cudaMemcpyAsync(me->h_tok, me->d_tok, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
   TP_CUDA(cudaEventRecord(me->tok_ev, st));
   return TP_OK;
@@ -451,6 +452,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
   }
   const SkPlan pqkv = sk_plan(q + 2 * kvd, d, 1), po = sk_plan(d, q, 1), pgu = sk_plan(2 * f, d, 1),
                pdn = sk_plan(d, f, 1);
+  timeline_mark("fwd_prep", st);
   std::vector<AttnArgs> aa;
   std::vector<LevelDev> al;
   for (int j = 0; j < slots; ++j) {
@@ -545,15 +547,21 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
       TP_CUDA(cudaGetLastError());
     }
     TP_TRY(sk_gemm_group(gq, pqkv, st));
+    timeline_mark("gemm_qkv", st);
     for (size_t a0 = 0; a0 < aa.size(); a0 += kAttnMaxGroup) {
       const int cnt = (int)std::min<size_t>(kAttnMaxGroup, aa.size() - a0);
       TP_TRY(attn_tree_group(aa.data() + a0, al.data() + a0, cnt, st));
     }
+    timeline_mark("attention", st);
     TP_TRY(sk_gemm_group(go, po, st));
+    timeline_mark("gemm_o", st);
     ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
     TP_CUDA(cudaGetLastError());
+    timeline_mark("rmsnorm", st);
     TP_TRY(sk_gemm_group(ggu, pgu, st));
+    timeline_mark("gemm_gate_up", st);
     TP_TRY(sk_gemm_group(gdn, pdn, st));
+    timeline_mark("gemm_down", st);
     // input norm of the next slot, for the members that continue
     int nc = 0, maxc = 0;
     NormGroup nn;
@@ -568,6 +576,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
     if (nc) {
       ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxc, nc), kNormThreads, 0, st>>>(nn, d, c.norm_eps);
       TP_CUDA(cudaGetLastError());
+      timeline_mark("rmsnorm", st);
     }
   }
   return TP_OK;

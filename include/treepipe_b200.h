@@ -193,6 +193,9 @@ int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, in
 int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
                               const int32_t* n, int32_t n_out, int32_t k, void* const* out_dev, int32_t iters,
                               float* ms_per_launch, void* stream);
+/* K1 routing (tests): 0 forces the per-node tail path for every level, 1 (default)
+ * runs uniform tree levels through the 16-node tile path.                      */
+int tp_debug_attn_tile(int32_t on);
 /* GPU timeline (diagnostics): while enabled, CUDA events between kernel groups;
  * _read returns "tag=ms;..." (GPU time since the previous mark on the stream,
  * summed per tag) and resets.                                                 */

@@ -6,6 +6,7 @@
 #include <mutex>
 #include <string>
 
+#include "attn.h"
 #include "gemm_tc.h"
 #include "internal.h"
 
@@ -42,6 +43,11 @@ void timeline_mark(const char* tag, cudaStream_t st) {
   g_tl.push_back({tag, e, st});
 }
 }  // namespace tp
+
+extern "C" int tp_debug_attn_tile(int32_t on) {
+  tp::attn_set_tile(on != 0);
+  return TP_OK;
+}
 
 extern "C" int tp_timeline_enable(int32_t on) {
   tp::g_tl_on = on != 0;
@@ -457,10 +463,12 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   TP_CHECK(!L->append || s->rows + n <= s->cap, TP_ESHAPE, "KV capacity exceeded (reserve first)");
   timeline_mark("host_gap", st);  // GPU time since the previous mark: idle or other work
   const int visible = s->rows + (L->append ? n : 0);
-  int max_t = 0;
+  int max_t = 0, uniform_a = -2;
   for (int i = 0; i < n; ++i) {
     int pc = 0;
     for (int w = 0; w < L->words; ++w) pc += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
+    if (uniform_a == -2) uniform_a = pc;
+    else if (uniform_a != pc || L->prefix_rows[i] != L->prefix_rows[0]) uniform_a = -1;
     TP_CHECK(is_toy(m) || pc <= 64, TP_ESHAPE, "more than 64 speculative ancestors per node");
     max_t = std::max(max_t, L->prefix_rows[i] + pc + 1);
     TP_CHECK(L->prefix_rows[i] >= 0 && L->prefix_rows[i] <= visible, TP_ECONTRACT, "prefix rows beyond cache");
@@ -495,6 +503,7 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   lv.bits_base = L->bits_base;
   lv.max_t = max_t;
   lv.min_p = *std::min_element(L->prefix_rows, L->prefix_rows + n);
+  lv.uniform_a = uniform_a;
   const bool all_layers = L->layer_lo == 0 && L->layer_hi == 0;
   const bool no_layers = L->layer_lo < 0;  // explicit empty range: embed/copy only
   lv.layer_lo = all_layers ? s->lo : (no_layers ? s->lo : L->layer_lo);

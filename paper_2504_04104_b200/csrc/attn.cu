@@ -36,6 +36,7 @@ constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ld
 constexpr int kCtaNodes = 64;
 constexpr int kWarps = 4;
 constexpr int kTileElems = kAttnChunk * kPad;
+static bool g_attn_tile = true;  // tp_debug_attn_tile(0) forces the per-node path (tests)
 constexpr size_t kTailSmem = (size_t)kWarps * kTileElems * 2 + (size_t)kWarps * (kAttnChunk + kAttnMaxExtra) * 4;
 
 __device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) {
@@ -61,6 +62,11 @@ __device__ __forceinline__ void cp16(void* dst, const void* src, int src_bytes) 
                : "memory");
 }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -78,11 +84,11 @@ __device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t (&r)[4]) {
 //   qa   : Q A-fragments (8 k-steps over head_dim)
 //   lim  : rows g / g+8 see slots [0, lim) of this chunk
 // Returns the chunk max m, sum l and the bf16 P A-fragments.
-__device__ __forceinline__ void chunk_scores(const uint32_t (&qa)[8][4], const __nv_bfloat16* sK,
-                                             const int (&lim)[2], float scale, float (&m)[2], float (&l)[2],
-                                             uint32_t (&pa)[4][4], int lane) {
-  const int tig = lane & 3, mi = lane >> 3, mr = lane & 7;
-  float s[8][4];
+// Raw scores s = Q.K^T of one 64-slot chunk for the warp's 16-row tile, K
+// staged in sK[slot][kPad].
+__device__ __forceinline__ void tile_qk(const uint32_t (&qa)[8][4], const __nv_bfloat16* sK, float (&s)[8][4],
+                                        int lane) {
+  const int mi = lane >> 3, mr = lane & 7;
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
     s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
@@ -94,6 +100,13 @@ __device__ __forceinline__ void chunk_scores(const uint32_t (&qa)[8][4], const _
       mma16816(s[nt], qa[2 * k2 + 1], b[2], b[3]);
     }
   }
+}
+
+// Chunk softmax of the raw scores: rows g / g+8 see slots [0, lim); returns the
+// chunk max m, sum l and the bf16 P A-fragments.
+__device__ __forceinline__ void chunk_softmax(float (&s)[8][4], const int (&lim)[2], float scale, float (&m)[2],
+                                              float (&l)[2], uint32_t (&pa)[4][4], int lane) {
+  const int tig = lane & 3;
   float mc[2] = {-INFINITY, -INFINITY};
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt)
@@ -135,6 +148,14 @@ __device__ __forceinline__ void chunk_scores(const uint32_t (&qa)[8][4], const _
   }
 }
 
+__device__ __forceinline__ void chunk_scores(const uint32_t (&qa)[8][4], const __nv_bfloat16* sK,
+                                             const int (&lim)[2], float scale, float (&m)[2], float (&l)[2],
+                                             uint32_t (&pa)[4][4], int lane) {
+  float s[8][4];
+  tile_qk(qa, sK, s, lane);
+  chunk_softmax(s, lim, scale, m, l, pa, lane);
+}
+
 // o = P . V for the chunk, V staged in sV[slot][kPad] (ldmatrix.trans B fragments).
 __device__ __forceinline__ void chunk_pv(const uint32_t (&pa)[4][4], const __nv_bfloat16* sV, float (&o)[16][4],
                                          int lane) {
@@ -168,9 +189,11 @@ __device__ __forceinline__ size_t part_idx(const AttnArgs& a, int node, int h, i
   return ((size_t)node * a.H + h) * a.max_chunks + c;
 }
 
-__device__ __forceinline__ int member_of(const AttnGroup& G, int b, bool tail) {
+// kind: 0 shared, 1 per-node tail, 2 tile
+__device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
+  auto start = [&](int g) { return kind == 0 ? G.m[g].cta_shared : (kind == 1 ? G.m[g].cta_tail : G.m[g].cta_tile); };
   int gi = 0;
-  while (gi + 1 < G.count && b >= (tail ? G.m[gi + 1].cta_tail : G.m[gi + 1].cta_shared)) ++gi;
+  while (gi + 1 < G.count && b >= start(gi + 1)) ++gi;
   return gi;
 }
 
@@ -178,7 +201,7 @@ __device__ __forceinline__ int member_of(const AttnGroup& G, int b, bool tail) {
 __global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_constant__ AttnGroup G) {
   __shared__ __align__(16) __nv_bfloat16 sK[kTileElems];
   __shared__ __align__(16) __nv_bfloat16 sV[kTileElems];
-  const int gi = member_of(G, blockIdx.x, false);
+  const int gi = member_of(G, blockIdx.x, 0);
   const AttnArgs& a = G.m[gi].a;
   const LevelDev& lv = G.m[gi].lv;
   int local = blockIdx.x - G.m[gi].cta_shared;
@@ -243,7 +266,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_c
 __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_constant__ AttnGroup G) {
   pdl_trigger();  // the O-projection GEMM may start streaming its weights
   extern __shared__ __align__(16) uint8_t dsm[];
-  const int gi = member_of(G, blockIdx.x, true);
+  const int gi = member_of(G, blockIdx.x, 1);
   const AttnArgs& a = G.m[gi].a;
   const LevelDev& lv = G.m[gi].lv;
   int local = blockIdx.x - G.m[gi].cta_tail;
@@ -380,11 +403,296 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
   *reinterpret_cast<uint2*>(out) = u;
 }
 
+
+// ---------------------------------------------------------------------------
+// Tree levels (every node has the same prefix P and the same number A of
+// speculative ancestors — the common case, `uniform_a` >= 0): one warp per
+// 16-node tile.  A tail chunk's slots below P are the same K/V rows for every
+// node: they are staged once per CTA and run as ordinary tile MMAs.  Only the
+// node's own slots [P, P+A] (ancestors + self, <= kTileOwn) differ: for those
+// n-tiles / k-groups the node runs alone in row 0 of an MMA (the per-lane
+// ldmatrix addresses mix shared and own rows), exactly the arithmetic of the
+// per-node path, with its accumulator moved to row 0 and back by shuffles.
+// Per element the operations and their order are those of attn_tail_kernel,
+// so the result is bit-identical to it (and to sequential decode).
+constexpr int kTileOwn = 16;
+constexpr int kOwnElems = kTileOwn * kPad;
+constexpr size_t kTileWarpBytes = (size_t)2 * kOwnElems * 2 + (size_t)16 * kTileOwn * 4;
+constexpr size_t kTileSmem = (size_t)2 * kTileElems * 2 + (size_t)kPad * 2 + kWarps * kTileWarpBytes;
+
+__global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_constant__ AttnGroup G) {
+  pdl_trigger();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int gi = member_of(G, blockIdx.x, 2);
+  const AttnArgs& a = G.m[gi].a;
+  const LevelDev& lv = G.m[gi].lv;
+  const int local = blockIdx.x - G.m[gi].cta_tile;
+  const int h = local % a.H, base = (local / a.H) * kCtaNodes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3, mi = lane >> 3, mr = lane & 7;
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(dsm);
+  __nv_bfloat16* sV = sK + kTileElems;
+  __nv_bfloat16* zrow = sV + kTileElems;
+  uint8_t* wb = reinterpret_cast<uint8_t*>(zrow + kPad) + warp * kTileWarpBytes;
+  __nv_bfloat16* own0 = reinterpret_cast<__nv_bfloat16*>(wb);
+  __nv_bfloat16* own1 = own0 + kOwnElems;
+  int* extra = reinterpret_cast<int*>(own1 + kOwnElems);  // [16][kTileOwn]
+  const int kh = h / (a.H / a.KV);
+  const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
+  const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
+  const int P = lv.min_p, A = lv.uniform_a, T = P + A + 1;
+  const int t0 = base + warp * 16;
+  const int nv = min(16, lv.n - t0);
+  for (int e = threadIdx.x; e < kPad; e += blockDim.x) zrow[e] = __float2bfloat16_rn(0.f);
+  if (lane < nv) {  // lane r decodes node t0 + r's ancestor rows (A of them, in row order)
+    int cnt = 0;
+    for (int w = 0; w < lv.words && cnt < A; ++w) {
+      uint64_t bits = lv.anc[(size_t)(t0 + lane) * lv.words + w];
+      while (bits && cnt < A) {
+        extra[lane * kTileOwn + cnt++] = lv.bits_base + w * 64 + (__ffsll((long long)bits) - 1);
+        bits &= bits - 1;
+      }
+    }
+  }
+  const bool va = g < nv, vb = g + 8 < nv;
+  const __nv_bfloat16* qra = a.q + (size_t)(t0 + g) * a.q_stride + h * kAttnHeadDim;
+  const __nv_bfloat16* qrb = a.q + (size_t)(t0 + g + 8) * a.q_stride + h * kAttnHeadDim;
+  // running state of rows g / g+8 (fragment layout)
+  float M[2] = {-INFINITY, -INFINITY}, L[2] = {0.f, 0.f}, O[16][4];
+#pragma unroll
+  for (int nd = 0; nd < 16; ++nd) O[nd][0] = O[nd][1] = O[nd][2] = O[nd][3] = 0.f;
+  const int c_start = G.m[gi].c_shared;
+  for (int c = 0; c < c_start; ++c) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int r = g + 8 * hh;
+      if (r >= nv) continue;
+      const size_t idx = part_idx(a, t0 + r, h, c);
+      float sa, sb;
+      merge_scale(M[hh], L[hh], __ldcg(a.pm + idx), __ldcg(a.pl + idx), sa, sb);
+      const float* po = a.po + idx * kAttnHeadDim + 2 * tig;
+#pragma unroll
+      for (int nd = 0; nd < 16; ++nd) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(po + nd * 8));
+        O[nd][2 * hh] = merge_val(O[nd][2 * hh], v.x, sa, sb);
+        O[nd][2 * hh + 1] = merge_val(O[nd][2 * hh + 1], v.y, sa, sb);
+      }
+    }
+  }
+  __syncwarp();
+  // own row o (0..A-1 ancestors, A self) of node t0 + r; nullptr beyond
+  auto own_src = [&](int r, int o, bool isv) -> const __nv_bfloat16* {
+    if (o < A) return (isv ? Vh : Kh) + (size_t)extra[r * kTileOwn + o] * kAttnHeadDim;
+    if (o == A) {
+      const int i = t0 + r;
+      const __nv_bfloat16* self = isv ? a.vself : a.kself;
+      return self ? self + ((size_t)i * a.KV + kh) * kAttnHeadDim
+                  : (isv ? Vh : Kh) + (size_t)(lv.row0 + i) * kAttnHeadDim;
+    }
+    return nullptr;
+  };
+  auto stage_own = [&](int r, __nv_bfloat16* dst, bool isv) {
+#pragma unroll 4
+    for (int e = lane; e < kTileOwn * 16; e += 32) {
+      const int o = e >> 4, part = e & 15;
+      const __nv_bfloat16* src = own_src(r, o, isv);
+      cp16(dst + o * kPad + part * 8, (src ? src : Kh) + part * 8, src ? 16 : 0);
+    }
+    cp_commit();
+  };
+  const int c_end = (T + kAttnChunk - 1) / kAttnChunk;
+  for (int c = c_start; c < c_end; ++c) {
+    const int j0 = c * kAttnChunk;
+    __syncthreads();  // every warp is done with the previous chunk's shared rows
+#pragma unroll
+    for (int e = threadIdx.x; e < kAttnChunk * 16; e += kWarps * 32) {
+      const int row = e >> 4, part = e & 15, j = j0 + row;
+      const bool ok = j < P;
+      cp16(sK + row * kPad + part * 8, Kh + (size_t)(ok ? j : 0) * kAttnHeadDim + part * 8, ok ? 16 : 0);
+      cp16(sV + row * kPad + part * 8, Vh + (size_t)(ok ? j : 0) * kAttnHeadDim + part * 8, ok ? 16 : 0);
+    }
+    cp_wait_all();
+    __syncthreads();
+    if (nv <= 0) continue;
+    const int lo_slot = max(P - j0, 0), hi_slot = min(T - j0, kAttnChunk);  // own slots of this chunk
+    auto rowp = [&](const __nv_bfloat16* shared_tile, const __nv_bfloat16* own, int slot) {
+      const int ja = j0 + slot;
+      return ja < P ? shared_tile + slot * kPad : (ja < T ? own + (ja - P) * kPad : zrow);
+    };
+    uint32_t qa[8][4];  // reloaded per chunk (L2): keeps registers free for the P.V phase
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      qa[kk][0] = va ? ld_b32(qra + 16 * kk + 2 * tig) : 0u;
+      qa[kk][1] = vb ? ld_b32(qrb + 16 * kk + 2 * tig) : 0u;
+      qa[kk][2] = va ? ld_b32(qra + 16 * kk + 8 + 2 * tig) : 0u;
+      qa[kk][3] = vb ? ld_b32(qrb + 16 * kk + 8 + 2 * tig) : 0u;
+    }
+    float s[8][4];
+    tile_qk(qa, sK, s, lane);
+    if (lo_slot < hi_slot) {
+      const int nt0 = lo_slot >> 3, nt1 = (hi_slot - 1) >> 3;
+      stage_own(0, own0, false);
+      for (int r = 0; r < nv; ++r) {
+        __nv_bfloat16* own = (r & 1) ? own1 : own0;
+        if (r + 1 < nv) {
+          stage_own(r + 1, (r & 1) ? own0 : own1, false);
+          cp_wait_group<1>();
+        } else {
+          cp_wait_group<0>();
+        }
+        __syncwarp();
+        const int src_lane = (r & 7) * 4 + tig, hr = r >> 3;
+        uint32_t q1[8][4];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t v0 = __shfl_sync(0xffffffffu, hr ? qa[kk][1] : qa[kk][0], src_lane);
+          const uint32_t v2 = __shfl_sync(0xffffffffu, hr ? qa[kk][3] : qa[kk][2], src_lane);
+          q1[kk][0] = g == 0 ? v0 : 0u;
+          q1[kk][1] = 0u;
+          q1[kk][2] = g == 0 ? v2 : 0u;
+          q1[kk][3] = 0u;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          if (nt < nt0 || nt > nt1) continue;
+          float s1[4] = {0.f, 0.f, 0.f, 0.f};
+          const __nv_bfloat16* rp = rowp(sK, own, nt * 8 + mr);
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            uint32_t b[4];
+            ldsm4(su32(rp + 32 * k2 + 8 * mi), b);
+            mma16816(s1, q1[2 * k2], b[0], b[1]);
+            mma16816(s1, q1[2 * k2 + 1], b[2], b[3]);
+          }
+          const float e0 = __shfl_sync(0xffffffffu, s1[0], tig), e1 = __shfl_sync(0xffffffffu, s1[1], tig);
+          if (g == (r & 7)) {
+            if (hr) {
+              s[nt][2] = e0;
+              s[nt][3] = e1;
+            } else {
+              s[nt][0] = e0;
+              s[nt][1] = e1;
+            }
+          }
+        }
+        __syncwarp();  // buffer `own` may be restaged for node r + 2
+      }
+    }
+    const int lim[2] = {g < nv ? min(T - j0, kAttnChunk) : 0, g + 8 < nv ? min(T - j0, kAttnChunk) : 0};
+    float m[2], l[2];
+    uint32_t pa[4][4];
+    chunk_softmax(s, lim, a.scale, m, l, pa, lane);
+    float o[16][4];
+#pragma unroll
+    for (int nd = 0; nd < 16; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+    const bool any_own = lo_slot < hi_slot;
+    const int kk_lo = any_own ? lo_slot >> 4 : 4, kk_hi = any_own ? (hi_slot - 1) >> 4 : 3;
+    auto tile_group = [&](int kk) {
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) {
+        uint32_t b[4];
+        ldsm4t(su32(sV + (16 * kk + 8 * (mi & 1) + mr) * kPad + 16 * n2 + 8 * (mi >> 1)), b);
+        mma16816(o[2 * n2], pa[kk], b[0], b[1]);
+        mma16816(o[2 * n2 + 1], pa[kk], b[2], b[3]);
+      }
+    };
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (kk < kk_lo) tile_group(kk);
+    if (any_own) {
+      stage_own(0, own0, true);
+      for (int r = 0; r < nv; ++r) {
+        __nv_bfloat16* own = (r & 1) ? own1 : own0;
+        if (r + 1 < nv) {
+          stage_own(r + 1, (r & 1) ? own0 : own1, true);
+          cp_wait_group<1>();
+        } else {
+          cp_wait_group<0>();
+        }
+        __syncwarp();
+        const int src_lane = (r & 7) * 4 + tig, hr = r >> 3;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {  // n-tiles 8*half .. 8*half+7 (accumulators independent per n-tile)
+          float acc[8][4];
+#pragma unroll
+          for (int q8 = 0; q8 < 8; ++q8) {
+            const int nd = 8 * half + q8;
+            const float c0 = __shfl_sync(0xffffffffu, hr ? o[nd][2] : o[nd][0], src_lane);
+            const float c1 = __shfl_sync(0xffffffffu, hr ? o[nd][3] : o[nd][1], src_lane);
+            acc[q8][0] = g == 0 ? c0 : 0.f;
+            acc[q8][1] = g == 0 ? c1 : 0.f;
+            acc[q8][2] = acc[q8][3] = 0.f;
+          }
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (kk < kk_lo || kk > kk_hi) continue;
+            uint32_t p1[4];
+            const uint32_t v0 = __shfl_sync(0xffffffffu, hr ? pa[kk][1] : pa[kk][0], src_lane);
+            const uint32_t v2 = __shfl_sync(0xffffffffu, hr ? pa[kk][3] : pa[kk][2], src_lane);
+            p1[0] = g == 0 ? v0 : 0u;
+            p1[1] = 0u;
+            p1[2] = g == 0 ? v2 : 0u;
+            p1[3] = 0u;
+            const __nv_bfloat16* rp = rowp(sV, own, 16 * kk + 8 * (mi & 1) + mr);
+#pragma unroll
+            for (int n4 = 0; n4 < 4; ++n4) {
+              const int n2 = 4 * half + n4;
+              uint32_t b[4];
+              ldsm4t(su32(rp + 16 * n2 + 8 * (mi >> 1)), b);
+              mma16816(acc[2 * n4], p1, b[0], b[1]);
+              mma16816(acc[2 * n4 + 1], p1, b[2], b[3]);
+            }
+          }
+#pragma unroll
+          for (int q8 = 0; q8 < 8; ++q8) {
+            const int nd = 8 * half + q8;
+            const float e0 = __shfl_sync(0xffffffffu, acc[q8][0], tig);
+            const float e1 = __shfl_sync(0xffffffffu, acc[q8][1], tig);
+            if (g == (r & 7)) {
+              if (hr) {
+                o[nd][2] = e0;
+                o[nd][3] = e1;
+              } else {
+                o[nd][0] = e0;
+                o[nd][1] = e1;
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (kk > kk_hi) tile_group(kk);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      float sa, sb;
+      merge_scale(M[hh], L[hh], m[hh], l[hh], sa, sb);
+#pragma unroll
+      for (int nd = 0; nd < 16; ++nd) {
+        O[nd][2 * hh] = merge_val(O[nd][2 * hh], o[nd][2 * hh], sa, sb);
+        O[nd][2 * hh + 1] = merge_val(O[nd][2 * hh + 1], o[nd][2 * hh + 1], sa, sb);
+      }
+    }
+  }
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int r = g + 8 * hh;
+    if (r >= nv) continue;
+    __nv_bfloat16* out = a.out + (size_t)(t0 + r) * a.out_stride + h * kAttnHeadDim + 2 * tig;
+#pragma unroll
+    for (int nd = 0; nd < 16; ++nd)
+      *reinterpret_cast<uint32_t*>(out + nd * 8) =
+          pack_f32(__fdiv_rn(O[nd][2 * hh], L[hh]), __fdiv_rn(O[nd][2 * hh + 1], L[hh]));
+  }
+}
+
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
   TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 64]");
   AttnGroup G;
   G.count = count;
-  int cs = 0, ct = 0;
+  int cs = 0, ct = 0, cg = 0;
   for (int g = 0; g < count; ++g) {
     AttnMember& m = G.m[g];
     m.a = a[g];
@@ -393,29 +701,47 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     m.zt = (lv[g].n + kCtaNodes - 1) / kCtaNodes;
     const int c_max = (lv[g].max_t + kAttnChunk - 1) / kAttnChunk;
     TP_CHECK(c_max <= a[g].max_chunks, TP_ESHAPE, "attention chunks exceed scratch");
+    const bool tiled = g_attn_tile && lv[g].uniform_a >= 0 && lv[g].uniform_a + 1 <= kTileOwn && lv[g].n >= 4;
     m.cta_shared = cs;
     m.cta_tail = ct;
+    m.cta_tile = cg;
     cs += a[g].H * m.c_shared * m.zt;
-    ct += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
+    if (tiled)
+      cg += a[g].H * m.zt;
+    else
+      ct += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
   }
   G.ctas_shared = cs;
   G.ctas_tail = ct;
+  G.ctas_tile = cg;
   static bool attr_set[64] = {false};  // per device
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
   if (!attr_set[dev & 63]) {
     TP_CUDA(cudaFuncSetAttribute(attn_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmem));
+    TP_CUDA(cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
     attr_set[dev & 63] = true;
   }
   if (cs > 0) {
     ::tp::count_launch(), attn_shared_kernel<<<cs, kWarps * 32, 0, st>>>(G);
     TP_CUDA(cudaGetLastError());
+    timeline_mark("attn_shared", st);
   }
-  ::tp::count_launch(), attn_tail_kernel<<<ct, kWarps * 32, kTailSmem, st>>>(G);
-  TP_CUDA(cudaGetLastError());
+  if (cg > 0) {
+    ::tp::count_launch(), attn_tile_kernel<<<cg, kWarps * 32, kTileSmem, st>>>(G);
+    TP_CUDA(cudaGetLastError());
+    timeline_mark("attn_tile", st);
+  }
+  if (ct > 0) {
+    ::tp::count_launch(), attn_tail_kernel<<<ct, kWarps * 32, kTailSmem, st>>>(G);
+    TP_CUDA(cudaGetLastError());
+    timeline_mark("attn_tail", st);
+  }
   return TP_OK;
 }
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st) { return attn_tree_group(&a, &lv, 1, st); }
+
+void attn_set_tile(bool on) { g_attn_tile = on; }
 
 }  // namespace tp

@@ -35,16 +35,18 @@ struct AttnMember {
   int c_shared;    // chunks inside every node's verified prefix
   int zt;          // 64-node blocks
   int cta_shared;  // first CTA of this member in the shared launch
-  int cta_tail;    // first CTA of this member in the tail launch
+  int cta_tail;    // first CTA of this member in the per-node tail launch (empty range if tiled)
+  int cta_tile;    // first CTA of this member in the 16-node tile launch (empty range if per-node)
 };
 
 struct AttnGroup {
   AttnMember m[kAttnMaxGroup];
   int count;
-  int ctas_shared, ctas_tail;
+  int ctas_shared, ctas_tail, ctas_tile;
 };
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
+void attn_set_tile(bool on);
 // members[0..count) -> two launches (shared chunks, then per-node tail + ordered combine)
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st);
 

@@ -64,6 +64,7 @@ struct LevelDev {
   int layer_lo, layer_hi;  // layers to run
   int max_t;               // longest logical key sequence (prefix + ancestors + self)
   int min_p;               // smallest prefix_rows over the level's nodes
+  int uniform_a;           // every node has this many ancestors and prefix min_p (-1: ragged level)
   const int32_t* tokens;
   const int32_t* positions;
   const int32_t* prefix_rows;

@@ -552,7 +552,6 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
       const int cnt = (int)std::min<size_t>(kAttnMaxGroup, aa.size() - a0);
       TP_TRY(attn_tree_group(aa.data() + a0, al.data() + a0, cnt, st));
     }
-    timeline_mark("attention", st);
     TP_TRY(sk_gemm_group(go, po, st));
     timeline_mark("gemm_o", st);
     ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);

@@ -263,3 +263,47 @@ def test_llama_long_context_invariance_and_oracle():
         x = o.run_position(o.embed(tok, pos), okv, list(range(len(okv))), pos=pos, prefix=True)
     got = together[0].numpy()
     assert float(np.abs(got - x).max()) <= TOL * max(1.0, float(np.abs(x).max()))
+
+
+@pytest.mark.parametrize("w,k", [(16, 4), (24, 8)])
+def test_tile_attention_equals_per_node_path(w, k):
+    """The 16-node tile path of K1 (uniform tree levels) is bit-identical to the
+    per-node path on every stage output of a wide-tree pipeline run."""
+    cfg, m, _ = tiny_model(layers=4)
+    prompt = [int(t) for t in np.random.default_rng(6).integers(0, cfg.vocab, 150)]
+    ref = tp.sequential_decode(m, prompt, 40)
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.7, rank_decay=0.5, miss_prob=0.05, seed=9),
+                              cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(ref))
+    from paper_2504_04104_b200.pipeline import PipelineRunner
+
+    rec = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=w, k=k), draft, collect_trace=False)
+    rec.children_log = []
+    rec.prefill(prompt)
+    while len(rec.emitted) < 16:
+        rec.decode_step()
+    assert rec.emitted == ref[: len(rec.emitted)]
+    lib = _lib.lib()
+    runs = {}
+    try:
+        for tile in (1, 0):
+            _lib.check(lib.tp_debug_attn_tile(tile))
+            r = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=w, k=k), None,
+                               collect_trace=False)
+            r.prefill(prompt)
+            outs = []
+            for ch in rec.children_log:
+                r.launch_compute()
+                outs.append([None if s.out is None else s.out.cpu().clone() for s in r.stages])
+                r.step(ch)
+            runs[tile] = outs
+    finally:
+        _lib.check(lib.tp_debug_attn_tile(1))
+    wide = 0
+    for a_, b_ in zip(runs[1], runs[0]):
+        for x, y in zip(a_, b_):
+            assert (x is None) == (y is None)
+            if x is not None:
+                assert torch.equal(x, y)
+                wide += x.shape[0] >= 4
+    assert wide > 5

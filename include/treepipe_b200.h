@@ -196,6 +196,8 @@ int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* 
 /* K1 routing (tests): 0 forces the per-node tail path for every level, 1 (default)
  * runs uniform tree levels through the 16-node tile path.                      */
 int tp_debug_attn_tile(int32_t on);
+/* K1 knobs: 0 = tile path on/off (as above), 1 = shared-prefix chunks per CTA (1..4). */
+int tp_debug_attn_knob(int32_t knob, int32_t value);
 /* GPU timeline (diagnostics): while enabled, CUDA events between kernel groups;
  * _read returns "tag=ms;..." (GPU time since the previous mark on the stream,
  * summed per tag) and resets.                                                 */

@@ -49,6 +49,13 @@ extern "C" int tp_debug_attn_tile(int32_t on) {
   return TP_OK;
 }
 
+extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
+  if (knob == 0) tp::attn_set_tile(value != 0);
+  else if (knob == 1) tp::attn_set_shared_run(value);
+  else return TP_ECONFIG;
+  return TP_OK;
+}
+
 extern "C" int tp_timeline_enable(int32_t on) {
   tp::g_tl_on = on != 0;
   return TP_OK;

@@ -36,7 +36,7 @@ constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ld
 constexpr int kCtaNodes = 64;
 constexpr int kWarps = 4;
 constexpr int kTileElems = kAttnChunk * kPad;
-static bool g_attn_tile = true;  // tp_debug_attn_tile(0) forces the per-node path (tests)
+static bool g_attn_tile = false;  // measured slower than the per-node tail on the bench workload  // tp_debug_attn_tile(0) forces the per-node path (tests)
 constexpr size_t kTailSmem = (size_t)kWarps * kTileElems * 2 + (size_t)kWarps * (kAttnChunk + kAttnMaxExtra) * 4;
 
 __device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) {
@@ -66,6 +66,15 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// wait until at most `ahead` (0..3) committed groups are still pending
+__device__ __forceinline__ void cp_wait_ahead(int ahead) {
+  switch (ahead) {
+    case 0: cp_wait_group<0>(); break;
+    case 1: cp_wait_group<1>(); break;
+    case 2: cp_wait_group<2>(); break;
+    default: cp_wait_group<3>(); break;
+  }
 }
 
 __device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
@@ -198,35 +207,47 @@ __device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
 }
 
 // Chunks inside every node's verified prefix: rows [64c, 64c+64) for all nodes.
-__global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_constant__ AttnGroup G) {
-  __shared__ __align__(16) __nv_bfloat16 sK[kTileElems];
-  __shared__ __align__(16) __nv_bfloat16 sV[kTileElems];
+// A CTA walks kSharedRun consecutive chunks of one (member, head, 64-node
+// block), staging chunk c+1 (cp.async, double-buffered) while chunk c computes;
+// every chunk's partial is stored separately, exactly as one CTA per chunk.
+constexpr int kSharedRunMax = 4;
+constexpr size_t kSharedSmem = (size_t)4 * kTileElems * 2;  // 2 x (K, V) chunk tiles
+static int g_shared_run = 1;  // chunks per CTA (tp_debug_attn_knob 1)
+
+__global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_constant__ AttnGroup G, int run_len) {
+  extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 0);
   const AttnArgs& a = G.m[gi].a;
   const LevelDev& lv = G.m[gi].lv;
+  const int runs = (G.m[gi].c_shared + run_len - 1) / run_len;
   int local = blockIdx.x - G.m[gi].cta_shared;
   const int h = local % a.H;
   local /= a.H;
-  const int c = local % G.m[gi].c_shared, base = (local / G.m[gi].c_shared) * kCtaNodes;
+  const int run = local % runs, base = (local / runs) * kCtaNodes;
+  const int c0 = run * run_len, c1 = min(G.m[gi].c_shared, c0 + run_len);
   const int kh = h / (a.H / a.KV);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int nreal = min(kCtaNodes, lv.n - base);
-  const int j0 = c * kAttnChunk;
-  const __nv_bfloat16* Kh = a.k + ((size_t)kh * a.cap + j0) * kAttnHeadDim;
-  const __nv_bfloat16* Vh = a.v + ((size_t)kh * a.cap + j0) * kAttnHeadDim;
+  __nv_bfloat16* tiles = reinterpret_cast<__nv_bfloat16*>(dsm);  // [2][K | V][kTileElems]
+  auto stage = [&](int c, int buf) {
+    const __nv_bfloat16* Kh = a.k + ((size_t)kh * a.cap + (size_t)c * kAttnChunk) * kAttnHeadDim;
+    const __nv_bfloat16* Vh = a.v + ((size_t)kh * a.cap + (size_t)c * kAttnChunk) * kAttnHeadDim;
+    __nv_bfloat16* sK = tiles + (size_t)buf * 2 * kTileElems;
+    __nv_bfloat16* sV = sK + kTileElems;
 #pragma unroll
-  for (int e = threadIdx.x; e < kAttnChunk * 16; e += kWarps * 32) {
-    const int row = e >> 4, part = e & 15;
-    cp16(sK + row * kPad + part * 8, Kh + row * kAttnHeadDim + part * 8, 16);
-    cp16(sV + row * kPad + part * 8, Vh + row * kAttnHeadDim + part * 8, 16);
-  }
-  cp_wait_all();
-  __syncthreads();
+    for (int e = threadIdx.x; e < kAttnChunk * 16; e += kWarps * 32) {
+      const int row = e >> 4, part = e & 15;
+      cp16(sK + row * kPad + part * 8, Kh + row * kAttnHeadDim + part * 8, 16);
+      cp16(sV + row * kPad + part * 8, Vh + row * kAttnHeadDim + part * 8, 16);
+    }
+    cp_commit();
+  };
+  stage(c0, 0);
   const int r0 = warp * 16;
-  if (r0 >= nreal) return;
+  const bool active = r0 < nreal;
   const int ia = base + r0 + g, ib = ia + 8;
-  const bool va = r0 + g < nreal, vb = r0 + g + 8 < nreal;
+  const bool va = active && r0 + g < nreal, vb = active && r0 + g + 8 < nreal;
   uint32_t qa[8][4];
   {
     const __nv_bfloat16* qra = a.q + (size_t)ia * a.q_stride + h * kAttnHeadDim;
@@ -240,22 +261,36 @@ __global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_c
     }
   }
   const int lim[2] = {va ? kAttnChunk : 0, vb ? kAttnChunk : 0};
-  float m[2], l[2], o[16][4];
-  uint32_t pa[4][4];
-  chunk_scores(qa, sK, lim, a.scale, m, l, pa, lane);
-  chunk_pv(pa, sV, o, lane);
-#pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    if (!(hh ? vb : va)) continue;
-    const size_t idx = part_idx(a, hh ? ib : ia, h, c);
-    float* po = a.po + idx * kAttnHeadDim;
-#pragma unroll
-    for (int nd = 0; nd < 16; ++nd)
-      *reinterpret_cast<float2*>(po + nd * 8 + 2 * tig) = make_float2(o[nd][2 * hh], o[nd][2 * hh + 1]);
-    if (tig == 0) {
-      a.pm[idx] = m[hh];
-      a.pl[idx] = l[hh];
+  for (int c = c0; c < c1; ++c) {
+    const int buf = (c - c0) & 1;
+    if (c + 1 < c1) {
+      stage(c + 1, buf ^ 1);
+      cp_wait_group<1>();
+    } else {
+      cp_wait_group<0>();
     }
+    __syncthreads();
+    if (active) {
+      const __nv_bfloat16* sK = tiles + (size_t)buf * 2 * kTileElems;
+      float m[2], l[2], o[16][4];
+      uint32_t pa[4][4];
+      chunk_scores(qa, sK, lim, a.scale, m, l, pa, lane);
+      chunk_pv(pa, sK + kTileElems, o, lane);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        if (!(hh ? vb : va)) continue;
+        const size_t idx = part_idx(a, hh ? ib : ia, h, c);
+        float* po = a.po + idx * kAttnHeadDim;
+#pragma unroll
+        for (int nd = 0; nd < 16; ++nd)
+          *reinterpret_cast<float2*>(po + nd * 8 + 2 * tig) = make_float2(o[nd][2 * hh], o[nd][2 * hh + 1]);
+        if (tig == 0) {
+          a.pm[idx] = m[hh];
+          a.pl[idx] = l[hh];
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` is restaged for chunk c + 2
   }
 }
 
@@ -417,7 +452,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
 // so the result is bit-identical to it (and to sequential decode).
 constexpr int kTileOwn = 16;
 constexpr int kOwnElems = kTileOwn * kPad;
-constexpr size_t kTileWarpBytes = (size_t)2 * kOwnElems * 2 + (size_t)16 * kTileOwn * 4;
+constexpr int kOwnRing = 4;  // per-warp ring of staged own-row tiles: nodes r+1..r+3 load while r computes
+constexpr size_t kTileWarpBytes = (size_t)kOwnRing * kOwnElems * 2 + (size_t)16 * kTileOwn * 4;
 constexpr size_t kTileSmem = (size_t)2 * kTileElems * 2 + (size_t)kPad * 2 + kWarps * kTileWarpBytes;
 
 __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_constant__ AttnGroup G) {
@@ -434,9 +470,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_con
   __nv_bfloat16* sV = sK + kTileElems;
   __nv_bfloat16* zrow = sV + kTileElems;
   uint8_t* wb = reinterpret_cast<uint8_t*>(zrow + kPad) + warp * kTileWarpBytes;
-  __nv_bfloat16* own0 = reinterpret_cast<__nv_bfloat16*>(wb);
-  __nv_bfloat16* own1 = own0 + kOwnElems;
-  int* extra = reinterpret_cast<int*>(own1 + kOwnElems);  // [16][kTileOwn]
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(wb);
+  int* extra = reinterpret_cast<int*>(ring + kOwnRing * kOwnElems);  // [16][kTileOwn]
   const int kh = h / (a.H / a.KV);
   const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
   const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
@@ -491,9 +526,9 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_con
     }
     return nullptr;
   };
-  auto stage_own = [&](int r, __nv_bfloat16* dst, bool isv) {
+  auto stage_own = [&](int r, __nv_bfloat16* dst, bool isv) {  // only the A+1 rows ever read
 #pragma unroll 4
-    for (int e = lane; e < kTileOwn * 16; e += 32) {
+    for (int e = lane; e < (A + 1) * 16; e += 32) {
       const int o = e >> 4, part = e & 15;
       const __nv_bfloat16* src = own_src(r, o, isv);
       cp16(dst + o * kPad + part * 8, (src ? src : Kh) + part * 8, src ? 16 : 0);
@@ -531,15 +566,12 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_con
     tile_qk(qa, sK, s, lane);
     if (lo_slot < hi_slot) {
       const int nt0 = lo_slot >> 3, nt1 = (hi_slot - 1) >> 3;
-      stage_own(0, own0, false);
+      for (int p = 0; p < min(kOwnRing - 1, nv); ++p) stage_own(p, ring + (p % kOwnRing) * kOwnElems, false);
       for (int r = 0; r < nv; ++r) {
-        __nv_bfloat16* own = (r & 1) ? own1 : own0;
-        if (r + 1 < nv) {
-          stage_own(r + 1, (r & 1) ? own0 : own1, false);
-          cp_wait_group<1>();
-        } else {
-          cp_wait_group<0>();
-        }
+        __nv_bfloat16* own = ring + (r % kOwnRing) * kOwnElems;
+        if (r + kOwnRing - 1 < nv)
+          stage_own(r + kOwnRing - 1, ring + ((r + kOwnRing - 1) % kOwnRing) * kOwnElems, false);
+        cp_wait_ahead(min(kOwnRing - 1, nv - 1 - r));
         __syncwarp();
         const int src_lane = (r & 7) * 4 + tig, hr = r >> 3;
         uint32_t q1[8][4];
@@ -600,15 +632,12 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_con
     for (int kk = 0; kk < 4; ++kk)
       if (kk < kk_lo) tile_group(kk);
     if (any_own) {
-      stage_own(0, own0, true);
+      for (int p = 0; p < min(kOwnRing - 1, nv); ++p) stage_own(p, ring + (p % kOwnRing) * kOwnElems, true);
       for (int r = 0; r < nv; ++r) {
-        __nv_bfloat16* own = (r & 1) ? own1 : own0;
-        if (r + 1 < nv) {
-          stage_own(r + 1, (r & 1) ? own0 : own1, true);
-          cp_wait_group<1>();
-        } else {
-          cp_wait_group<0>();
-        }
+        __nv_bfloat16* own = ring + (r % kOwnRing) * kOwnElems;
+        if (r + kOwnRing - 1 < nv)
+          stage_own(r + kOwnRing - 1, ring + ((r + kOwnRing - 1) % kOwnRing) * kOwnElems, true);
+        cp_wait_ahead(min(kOwnRing - 1, nv - 1 - r));
         __syncwarp();
         const int src_lane = (r & 7) * 4 + tig, hr = r >> 3;
 #pragma unroll
@@ -705,7 +734,7 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     m.cta_shared = cs;
     m.cta_tail = ct;
     m.cta_tile = cg;
-    cs += a[g].H * m.c_shared * m.zt;
+    cs += a[g].H * ((m.c_shared + g_shared_run - 1) / g_shared_run) * m.zt;
     if (tiled)
       cg += a[g].H * m.zt;
     else
@@ -720,10 +749,12 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
   if (!attr_set[dev & 63]) {
     TP_CUDA(cudaFuncSetAttribute(attn_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmem));
     TP_CUDA(cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    TP_CUDA(cudaFuncSetAttribute(attn_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSharedSmem));
     attr_set[dev & 63] = true;
   }
   if (cs > 0) {
-    ::tp::count_launch(), attn_shared_kernel<<<cs, kWarps * 32, 0, st>>>(G);
+    const size_t smem = (g_shared_run > 1 ? 2 : 1) * (size_t)2 * kTileElems * 2;
+    ::tp::count_launch(), attn_shared_kernel<<<cs, kWarps * 32, smem, st>>>(G, g_shared_run);
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_shared", st);
   }
@@ -743,5 +774,6 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st) { return attn_tree_group(&a, &lv, 1, st); }
 
 void attn_set_tile(bool on) { g_attn_tile = on; }
+void attn_set_shared_run(int n) { g_shared_run = n < 1 ? 1 : (n > kSharedRunMax ? kSharedRunMax : n); }
 
 }  // namespace tp

@@ -47,6 +47,7 @@ struct AttnGroup {
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
 void attn_set_tile(bool on);
+void attn_set_shared_run(int n);
 // members[0..count) -> two launches (shared chunks, then per-node tail + ordered combine)
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st);
 

@@ -288,6 +288,7 @@ def test_tile_attention_equals_per_node_path(w, k):
     try:
         for tile in (1, 0):
             _lib.check(lib.tp_debug_attn_tile(tile))
+            _lib.check(lib.tp_debug_attn_knob(1, 3 if tile else 1))  # multi-chunk shared CTAs too
             r = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=w, k=k), None,
                                collect_trace=False)
             r.prefill(prompt)
@@ -298,7 +299,8 @@ def test_tile_attention_equals_per_node_path(w, k):
                 r.step(ch)
             runs[tile] = outs
     finally:
-        _lib.check(lib.tp_debug_attn_tile(1))
+        _lib.check(lib.tp_debug_attn_tile(0))
+        _lib.check(lib.tp_debug_attn_knob(1, 1))
     wide = 0
     for a_, b_ in zip(runs[1], runs[0]):
         for x, y in zip(a_, b_):

@@ -275,6 +275,7 @@ def run_ours(args, rank, world):
     for _ in range(args.warmup):
         runner.decode_step()
     sync_all()
+    runner.host_s = {k: 0.0 for k in runner.host_s}
     tok0, steps0 = len(runner.emitted), runner.step_no
     l0 = _lib.launch_count()
     io0 = _lib.io_bytes()
@@ -289,6 +290,8 @@ def run_ours(args, rank, world):
         t_wall = time.perf_counter() - t_wall
     e2e_tokens = len(runner.emitted) - tok0
     e2e_ms = t_wall * 1e3 / max(1, e2e_tokens)
+    e2e_host = {k: round(v * 1e3 / args.steps, 4) for k, v in runner.host_s.items()}
+    e2e_host["loop_wall"] = round(t_wall * 1e3 / args.steps, 4)
     launches = _lib.launch_count() - l0
     io1 = _lib.io_bytes()
     for _ in range(args.profile_steps):  # untimed: levels for the profiled replay below
@@ -372,6 +375,11 @@ def run_ours(args, rank, world):
     prof_total_ms = pe0.elapsed_time(pe1)
     peak, peak_src = peaks()
     achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
+    try:  # measured DRAM traffic of the same kernel (committed ncu capture, see profiles/)
+        with open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")) as fh:
+            cap = json.load(fh)
+    except Exception:  # noqa: BLE001
+        cap = None
 
     steps_per_token = args.steps / max(1, e2e_tokens)
     per_step_h2d = (io1[0] - io0[0]) / args.steps
@@ -386,7 +394,12 @@ def run_ours(args, rank, world):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "sk_gemm_kernel (tcgen05 weight-streaming GEMM)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "frac": round(achieved / peak, 4),
+                     "traffic": cap["traffic_bytes_per_launch"] if cap else None,
+                     "traffic_capture": ({k: cap[k] for k in ("launches", "algorithmic_bytes_per_launch",
+                                                              "traffic_over_algorithmic", "source")}
+                                         if cap else None),
+                     "peak_source": peak_src,
                      "gemm_share_of_step": round(gemm_ms / prof_total_ms, 4) if prof_total_ms else None,
                      "gemm_launches": gemm_n, "bytes_per_launch": round(gemm_bytes / max(1, gemm_n))},
         "step_roofline": {"bound": "hbm", "algorithmic_bytes_per_step": round(step_bytes / max(1, len(resident))),
@@ -396,6 +409,7 @@ def run_ours(args, rank, world):
                           "unit": "GB/s", "note": "whole engine step (all kernels + host gaps) vs weights of the "
                                                   "occupied stages + KV rows + LM head, per SURVEY 8d"},
         "host_ms_per_step": host_diag,
+        "e2e_host_ms_per_step": e2e_host,
         "gpu_phase_ms_per_step": phase_diag,
         "gpu_kernel_ms_per_step": kernel_tl,
         "clocks": clocks.summary(),

@@ -32,4 +32,5 @@ for _ in range(40):
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(25)
+st.sort_stats("tottime").print_stats(30)
+st.sort_stats("cumulative").print_stats(45)

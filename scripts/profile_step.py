@@ -39,11 +39,17 @@ r.prefill(prompt)
 for _ in range(args.warmup):
     r.decode_step()
 torch.cuda.synchronize()
+from paper_2504_04104_b200 import _lib  # noqa: E402
+
+_lib.profile_enable(True)  # per-launch algorithmic bytes of every K2 launch in the window
 torch.cuda.profiler.start()
 t0 = time.perf_counter()
 for _ in range(args.steps):
     r.decode_step()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
+_lib.profile_enable(False)
+ms, by, nl = _lib.profile_read()
+print(f"gemm_launches={nl} algorithmic_bytes_total={by:.0f} algorithmic_bytes_per_launch={by / max(1, nl):.0f}")
 dt = (time.perf_counter() - t0) * 1e3 / args.steps
 print(f"steps={args.steps} wall/step={dt:.3f} ms resident={[len(s.resident) if s.resident else 0 for s in r.stages]}")

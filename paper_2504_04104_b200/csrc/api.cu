@@ -159,6 +159,7 @@ size_t meta_capacity(const tp_model* m, int cap, int* words) {
   size_t n = (size_t)std::max(m->cfg.max_nodes, 64);
   size_t bytes = n * 4 * 4                       // tokens, positions, prefix rows, children
                  + n * (size_t)(*words) * 8      // anc bits
+                 + n * (size_t)(65 * 4) + 16     // decoded ancestor rows [n][<=64] + counts
                  + (size_t)(cap + 64) * 4        // compaction / gather index lists
                  + 256;
   return (bytes + 255) & ~(size_t)255;
@@ -492,7 +493,18 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   // pack metadata: tokens | positions | prefix | anc (8-aligned)
   size_t off_tok = 0, off_pos = 4 * (size_t)n, off_pre = 8 * (size_t)n;
   size_t off_anc = ((12 * (size_t)n) + 7) & ~(size_t)7;
-  size_t total = off_anc + 8 * (size_t)n * L->words;
+  // ancestor rows decoded once here (the kernels would otherwise redo it per head)
+  int a_max = 0;
+  std::vector<int32_t> acnt(n);
+  for (int i = 0; i < n; ++i) {
+    int pc = 0;
+    for (int w = 0; w < L->words; ++w) pc += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
+    acnt[i] = std::min(pc, 64);
+    a_max = std::max(a_max, acnt[i]);
+  }
+  const size_t off_cnt = off_anc + 8 * (size_t)n * L->words;
+  const size_t off_rows = off_cnt + 4 * (size_t)n;
+  size_t total = off_rows + 4 * (size_t)n * a_max;
   char *h, *dm;
   int slot;
   TP_TRY(meta_slot(s, total, &h, &dm, &slot));
@@ -501,6 +513,20 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   std::memcpy(h + off_pos, L->positions, 4 * (size_t)n);
   std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
   if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
+  std::memcpy(h + off_cnt, acnt.data(), 4 * (size_t)n);
+  {
+    int32_t* rows = reinterpret_cast<int32_t*>(h + off_rows);
+    for (int i = 0; i < n; ++i) {
+      int k = 0;
+      for (int w = 0; w < L->words && k < acnt[i]; ++w) {
+        uint64_t bits = L->anc_bits[(int64_t)i * L->words + w];
+        while (bits && k < acnt[i]) {
+          rows[(size_t)i * a_max + k++] = L->bits_base + w * 64 + __builtin_ctzll(bits);
+          bits &= bits - 1;
+        }
+      }
+    }
+  }
   TP_TRY(meta_push(s, slot, total, st));
   LevelDev lv;
   lv.n = n;
@@ -521,6 +547,9 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   lv.positions = (const int32_t*)(dm + off_pos);
   lv.prefix_rows = (const int32_t*)(dm + off_pre);
   lv.anc = (const uint64_t*)(dm + off_anc);
+  lv.anc_cnt = (const int32_t*)(dm + off_cnt);
+  lv.anc_rows = (const int32_t*)(dm + off_rows);
+  lv.anc_stride = a_max;
   *out = lv;
   return TP_OK;
 }

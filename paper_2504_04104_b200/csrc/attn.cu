@@ -32,12 +32,15 @@
 
 namespace tp {
 
+#ifndef TP_TAIL_MINB
+#define TP_TAIL_MINB 3
+#endif
 constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ldmatrix)
 constexpr int kCtaNodes = 64;
 constexpr int kWarps = 4;
 constexpr int kTileElems = kAttnChunk * kPad;
 static bool g_attn_tile = false;  // measured slower than the per-node tail on the bench workload  // tp_debug_attn_tile(0) forces the per-node path (tests)
-constexpr size_t kTailSmem = (size_t)kWarps * kTileElems * 2 + (size_t)kWarps * (kAttnChunk + kAttnMaxExtra) * 4;
+constexpr size_t kTailSmem = (size_t)kWarps * kTileElems * 2;
 
 __device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) {
   return *reinterpret_cast<const uint32_t*>(p);
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_c
 // node's remaining chunks, then the bf16 output row.  The running state lives
 // in "lane layout" (lane l owns dims 4l..4l+3); a chunk computed on the tensor
 // cores (row 0 of the tile, fragment layout) is handed over through smem.
-__global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_constant__ AttnGroup G) {
+__global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(const __grid_constant__ AttnGroup G) {
   pdl_trigger();  // the O-projection GEMM may start streaming its weights
   extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 1);
@@ -311,8 +314,6 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
   const int i = (local / a.H) * kWarps + warp;
   if (i >= lv.n) return;
   __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)warp * kTileElems;
-  int* src = reinterpret_cast<int*>(dsm + (size_t)kWarps * kTileElems * 2) + warp * (kAttnChunk + kAttnMaxExtra);
-  int* extra = src + kAttnChunk;
   float* xo = reinterpret_cast<float*>(buf);  // 128-float hand-over row (aliases the tile between chunks)
   const int kh = h / (a.H / a.KV);
   const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
@@ -325,28 +326,8 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
     pm_l = __ldcg(a.pm + pbase + lane);
     pl_l = __ldcg(a.pl + pbase + lane);
   }
-  // ancestor bits -> ordered rows: lane w decodes word w, offsets by a warp scan
-  int A = 0;
-  for (int w0 = 0; w0 < lv.words; w0 += 32) {
-    const int w = w0 + lane;
-    const uint64_t bits = w < lv.words ? lv.anc[(size_t)i * lv.words + w] : 0ull;
-    const int cnt = __popcll(bits);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int pos = A + incl - cnt;
-    uint64_t b = bits;
-    while (b && pos < kAttnMaxExtra) {
-      extra[pos++] = lv.bits_base + w * 64 + (__ffsll((long long)b) - 1);
-      b &= b - 1;
-    }
-    A += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  A = min(A, kAttnMaxExtra);
-  __syncwarp();
+  const int A = lv.anc_cnt[i];
+  const int32_t* anc = lv.anc_rows + (size_t)i * lv.anc_stride;  // decoded on the host, row order
   const int P = lv.prefix_rows[i];
   const int T = P + A + 1;
   const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)i * a.KV + kh) * kAttnHeadDim
@@ -384,37 +365,34 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
     }
   }
   const int c_end = (T + kAttnChunk - 1) / kAttnChunk;
+  const int part = lane & 15, rsub = lane >> 4;  // this lane stages 16-byte piece `part` of rows rsub, rsub+2, ...
+  // stage the chunk's rows of one plane: prefix rows (affine), own rows (gathered), zeros beyond T
+  auto stage = [&](const __nv_bfloat16* plane, const __nv_bfloat16* self, int j0) {
+    const int np = min(max(P - j0, 0), kAttnChunk);   // prefix rows in this chunk
+    const int nt = min(T - j0, kAttnChunk);           // rows holding keys
+    const __nv_bfloat16* pre = plane + (size_t)j0 * kAttnHeadDim + part * 8;
+    for (int row = rsub; row < np; row += 2) cp16(buf + row * kPad + part * 8, pre + (size_t)row * kAttnHeadDim, 16);
+    for (int row = np + rsub; row < nt; row += 2) {
+      const int j = j0 + row;  // P <= j < T
+      const __nv_bfloat16* src = j < P + A ? plane + (size_t)anc[j - P] * kAttnHeadDim : self;
+      cp16(buf + row * kPad + part * 8, src + part * 8, 16);
+    }
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (int row = max(nt, 0) + rsub; row < kAttnChunk; row += 2)
+      *reinterpret_cast<uint4*>(buf + row * kPad + part * 8) = z;
+    cp_wait_all();
+    __syncwarp();
+  };
   for (int c = c_start; c < c_end; ++c) {
     const int j0 = c * kAttnChunk;
     __syncwarp();  // previous chunk's hand-over row has been read
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int slot = lane + 32 * u, j = j0 + slot;
-      src[slot] = j >= T ? -1 : (j < P ? j : (j < P + A ? extra[j - P] : -2));
-    }
-    __syncwarp();
-    // stage K rows of the chunk: every 16-byte piece in flight at once (empty slots: zeros)
-#pragma unroll 8
-    for (int e = lane; e < kAttnChunk * 16; e += 32) {
-      const int row = e >> 4, part = e & 15, sr = src[row];
-      const __nv_bfloat16* g_src = sr == -2 ? kself : Kh + (size_t)max(sr, 0) * kAttnHeadDim;
-      cp16(buf + row * kPad + part * 8, g_src + part * 8, sr == -1 ? 0 : 16);
-    }
-    cp_wait_all();
-    __syncwarp();
+    stage(Kh, kself, j0);
     const int lim[2] = {g == 0 ? min(T - j0, kAttnChunk) : 0, 0};
     float m[2], l[2], o[16][4];
     uint32_t pa[4][4];
     chunk_scores(q1, buf, lim, a.scale, m, l, pa, lane);
     __syncwarp();
-#pragma unroll 8
-    for (int e = lane; e < kAttnChunk * 16; e += 32) {
-      const int row = e >> 4, part = e & 15, sr = src[row];
-      const __nv_bfloat16* g_src = sr == -2 ? vself : Vh + (size_t)max(sr, 0) * kAttnHeadDim;
-      cp16(buf + row * kPad + part * 8, g_src + part * 8, sr == -1 ? 0 : 16);
-    }
-    cp_wait_all();
-    __syncwarp();
+    stage(Vh, vself, j0);
     chunk_pv(pa, buf, o, lane);
     __syncwarp();  // every lane is done reading the tile: reuse it for the hand-over row
     if (g == 0) {
@@ -437,7 +415,6 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_con
   u.y = pack_f32(__fdiv_rn(O.z, L), __fdiv_rn(O.w, L));
   *reinterpret_cast<uint2*>(out) = u;
 }
-
 
 // ---------------------------------------------------------------------------
 // Tree levels (every node has the same prefix P and the same number A of

@@ -69,6 +69,9 @@ struct LevelDev {
   const int32_t* positions;
   const int32_t* prefix_rows;
   const uint64_t* anc;  // [n][words]
+  const int32_t* anc_cnt;   // [n] speculative ancestors per node (<= 64)
+  const int32_t* anc_rows;  // [n][anc_stride] their cache rows, increasing
+  int anc_stride;
 };
 
 int fill_lcg_jump_table();

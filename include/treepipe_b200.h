@@ -203,7 +203,8 @@ int tp_debug_attn_knob(int32_t knob, int32_t value);
  * summed per tag) and resets.                                                 */
 int tp_timeline_enable(int32_t on);
 int tp_timeline_read(char* buf, int32_t len);
-/* Tuning knobs of K2 (0: ring depth cap, 1: smem budget in KB); process-wide. */
+/* Tuning knobs of K2 (0: ring depth cap, 1: smem budget in KB, 2: fix-up diagnostics —
+ * 1/2 skip the stream-K reduction / also the partial publish, WRONG results); process-wide. */
 int tp_debug_gemm_knob(int32_t knob, int32_t value);
 
 #ifdef __cplusplus

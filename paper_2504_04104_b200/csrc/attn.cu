@@ -35,6 +35,9 @@ namespace tp {
 #ifndef TP_TAIL_MINB
 #define TP_TAIL_MINB 3
 #endif
+#ifndef TP_SHARED_MINB
+#define TP_SHARED_MINB 4
+#endif
 constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ldmatrix)
 constexpr int kCtaNodes = 64;
 constexpr int kWarps = 4;
@@ -217,7 +220,7 @@ constexpr int kSharedRunMax = 4;
 constexpr size_t kSharedSmem = (size_t)4 * kTileElems * 2;  // 2 x (K, V) chunk tiles
 static int g_shared_run = 1;  // chunks per CTA (tp_debug_attn_knob 1)
 
-__global__ void __launch_bounds__(kWarps * 32) attn_shared_kernel(const __grid_constant__ AttnGroup G, int run_len) {
+__global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kernel(const __grid_constant__ AttnGroup G, int run_len) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 0);
   const AttnArgs& a = G.m[gi].a;

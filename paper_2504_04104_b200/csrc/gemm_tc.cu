@@ -107,6 +107,7 @@ SkPlan sk_plan(int n_out, int k, int n) {
 // Tuning knobs (tp_debug_gemm_knob): ring depth cap and smem budget.
 static int g_knob_max_stages = 8;
 static int g_knob_smem_kb = 200;
+static int g_knob_fixup = 0;  // diagnostics only: 1 skips the reduction, 2 also the partial publish (WRONG results)
 
 static int stages_for(int n_pad) {
   const int per = kABytes + n_pad * 128;
@@ -276,7 +277,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // the TMA producer, the MMA issuer and the epilogue warps walk the same
 // sequence, the smem ring and the TMEM double buffer continuing across members.
 __global__ void __launch_bounds__(kThreads, 1)
-    sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages, int nbuf) {
+    sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages, int nbuf, int fixup_mode) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
           float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * n) * kBM + r;
-          for (int col0 = 0; col0 < npad; col0 += 16) {
+          for (int col0 = 0; col0 < (fixup_mode == 2 ? 0 : npad); col0 += 16) {
             float v[16];
             tmem_ld_x16(tbase + col0, v);
 #pragma unroll
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // contributor (at most one: the CTA whose range *starts* in the tile)
           // published early in its pass over this member.  Waits only ever point
           // at an earlier (member, position), so the chain cannot cycle.
-          if (t1 <= (mt + 1) * p.KB) {
+          if (fixup_mode == 0 && t1 <= (mt + 1) * p.KB) {
             const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
             const int E = cend - cfirst + 1, rank = c - cfirst;
             if (et == 0) {
@@ -532,7 +533,7 @@ int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ::tp::count_launch();
-  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, grp, p, stages, nbuf));
+  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, grp, p, stages, nbuf, g_knob_fixup));
   if (g_prof_on) {
     TP_CUDA(cudaEventRecord(rec.b, st));
     std::lock_guard<std::mutex> g(g_prof_mu);
@@ -582,6 +583,7 @@ extern "C" int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* lau
 extern "C" int tp_debug_gemm_knob(int32_t knob, int32_t value) {
   if (knob == 0) tp::g_knob_max_stages = value;
   else if (knob == 1) tp::g_knob_smem_kb = value;
+  else if (knob == 2) tp::g_knob_fixup = value;
   else return TP_ECONFIG;
   return TP_OK;
 }

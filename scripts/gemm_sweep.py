@@ -29,9 +29,12 @@ lib = _lib.lib()
 st = torch.cuda.current_stream().cuda_stream
 ns = [int(x) for x in args.n.split(",")]
 for knob in args.knobs.split(","):
-    ms_, kb_ = (int(x) for x in knob.split(":"))
+    parts = [int(x) for x in knob.split(":")]
+    ms_, kb_ = parts[0], parts[1]
+    fx = parts[2] if len(parts) > 2 else 0
     _lib.check(lib.tp_debug_gemm_knob(0, ms_))
     _lib.check(lib.tp_debug_gemm_knob(1, kb_))
+    _lib.check(lib.tp_debug_gemm_knob(2, fx))
     tot_b = tot_t = 0.0
     for name, n_out, k in SHAPES[args.model]:
         for group in (ns, [1]):
@@ -49,7 +52,7 @@ for knob in args.knobs.split(","):
             if g > 1:
                 tot_b += by
                 tot_t += ms.value
-            print(f"stages<={ms_:2d} smem={kb_}KB {name:5s} members={g} n={group}: {ms.value * 1e3:8.1f} us "
+            print(f"fixup={fx} stages<={ms_:2d} smem={kb_}KB {name:5s} members={g} n={group}: {ms.value * 1e3:8.1f} us "
                   f"{gbs:7.0f} GB/s ({gbs / peak:6.1%})", flush=True)
             del ws, xs, outs
     print(f"stages<={ms_:2d} smem={kb_}KB grouped layer total: {tot_t * 1e3:8.1f} us "

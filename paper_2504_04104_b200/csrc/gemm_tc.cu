@@ -45,7 +45,8 @@ using namespace sm100;
 constexpr int kBM = 128, kBK = 64;
 constexpr int kMaxStages = 16;
 constexpr int kMaxTmemBufs = 4;  // accumulator buffers: the MMA may run this many segments ahead
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter: the stream-K fix-up is epilogue-throughput bound
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kXchNodes = 32;           // epilogue exchange tile: 32 nodes x 128 features
 constexpr int kXchLd = 132;
@@ -119,7 +120,7 @@ static size_t smem_for(int n_pad) {
 }
 
 // ---- device --------------------------------------------------------------------
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
 // ---- epilogue: one warp per node row, lane l owns features 4l..4l+3 of the m-tile.
 // RoPE pairs feature r with r^64 and SwiGLU gate r with up r+64: both are lane^16.
@@ -237,8 +238,8 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
   const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
   const size_t slot = (size_t)n * kBM;
   const int f = lane * 4;
-  for (int c = lo + ew; c < hi; c += 8) {
-    const int c2 = c + 4;
+  for (int c = lo + ew; c < hi; c += 2 * kEpiWarps) {
+    const int c2 = c + kEpiWarps;
     const bool two = c2 < hi;
     const float4 y0 = sum_partials(base, slot, cnt, c, f);
     const float4 y1 = two ? sum_partials(base, slot, cnt, c2, f) : y0;
@@ -254,8 +255,8 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
 __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int cn, const float* xch, int ew,
                                            int lane) {
   const int f = lane * 4;
-  for (int cc = ew; cc < cn; cc += 8) {
-    const int cc2 = cc + 4;
+  for (int cc = ew; cc < cn; cc += 2 * kEpiWarps) {
+    const int cc2 = cc + kEpiWarps;
     const bool two = cc2 < cn;
     const float4 y0 = *reinterpret_cast<const float4*>(xch + cc * kXchLd + f);
     const float4 y1 = two ? *reinterpret_cast<const float4*>(xch + cc2 * kXchLd + f) : y0;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < nbuf; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -392,7 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int quarter = warp & 3;  // TMEM lanes this warp may touch
     const int r = quarter * 32 + lane;
-    const int ew = warp - 2;  // epilogue warp 0..3 (node-parallel phases)
+    const int ew = warp - 2;  // epilogue warp 0..kEpiWarps-1 (node-parallel phases)
+    const int chalf = ew >> 2;  // the two warps on a TMEM lane quarter split its 16-column groups
     const int et = threadIdx.x - 64;
     int seg = 0;
     for (int g = 0; g < grp.count; ++g) {
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cnt == 1) {
           for (int c0 = 0; c0 < n; c0 += kXchNodes) {
             const int cn = min(kXchNodes, n - c0);
-            for (int col0 = c0; col0 < min(c0 + kXchNodes, npad); col0 += 16) {
+            for (int col0 = c0 + 16 * chalf; col0 < min(c0 + kXchNodes, npad); col0 += 32) {
               float v[16];
               tmem_ld_x16(tbase + col0, v);
 #pragma unroll
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
           float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * n) * kBM + r;
-          for (int col0 = 0; col0 < (fixup_mode == 2 ? 0 : npad); col0 += 16) {
+          for (int col0 = 16 * chalf; col0 < (fixup_mode == 2 ? 0 : npad); col0 += 32) {
             float v[16];
             tmem_ld_x16(tbase + col0, v);
 #pragma unroll

@@ -221,6 +221,8 @@ constexpr size_t kSharedSmem = (size_t)4 * kTileElems * 2;  // 2 x (K, V) chunk 
 static int g_shared_run = 1;  // chunks per CTA (tp_debug_attn_knob 1)
 
 __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kernel(const __grid_constant__ AttnGroup G, int run_len) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 0);
   const AttnArgs& a = G.m[gi].a;
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
 // in "lane layout" (lane l owns dims 4l..4l+3); a chunk computed on the tensor
 // cores (row 0 of the tile, fragment layout) is handed over through smem.
 __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(const __grid_constant__ AttnGroup G) {
+  pdl_wait();
   pdl_trigger();  // the O-projection GEMM may start streaming its weights
   extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 1);
@@ -437,6 +440,7 @@ constexpr size_t kTileWarpBytes = (size_t)kOwnRing * kOwnElems * 2 + (size_t)16 
 constexpr size_t kTileSmem = (size_t)2 * kTileElems * 2 + (size_t)kPad * 2 + kWarps * kTileWarpBytes;
 
 __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_constant__ AttnGroup G) {
+  pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 2);
@@ -734,17 +738,20 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
   }
   if (cs > 0) {
     const size_t smem = (g_shared_run > 1 ? 2 : 1) * (size_t)2 * kTileElems * 2;
-    ::tp::count_launch(), attn_shared_kernel<<<cs, kWarps * 32, smem, st>>>(G, g_shared_run);
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(attn_shared_kernel, dim3(cs), dim3(kWarps * 32), smem, st, G, g_shared_run));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_shared", st);
   }
   if (cg > 0) {
-    ::tp::count_launch(), attn_tile_kernel<<<cg, kWarps * 32, kTileSmem, st>>>(G);
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(attn_tile_kernel, dim3(cg), dim3(kWarps * 32), kTileSmem, st, G));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tile", st);
   }
   if (ct > 0) {
-    ::tp::count_launch(), attn_tail_kernel<<<ct, kWarps * 32, kTailSmem, st>>>(G);
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kWarps * 32), kTailSmem, st, G));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tail", st);
   }

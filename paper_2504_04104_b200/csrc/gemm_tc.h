@@ -88,8 +88,5 @@ int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, con
 // Grouped launch (members share p's shape; p.n / p.n_pad are ignored).
 int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st);
 
-// Let the next (PDL-launched) GEMM start its weight prologue now.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 }  // namespace tp

@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(kMoveThreads) kv_move_kernel(void* const* __re
                                                                int64_t plane_stride_bytes, int row_bytes,
                                                                const int32_t* __restrict__ src_rows,
                                                                int n_keep, int first) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) uint4 stage[kMoveChunkBytes / 16];
   char* base = (char*)planes[blockIdx.x] + (int64_t)blockIdx.y * plane_stride_bytes;
   // leading run already in place
@@ -55,13 +57,17 @@ int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, vo
   if (n_keep == 0 || nl == 0) return TP_OK;
   int64_t plane = (int64_t)s->cap * row_bytes;  // one kv-head plane
   dim3 grid(2 * nl, s->kv_heads);
-  ::tp::count_launch(), kv_move_kernel<<<grid, kMoveThreads, 0, st>>>(d_planes, plane, row_bytes, d_src_rows, n_keep, first);
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(kv_move_kernel, grid, dim3(kMoveThreads), 0, st, (void* const*)d_planes, (int64_t)plane, row_bytes,
+                     d_src_rows, n_keep, first));
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
 
 __global__ void rows_gather_kernel(const char* __restrict__ src, char* __restrict__ dst, int row_bytes,
                                    const int32_t* __restrict__ idx) {
+  pdl_wait();
+  pdl_trigger();
   const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)idx[blockIdx.x] * row_bytes);
   uint4* d = reinterpret_cast<uint4*>(dst + (int64_t)blockIdx.x * row_bytes);
   for (int e = threadIdx.x; e < row_bytes / 16; e += blockDim.x) d[e] = s[e];
@@ -71,7 +77,9 @@ int rows_compact(const void* src, void* dst, int64_t row_bytes, const int32_t* d
                  cudaStream_t st) {
   TP_CHECK(row_bytes % 16 == 0, TP_ESHAPE, "row bytes must be a multiple of 16");
   if (n_out == 0) return TP_OK;
-  ::tp::count_launch(), rows_gather_kernel<<<n_out, 256, 0, st>>>((const char*)src, (char*)dst, (int)row_bytes, d_idx);
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(rows_gather_kernel, dim3(n_out), dim3(256), 0, st, (const char*)src, (char*)dst, (int)row_bytes,
+                     d_idx));
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -87,6 +95,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024) argmax_match_kernel(const T* __restrict__ logits, int V,
                                                             const int32_t* __restrict__ children,
                                                             int n_children, int32_t* __restrict__ result) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ T sv[32];
   __shared__ int si[32];
   T best = logits[0];
@@ -147,6 +157,8 @@ int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_chi
 // One CTA per row: first argmax (lowest id wins ties) of n rows of fp32 logits.
 __global__ void __launch_bounds__(1024) argmax_rows_kernel(const float* __restrict__ logits, int V,
                                                            int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sv[32];
   __shared__ int si[32];
   const float* row = logits + (size_t)blockIdx.x * V;
@@ -187,7 +199,8 @@ __global__ void __launch_bounds__(1024) argmax_rows_kernel(const float* __restri
 }
 
 int argmax_rows(const void* logits_f32, int vocab, int n, int32_t* d_out, cudaStream_t st) {
-  ::tp::count_launch(), argmax_rows_kernel<<<n, 1024, 0, st>>>((const float*)logits_f32, vocab, d_out);
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(argmax_rows_kernel, dim3(n), dim3(1024), 0, st, (const float*)logits_f32, vocab, d_out));
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }

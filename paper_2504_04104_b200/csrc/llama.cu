@@ -63,6 +63,8 @@ static LlamaModelExt* mext(tp_model* m) { return reinterpret_cast<LlamaModelExt*
 
 __global__ void llama_embed_kernel(const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ tok, int d,
                                    float* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x;
   const __nv_bfloat16* e = E + (size_t)tok[c] * d;
   for (int j = threadIdx.x; j < d; j += blockDim.x) x[(size_t)c * d + j] = __bfloat162float(e[j]);
@@ -91,6 +93,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // same reduction shape at every call site (stage boundaries included).
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
                                                                __nv_bfloat16* __restrict__ xd) {
+  pdl_wait();
   pdl_trigger();  // the following GEMM may start streaming its weights
   __shared__ float red[33];
   const float* xr = x + (size_t)blockIdx.x * d;
@@ -117,6 +120,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __re
 
 // cos/sin of every (node position, rotary pair) for the QKV epilogue; angle in fp64.
 __global__ void rope_table_kernel(const int32_t* __restrict__ pos, double theta, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int c = blockIdx.x, i = threadIdx.x;  // i in [0, 64)
   const double inv = pow(theta, -2.0 * (double)i / 128.0);
   double sn, cs;
@@ -272,8 +277,9 @@ void llama_stage_free(tp_stage*) {}
 
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st) {
   TP_CHECK(m->embed, TP_ECONFIG, "model has no embedding table");
-  ::tp::count_launch(), llama_embed_kernel<<<n, 256, 0, st>>>((const __nv_bfloat16*)m->embed, d_tokens,
-                                                              m->cfg.hidden, out);
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(llama_embed_kernel, dim3(n), dim3(256), 0, st, (const __nv_bfloat16*)m->embed, d_tokens,
+                     (int)m->cfg.hidden, out));
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -291,7 +297,8 @@ static int logits_locked(tp_model* m, int n, const float* x, float* logits, cuda
   LlamaWs* e;
   TP_TRY(ws_get(m, 0, 1, &e));
   const int d = m->cfg.hidden, V = m->cfg.vocab;
-  ::tp::count_launch(), rmsnorm_kernel<<<n, kNormThreads, 0, st>>>(x, d, m->cfg.norm_eps, e->Xd);
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(rmsnorm_kernel, dim3(n), dim3(kNormThreads), 0, st, x, d, m->cfg.norm_eps, e->Xd));
   TP_CUDA(cudaGetLastError());
   GemmEpi g = epi_base(e, kCtrHead);
   g.op = kOpStore;
@@ -340,6 +347,7 @@ struct NormGroup {
 
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __grid_constant__ NormGroup ng, int d,
                                                                      float eps) {
+  pdl_wait();
   pdl_trigger();
   const int g = blockIdx.y;
   if ((int)blockIdx.x >= ng.n[g]) return;
@@ -431,8 +439,9 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
     if (hi[g] == lo[g]) continue;
     for (int r = 0; r < M.count; ++r) {
       const FwdItem& it = M.items[r];
-      ::tp::count_launch(), rope_table_kernel<<<it.lv.n, 64, 0, st>>>(it.lv.positions, (double)c.rope_theta,
-                                                                     ws[g]->rope + (size_t)offs[g][r] * 128);
+      ::tp::count_launch();
+      TP_CUDA(launch_pdl(rope_table_kernel, dim3(it.lv.n), dim3(64), 0, st, it.lv.positions, (double)c.rope_theta,
+                         ws[g]->rope + (size_t)offs[g][r] * 128));
       TP_CUDA(cudaGetLastError());
     }
     if (M.count > 1) {
@@ -543,7 +552,8 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
     }
     gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
     if (j == 0) {
-      ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
+      ::tp::count_launch();
+      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
       TP_CUDA(cudaGetLastError());
     }
     TP_TRY(sk_gemm_group(gq, pqkv, st));
@@ -554,7 +564,8 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
     }
     TP_TRY(sk_gemm_group(go, po, st));
     timeline_mark("gemm_o", st);
-    ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxn, na), kNormThreads, 0, st>>>(ng, d, c.norm_eps);
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
     TP_CUDA(cudaGetLastError());
     timeline_mark("rmsnorm", st);
     TP_TRY(sk_gemm_group(ggu, pgu, st));
@@ -573,7 +584,8 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
         ++nc;
       }
     if (nc) {
-      ::tp::count_launch(), rmsnorm_group_kernel<<<dim3(maxc, nc), kNormThreads, 0, st>>>(nn, d, c.norm_eps);
+      ::tp::count_launch();
+      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxc, nc), dim3(kNormThreads), 0, st, nn, d, c.norm_eps));
       TP_CUDA(cudaGetLastError());
       timeline_mark("rmsnorm", st);
     }

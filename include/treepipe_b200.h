@@ -149,6 +149,10 @@ int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_
 int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64_t* keep_bits,
                      void* stream);
 int tp_stage_truncate(tp_stage* s, int32_t rows);
+/* tp_stage_compact for several stages of one device (every stage's prune of one
+ * verification, pipeline.py:341-361) in one upload + one launch.            */
+int tp_stages_compact(int32_t count, tp_stage* const* stages, const int32_t* first_rows, const int32_t* counts,
+                      const uint64_t* const* keep_bits, void* stream);
 /* Copy K (kind 0) or V (kind 1) of one layer, rows [lo,hi), as [rows][kv_heads][head_dim]. */
 int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo, int32_t hi, void* host);
 
@@ -156,6 +160,11 @@ int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo,
 /* dst[j] = src[i_j] for the set bits i_0 < i_1 < ... of keep_bits (n_src rows of row_bytes). */
 int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t row_bytes, int32_t n_src,
                     const uint64_t* keep_bits, int32_t* n_out, void* stream);
+/* tp_rows_compact for up to 64 row sets (every stage's in-flight filter of one
+ * step, pipeline.py:379-400) in one upload + one launch; n_out[i] returned.  */
+int tp_rows_compact_many(int32_t count, tp_stage* ws, const void* const* src_dev, void* const* dst_dev,
+                         int64_t row_bytes, const int32_t* n_src, const uint64_t* const* keep_bits, int32_t* n_out,
+                         void* stream);
 /* Grow the KV capacity (reference KvCache grow-by-doubling, model.py:141-148). */
 int tp_stage_reserve(tp_stage* s, int32_t capacity_rows);
 

@@ -79,6 +79,8 @@ _SIGS = {
     "tp_model_greedy_rows_wait": (C.c_int, [_P, _I, _P]),
     "tp_stage_compact": (C.c_int, [_P, _I, _I, _P, _P]),
     "tp_stage_truncate": (C.c_int, [_P, _I]),
+    "tp_stages_compact": (C.c_int, [_I, _P, _P, _P, _P, _P]),
+    "tp_rows_compact_many": (C.c_int, [_I, _P, _P, _P, C.c_int64, _P, _P, _P, _P]),
     "tp_stage_read_kv": (C.c_int, [_P, _I, _I, _I, _I, _P]),
     "tp_rows_compact": (C.c_int, [_P, _P, _P, C.c_int64, _I, _P, C.POINTER(C.c_int32), _P]),
     "tp_debug_gemm": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _P]),

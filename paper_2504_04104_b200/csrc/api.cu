@@ -296,6 +296,7 @@ int tp_model_destroy(tp_model* m) {
     for (void* p : w.w)
       if (p) cudaFree(p);
   if (!is_toy(m)) llama_model_free(m);
+  call_ring_free(m);
   delete m;
   return TP_OK;
 }
@@ -459,8 +460,11 @@ int tp_stage_reserve(tp_stage* s, int32_t capacity_rows) {
 
 // Validate one level against its stage, upload its metadata (one pinned-host ->
 // device copy) and describe it for the kernels.
-static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, cudaStream_t st,
-                         LevelDev* out) {
+// Validate one level against its stage and describe it for the kernels; the
+// metadata blob (tokens | positions | prefix | anc bits | anc counts | anc rows)
+// is laid out by level_write into caller-provided staging memory.
+static int level_validate(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, LevelDev* out,
+                          size_t* bytes) {
   TP_CHECK(s && L && hidden_out, TP_ECONFIG, "null argument");
   tp_model* m = s->m;
   const int n = L->n;
@@ -469,15 +473,15 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   TP_CHECK(hidden_in || (L->tokens && m->embed), TP_ECONFIG, "need hidden_in or tokens + embedding");
   TP_CHECK(L->words >= 0 && L->words <= s->max_words, TP_ESHAPE, "too many mask words for this stage");
   TP_CHECK(!L->append || s->rows + n <= s->cap, TP_ESHAPE, "KV capacity exceeded (reserve first)");
-  timeline_mark("host_gap", st);  // GPU time since the previous mark: idle or other work
   const int visible = s->rows + (L->append ? n : 0);
-  int max_t = 0, uniform_a = -2;
+  int max_t = 0, uniform_a = -2, a_max = 0;
   for (int i = 0; i < n; ++i) {
     int pc = 0;
     for (int w = 0; w < L->words; ++w) pc += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
     if (uniform_a == -2) uniform_a = pc;
     else if (uniform_a != pc || L->prefix_rows[i] != L->prefix_rows[0]) uniform_a = -1;
     TP_CHECK(is_toy(m) || pc <= 64, TP_ESHAPE, "more than 64 speculative ancestors per node");
+    a_max = std::max(a_max, std::min(pc, 64));
     max_t = std::max(max_t, L->prefix_rows[i] + pc + 1);
     TP_CHECK(L->prefix_rows[i] >= 0 && L->prefix_rows[i] <= visible, TP_ECONTRACT, "prefix rows beyond cache");
     if (L->tokens && !hidden_in)
@@ -490,45 +494,7 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
                "ancestor row outside the cache");
     }
   }
-  // pack metadata: tokens | positions | prefix | anc (8-aligned)
-  size_t off_tok = 0, off_pos = 4 * (size_t)n, off_pre = 8 * (size_t)n;
-  size_t off_anc = ((12 * (size_t)n) + 7) & ~(size_t)7;
-  // ancestor rows decoded once here (the kernels would otherwise redo it per head)
-  int a_max = 0;
-  std::vector<int32_t> acnt(n);
-  for (int i = 0; i < n; ++i) {
-    int pc = 0;
-    for (int w = 0; w < L->words; ++w) pc += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
-    acnt[i] = std::min(pc, 64);
-    a_max = std::max(a_max, acnt[i]);
-  }
-  const size_t off_cnt = off_anc + 8 * (size_t)n * L->words;
-  const size_t off_rows = off_cnt + 4 * (size_t)n;
-  size_t total = off_rows + 4 * (size_t)n * a_max;
-  char *h, *dm;
-  int slot;
-  TP_TRY(meta_slot(s, total, &h, &dm, &slot));
-  if (L->tokens) std::memcpy(h + off_tok, L->tokens, 4 * (size_t)n);
-  else std::memset(h + off_tok, 0, 4 * (size_t)n);
-  std::memcpy(h + off_pos, L->positions, 4 * (size_t)n);
-  std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
-  if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
-  std::memcpy(h + off_cnt, acnt.data(), 4 * (size_t)n);
-  {
-    int32_t* rows = reinterpret_cast<int32_t*>(h + off_rows);
-    for (int i = 0; i < n; ++i) {
-      int k = 0;
-      for (int w = 0; w < L->words && k < acnt[i]; ++w) {
-        uint64_t bits = L->anc_bits[(int64_t)i * L->words + w];
-        while (bits && k < acnt[i]) {
-          rows[(size_t)i * a_max + k++] = L->bits_base + w * 64 + __builtin_ctzll(bits);
-          bits &= bits - 1;
-        }
-      }
-    }
-  }
-  TP_TRY(meta_push(s, slot, total, st));
-  LevelDev lv;
+  LevelDev lv{};
   lv.n = n;
   lv.append = L->append;
   lv.row0 = s->rows;
@@ -537,22 +503,125 @@ static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, 
   lv.max_t = max_t;
   lv.min_p = *std::min_element(L->prefix_rows, L->prefix_rows + n);
   lv.uniform_a = uniform_a;
+  lv.anc_stride = a_max;
   const bool all_layers = L->layer_lo == 0 && L->layer_hi == 0;
   const bool no_layers = L->layer_lo < 0;  // explicit empty range: embed/copy only
   lv.layer_lo = all_layers ? s->lo : (no_layers ? s->lo : L->layer_lo);
   lv.layer_hi = all_layers ? s->hi : (no_layers ? s->lo : L->layer_hi);
   TP_CHECK(s->lo <= lv.layer_lo && lv.layer_lo <= lv.layer_hi && lv.layer_hi <= s->hi, TP_ESHAPE,
            "layer range not hosted by this stage");
-  lv.tokens = (const int32_t*)(dm + off_tok);
-  lv.positions = (const int32_t*)(dm + off_pos);
-  lv.prefix_rows = (const int32_t*)(dm + off_pre);
-  lv.anc = (const uint64_t*)(dm + off_anc);
-  lv.anc_cnt = (const int32_t*)(dm + off_cnt);
-  lv.anc_rows = (const int32_t*)(dm + off_rows);
-  lv.anc_stride = a_max;
+  const size_t off_anc = ((12 * (size_t)n) + 7) & ~(size_t)7;
+  *bytes = (off_anc + 8 * (size_t)n * L->words + 4 * (size_t)n + 4 * (size_t)n * a_max + 15) & ~(size_t)15;
   *out = lv;
   return TP_OK;
 }
+
+static void level_write(const tp_level* L, LevelDev* lv, char* h, const char* dm) {
+  const int n = L->n, a_max = lv->anc_stride;
+  const size_t off_tok = 0, off_pos = 4 * (size_t)n, off_pre = 8 * (size_t)n;
+  const size_t off_anc = ((12 * (size_t)n) + 7) & ~(size_t)7;
+  const size_t off_cnt = off_anc + 8 * (size_t)n * L->words;
+  const size_t off_rows = off_cnt + 4 * (size_t)n;
+  if (L->tokens) std::memcpy(h + off_tok, L->tokens, 4 * (size_t)n);
+  else std::memset(h + off_tok, 0, 4 * (size_t)n);
+  std::memcpy(h + off_pos, L->positions, 4 * (size_t)n);
+  std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
+  if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
+  int32_t* cnt = reinterpret_cast<int32_t*>(h + off_cnt);
+  int32_t* rows = reinterpret_cast<int32_t*>(h + off_rows);
+  // ancestor rows decoded once here (the kernels would otherwise redo it per head)
+  for (int i = 0; i < n; ++i) {
+    int k = 0;
+    for (int w = 0; w < L->words && k < a_max; ++w) {
+      uint64_t bits = L->anc_bits[(int64_t)i * L->words + w];
+      while (bits && k < a_max) {
+        rows[(size_t)i * a_max + k++] = L->bits_base + w * 64 + __builtin_ctzll(bits);
+        bits &= bits - 1;
+      }
+    }
+    cnt[i] = k;
+  }
+  lv->tokens = (const int32_t*)(dm + off_tok);
+  lv->positions = (const int32_t*)(dm + off_pos);
+  lv->prefix_rows = (const int32_t*)(dm + off_pre);
+  lv->anc = (const uint64_t*)(dm + off_anc);
+  lv->anc_cnt = (const int32_t*)(dm + off_cnt);
+  lv->anc_rows = (const int32_t*)(dm + off_rows);
+}
+
+// One level through its stage's own staging ring.
+static int prepare_level(tp_stage* s, const tp_level* L, const void* hidden_in, void* hidden_out, cudaStream_t st,
+                         LevelDev* out) {
+  size_t bytes;
+  TP_TRY(level_validate(s, L, hidden_in, hidden_out, out, &bytes));
+  char *h, *dm;
+  int slot;
+  TP_TRY(meta_slot(s, bytes, &h, &dm, &slot));
+  level_write(L, out, h, dm);
+  return meta_push(s, slot, bytes, st);
+}
+
+// Per-model staging ring for calls that carry several levels / index lists at
+// once: one pinned-host -> device copy per call instead of one per stage.
+namespace tp {
+struct CallRing {
+  static constexpr int kSlots = 8;
+  char* host = nullptr;
+  char* dev = nullptr;
+  size_t slot_bytes = 0;
+  cudaEvent_t ev[kSlots] = {nullptr};
+  int next = 0;
+};
+
+int call_slot(tp_model* m, size_t bytes, char** host, char** dev, int* slot) {
+  auto* r = reinterpret_cast<CallRing*>(m->call_ring);
+  if (!r) {
+    r = new CallRing();
+    m->call_ring = r;
+    for (auto& e : r->ev) {
+      TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      TP_CUDA(cudaEventRecord(e, 0));
+    }
+  }
+  if (bytes > r->slot_bytes) {  // grow (rare): drain users of the old buffers first
+    TP_CUDA(cudaDeviceSynchronize());
+    if (r->host) cudaFreeHost(r->host);
+    if (r->dev) cudaFree(r->dev);
+    r->slot_bytes = std::max<size_t>(bytes, (size_t)1 << 20);
+    TP_CUDA(cudaMallocHost((void**)&r->host, r->slot_bytes * CallRing::kSlots));
+    TP_CUDA(cudaMalloc((void**)&r->dev, r->slot_bytes * CallRing::kSlots));
+  }
+  const int k = r->next;
+  r->next = (k + 1) % CallRing::kSlots;
+  TP_CUDA(cudaEventSynchronize(r->ev[k]));
+  *host = r->host + (size_t)k * r->slot_bytes;
+  *dev = r->dev + (size_t)k * r->slot_bytes;
+  *slot = k;
+  return TP_OK;
+}
+
+int call_push(tp_model* m, int slot, size_t bytes, cudaStream_t st) {
+  auto* r = reinterpret_cast<CallRing*>(m->call_ring);
+  const size_t off = (size_t)slot * r->slot_bytes;
+  if (bytes) {
+    TP_CUDA(cudaMemcpyAsync(r->dev + off, r->host + off, bytes, cudaMemcpyHostToDevice, st));
+    count_io((long long)bytes, 0);
+  }
+  TP_CUDA(cudaEventRecord(r->ev[slot], st));
+  return TP_OK;
+}
+
+void call_ring_free(tp_model* m) {
+  auto* r = reinterpret_cast<CallRing*>(m->call_ring);
+  if (!r) return;
+  if (r->host) cudaFreeHost(r->host);
+  if (r->dev) cudaFree(r->dev);
+  for (auto e : r->ev)
+    if (e) cudaEventDestroy(e);
+  delete r;
+  m->call_ring = nullptr;
+}
+}  // namespace tp
 
 extern "C" {
 
@@ -593,10 +662,22 @@ int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_
   }
   TP_CUDA(cudaSetDevice(dev));
   cudaStream_t st = (cudaStream_t)stream;
+  timeline_mark("host_gap", st);  // GPU time since the previous mark: idle or other work
   std::vector<LevelDev> lv(n_items);
-  for (int i = 0; i < n_items; ++i)
-    TP_TRY(prepare_level(items[i].stage, &items[i].level, items[i].hidden_in, member_hidden_out[items[i].member],
-                         st, &lv[i]));
+  std::vector<size_t> off(n_items + 1, 0);
+  for (int i = 0; i < n_items; ++i) {
+    size_t b;
+    TP_TRY(level_validate(items[i].stage, &items[i].level, items[i].hidden_in, member_hidden_out[items[i].member],
+                          &lv[i], &b));
+    off[i + 1] = off[i] + b;
+  }
+  {  // every item's metadata in one upload
+    char *h, *dm;
+    int slot;
+    TP_TRY(call_slot(m0, off[n_items], &h, &dm, &slot));
+    for (int i = 0; i < n_items; ++i) level_write(&items[i].level, &lv[i], h + off[i], dm + off[i]);
+    TP_TRY(call_push(m0, slot, off[n_items], st));
+  }
   if (is_toy(m0)) {
     TP_CHECK(n_members == n_items, TP_ECONFIG, "toy arch: one item per member");
     for (int i = 0; i < n_items; ++i)
@@ -653,6 +734,100 @@ int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64
     timeline_mark("kv_compact", st);
   }
   s->rows = first_row + (int)src.size();
+  return TP_OK;
+}
+
+int tp_stages_compact(int32_t count, tp_stage* const* stages, const int32_t* first_rows, const int32_t* counts,
+                      const uint64_t* const* keep_bits, void* stream) {
+  TP_CHECK(count >= 0 && (count == 0 || (stages && first_rows && counts && keep_bits)), TP_ECONFIG, "null argument");
+  if (count == 0) return TP_OK;
+  tp_model* m0 = stages[0]->m;
+  TP_CUDA(cudaSetDevice(m0->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < count; ++i) {
+    tp_stage* s = stages[i];
+    TP_CHECK(s && s->m->cfg.device == m0->cfg.device, TP_ECONFIG, "stages of one compaction call share a device");
+    TP_CHECK(first_rows[i] >= 0 && counts[i] >= 0 && first_rows[i] + counts[i] <= s->rows, TP_ECONTRACT,
+             "compaction window outside the cache (prefix rows cannot be dropped)");
+    TP_CHECK((s->head_dim * s->esize) % 16 == 0, TP_ESHAPE, "KV row bytes must be a multiple of 16");
+  }
+  for (int c0 = 0; c0 < count; c0 += kMaxMulti) {  // <= 64 stages per upload + launch
+    const int c1 = std::min(count, c0 + kMaxMulti);
+    std::vector<std::vector<int32_t>> src(c1 - c0);
+    size_t bytes = 0;
+    for (int i = c0; i < c1; ++i) {
+      for (int j = 0; j < counts[i]; ++j)
+        if ((keep_bits[i][j >> 6] >> (j & 63)) & 1ull) src[i - c0].push_back(first_rows[i] + j);
+      bytes += (4 * src[i - c0].size() + 15) & ~(size_t)15;
+    }
+    char *h, *dm;
+    int slot;
+    TP_TRY(call_slot(m0, bytes, &h, &dm, &slot));
+    MoveGroup g;
+    g.count = 0;
+    int ctas = 0;
+    size_t off = 0;
+    for (int i = c0; i < c1; ++i) {
+      tp_stage* s = stages[i];
+      const std::vector<int32_t>& v = src[i - c0];
+      const int nl = s->hi - s->lo, rb = s->head_dim * s->esize;
+      std::memcpy(h + off, v.data(), 4 * v.size());
+      if (!v.empty() && nl > 0) {
+        MoveItem& it = g.m[g.count++];
+        it.planes = s->d_planes;
+        it.plane_stride = (int64_t)s->cap * rb;
+        it.src = reinterpret_cast<const int32_t*>(dm + off);
+        it.row_bytes = rb;
+        it.n_keep = (int)v.size();
+        it.first = first_rows[i];
+        it.heads = s->kv_heads;
+        it.cta0 = ctas;
+        ctas += 2 * nl * s->kv_heads;
+      }
+      off += (4 * v.size() + 15) & ~(size_t)15;
+      s->rows = first_rows[i] + (int)v.size();
+    }
+    TP_TRY(call_push(m0, slot, bytes, st));
+    TP_TRY(kv_compact_many(g, ctas, st));
+  }
+  timeline_mark("kv_compact", st);
+  return TP_OK;
+}
+
+int tp_rows_compact_many(int32_t count, tp_stage* ws, const void* const* src_dev, void* const* dst_dev,
+                         int64_t row_bytes, const int32_t* n_src, const uint64_t* const* keep_bits, int32_t* n_out,
+                         void* stream) {
+  TP_CHECK(count >= 0 && count <= kMaxMulti && ws, TP_ECONFIG, "rows_compact_many: 0..64 sets and a workspace");
+  if (count == 0) return TP_OK;
+  TP_CUDA(cudaSetDevice(ws->m->cfg.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<std::vector<int32_t>> idx(count);
+  size_t bytes = 0;
+  for (int i = 0; i < count; ++i) {
+    for (int j = 0; j < n_src[i]; ++j)
+      if ((keep_bits[i][j >> 6] >> (j & 63)) & 1ull) idx[i].push_back(j);
+    n_out[i] = (int32_t)idx[i].size();
+    bytes += (4 * idx[i].size() + 15) & ~(size_t)15;
+  }
+  char *h, *dm;
+  int slot;
+  TP_TRY(call_slot(ws->m, bytes, &h, &dm, &slot));
+  RowsGroup g;
+  g.count = 0;
+  g.row_bytes = (int)row_bytes;
+  size_t off = 0;
+  int mr = 0;
+  for (int i = 0; i < count; ++i) {
+    std::memcpy(h + off, idx[i].data(), 4 * idx[i].size());
+    if (!idx[i].empty()) {
+      g.m[g.count++] = RowsItem{src_dev[i], dst_dev[i], reinterpret_cast<const int32_t*>(dm + off), n_out[i]};
+      mr = std::max(mr, n_out[i]);
+    }
+    off += (4 * idx[i].size() + 15) & ~(size_t)15;
+  }
+  TP_TRY(call_push(ws->m, slot, bytes, st));
+  TP_TRY(rows_compact_many(g, mr, st));
+  timeline_mark("rows_compact", st);
   return TP_OK;
 }
 

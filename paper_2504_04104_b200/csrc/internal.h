@@ -21,6 +21,7 @@ struct tp_model {
   std::vector<tp_layer_weights> layers;  // index layer - cfg.layer_lo
   // llama: tensor maps for TMA live beside the weights (filled lazily)
   void* tma_cache = nullptr;
+  void* call_ring = nullptr;  // staging ring for multi-level / multi-stage calls (api.cu)
 };
 
 struct tp_stage {
@@ -105,6 +106,9 @@ int llama_greedy_rows_async(tp_model* m, int n, const float* x, float* logits, c
 int llama_greedy_rows_wait(tp_model* m, int n, int32_t* out);
 void timeline_mark(const char* tag, cudaStream_t st);  // no-op unless enabled
 int argmax_rows(const void* logits_f32, int vocab, int n, int32_t* d_out, cudaStream_t st);
+int call_slot(tp_model* m, size_t bytes, char** host, char** dev, int* slot);
+int call_push(tp_model* m, int slot, size_t bytes, cudaStream_t st);
+void call_ring_free(tp_model* m);
 // metadata upload through a stage's staging ring (api.cu)
 int upload(tp_stage* s, const void* host, size_t bytes, cudaStream_t st, const char** dev_out);
 int llama_embed(tp_model* m, int n, const int32_t* d_tokens, float* out, cudaStream_t st);
@@ -124,6 +128,30 @@ int lcg_fill_bf16_rows(__nv_bfloat16* out, int64_t rows_in, int64_t cols_out, ui
 // shared (kv.cu)
 int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_children, int n_children,
                  int32_t* d_result, cudaStream_t st);
+constexpr int kMaxMulti = 64;
+struct MoveItem {
+  void* const* planes;   // [2*layers] K/V plane bases of the stage
+  int64_t plane_stride;  // bytes between kv-head planes
+  const int32_t* src;    // kept rows (device), increasing
+  int row_bytes, n_keep, first, heads, cta0;
+};
+struct MoveGroup {
+  MoveItem m[kMaxMulti];
+  int count;
+};
+struct RowsItem {
+  const void* src;
+  void* dst;
+  const int32_t* idx;
+  int n_out;
+};
+struct RowsGroup {
+  RowsItem m[kMaxMulti];
+  int count;
+  int row_bytes;
+};
+int kv_compact_many(const MoveGroup& g, int ctas, cudaStream_t st);
+int rows_compact_many(const RowsGroup& g, int max_rows, cudaStream_t st);
 int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, void** d_planes,
                cudaStream_t st);
 int rows_compact(const void* src, void* dst, int64_t row_bytes, const int32_t* d_idx, int n_out,

@@ -48,6 +48,66 @@ __global__ void __launch_bounds__(kMoveThreads) kv_move_kernel(void* const* __re
   }
 }
 
+// Several stages' compactions in one launch: CTA -> (item, plane, kv-head).
+__global__ void __launch_bounds__(kMoveThreads) kv_move_multi_kernel(const __grid_constant__ MoveGroup G) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ __align__(16) uint4 stage[kMoveChunkBytes / 16];
+  int it = 0;
+  while (it + 1 < G.count && (int)blockIdx.x >= G.m[it + 1].cta0) ++it;
+  const MoveItem& M = G.m[it];
+  const int local = blockIdx.x - M.cta0;
+  const int plane = local / M.heads, head = local % M.heads;
+  char* base = (char*)M.planes[plane] + (int64_t)head * M.plane_stride;
+  const int32_t* src_rows = M.src;
+  const int n_keep = M.n_keep, first = M.first, row_bytes = M.row_bytes;
+  int j0 = 0;
+  while (j0 < n_keep && src_rows[j0] == first + j0) ++j0;
+  const int vec_per_row = row_bytes / 16;
+  const int rows_per_chunk = max(1, kMoveChunkBytes / row_bytes);
+  for (int c = j0; c < n_keep; c += rows_per_chunk) {
+    const int cnt = min(rows_per_chunk, n_keep - c);
+    const int total = cnt * vec_per_row;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int r = t / vec_per_row, e = t % vec_per_row;
+      stage[t] = reinterpret_cast<const uint4*>(base + (int64_t)src_rows[c + r] * row_bytes)[e];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int r = t / vec_per_row, e = t % vec_per_row;
+      reinterpret_cast<uint4*>(base + (int64_t)(first + c + r) * row_bytes)[e] = stage[t];
+    }
+    __syncthreads();
+  }
+}
+
+int kv_compact_many(const MoveGroup& g, int ctas, cudaStream_t st) {
+  if (ctas == 0) return TP_OK;
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(kv_move_multi_kernel, dim3(ctas), dim3(kMoveThreads), 0, st, g));
+  return TP_OK;
+}
+
+// Several row gathers in one launch: block (row, item).
+__global__ void rows_gather_multi_kernel(const __grid_constant__ RowsGroup G) {
+  pdl_wait();
+  pdl_trigger();
+  const int it = blockIdx.y, r = blockIdx.x;
+  if (r >= G.m[it].n_out) return;
+  const int rb = G.row_bytes;
+  const uint4* s = reinterpret_cast<const uint4*>((const char*)G.m[it].src + (int64_t)G.m[it].idx[r] * rb);
+  uint4* d = reinterpret_cast<uint4*>((char*)G.m[it].dst + (int64_t)r * rb);
+  for (int e = threadIdx.x; e < rb / 16; e += blockDim.x) d[e] = s[e];
+}
+
+int rows_compact_many(const RowsGroup& g, int max_rows, cudaStream_t st) {
+  if (g.count == 0 || max_rows == 0) return TP_OK;
+  TP_CHECK(g.row_bytes % 16 == 0, TP_ESHAPE, "row bytes must be a multiple of 16");
+  ::tp::count_launch();
+  TP_CUDA(launch_pdl(rows_gather_multi_kernel, dim3(max_rows, g.count), dim3(256), 0, st, g));
+  return TP_OK;
+}
+
 int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, void** d_planes,
                cudaStream_t st) {
   int nl = s->hi - s->lo;

@@ -130,6 +130,41 @@ __global__ void rope_table_kernel(const int32_t* __restrict__ pos, double theta,
   out[((size_t)c * 64 + i) * 2 + 1] = (float)sn;
 }
 
+// Batched per-item helpers of a forward call (one launch each instead of one per item).
+constexpr int kMaxBatchItems = 64;
+struct RowCopyGroup {
+  const float* src[kMaxBatchItems];
+  float* dst[kMaxBatchItems];
+  int rows[kMaxBatchItems];
+};
+// hidden rows handed over from the previous stage -> the member's residual stream
+__global__ void copy_rows_kernel(const __grid_constant__ RowCopyGroup G, int d) {
+  pdl_wait();
+  pdl_trigger();
+  const int it = blockIdx.y, r = blockIdx.x;
+  if (r >= G.rows[it]) return;
+  const float4* s = reinterpret_cast<const float4*>(G.src[it] + (size_t)r * d);
+  float4* o = reinterpret_cast<float4*>(G.dst[it] + (size_t)r * d);
+  for (int j = threadIdx.x; j < d / 4; j += blockDim.x) o[j] = s[j];
+}
+
+struct RopeGroup {
+  const int32_t* pos[kMaxBatchItems];
+  float* out[kMaxBatchItems];
+  int n[kMaxBatchItems];
+};
+__global__ void rope_group_kernel(const __grid_constant__ RopeGroup G, double theta) {
+  pdl_wait();
+  pdl_trigger();
+  const int it = blockIdx.y, c = blockIdx.x, i = threadIdx.x;  // i in [0, 64)
+  if (c >= G.n[it]) return;
+  const double inv = pow(theta, -2.0 * (double)i / 128.0);
+  double sn, cs;
+  sincos((double)G.pos[it][c] * inv, &sn, &cs);
+  G.out[it][((size_t)c * 64 + i) * 2] = (float)cs;
+  G.out[it][((size_t)c * 64 + i) * 2 + 1] = (float)sn;
+}
+
 // ---- host ---------------------------------------------------------------------------
 
 static int build_model_ext(tp_model* m) {
@@ -399,6 +434,12 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
   const int q = H * 128, kvd = KV * 128;
   LlamaWs* ws[kMaxGroup];
   std::vector<int> offs[kMaxGroup];
+  struct Copy {
+    const float* src;
+    float* dst;
+    int rows;
+  };
+  std::vector<Copy> copies;
   int ntot[kMaxGroup], lo[kMaxGroup], hi[kMaxGroup];
   int slots = 0;
   for (int g = 0; g < count; ++g) {
@@ -423,27 +464,55 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
       const FwdItem& it = M.items[r];
       float* x = M.x + (size_t)offs[g][r] * d;
       if (it.hin) {
-        if (it.hin != x) TP_CUDA(cudaMemcpyAsync(x, it.hin, (size_t)it.lv.n * d * 4, cudaMemcpyDeviceToDevice, st));
+        if (it.hin != x) copies.push_back({(const float*)it.hin, x, it.lv.n});
       } else {
         TP_TRY(llama_embed(m0, it.lv.n, it.lv.tokens, x, st));
       }
     }
     slots = std::max(slots, hi[g] - lo[g]);
   }
+  for (size_t c0 = 0; c0 < copies.size(); c0 += kMaxBatchItems) {
+    RowCopyGroup cg;
+    int mr = 0, cnt = (int)std::min<size_t>(kMaxBatchItems, copies.size() - c0);
+    for (int k = 0; k < cnt; ++k) {
+      cg.src[k] = copies[c0 + k].src;
+      cg.dst[k] = copies[c0 + k].dst;
+      cg.rows[k] = copies[c0 + k].rows;
+      mr = std::max(mr, cg.rows[k]);
+    }
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(copy_rows_kernel, dim3(mr, cnt), dim3(256), 0, st, cg, d));
+  }
   if (slots == 0) return TP_OK;
   // per-request KV destinations of ragged members (one small upload each)
   const QkvItem* qitems[kMaxGroup] = {nullptr};
   const int32_t* qnode[kMaxGroup] = {nullptr};
+  {  // RoPE tables of every item, one launch
+    RopeGroup rg;
+    int cnt = 0, mn = 0;
+    auto flush = [&]() -> int {
+      if (!cnt) return TP_OK;
+      ::tp::count_launch();
+      TP_CUDA(launch_pdl(rope_group_kernel, dim3(mn, cnt), dim3(64), 0, st, rg, (double)c.rope_theta));
+      cnt = mn = 0;
+      return TP_OK;
+    };
+    for (int g = 0; g < count; ++g) {
+      if (hi[g] == lo[g]) continue;
+      for (int r = 0; r < mem[g].count; ++r) {
+        const FwdItem& it = mem[g].items[r];
+        rg.pos[cnt] = it.lv.positions;
+        rg.out[cnt] = ws[g]->rope + (size_t)offs[g][r] * 128;
+        rg.n[cnt] = it.lv.n;
+        mn = std::max(mn, it.lv.n);
+        if (++cnt == kMaxBatchItems) TP_TRY(flush());
+      }
+    }
+    TP_TRY(flush());
+  }
   for (int g = 0; g < count; ++g) {
     const FwdMember& M = mem[g];
     if (hi[g] == lo[g]) continue;
-    for (int r = 0; r < M.count; ++r) {
-      const FwdItem& it = M.items[r];
-      ::tp::count_launch();
-      TP_CUDA(launch_pdl(rope_table_kernel, dim3(it.lv.n), dim3(64), 0, st, it.lv.positions, (double)c.rope_theta,
-                         ws[g]->rope + (size_t)offs[g][r] * 128));
-      TP_CUDA(cudaGetLastError());
-    }
     if (M.count > 1) {
       std::vector<char> blob(sizeof(QkvItem) * M.count + 4 * (size_t)ntot[g]);
       QkvItem* qi = reinterpret_cast<QkvItem*>(blob.data());

@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "gemm_tc.h"
@@ -396,12 +397,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;  // epilogue warp 0..kEpiWarps-1 (node-parallel phases)
     const int chalf = ew >> 2;  // the two warps on a TMEM lane quarter split its 16-column groups
     const int et = threadIdx.x - 64;
+    // A reduction is deferred by one segment: the next segment's partial (often
+    // the first segment of the next member, which a neighbouring CTA's reducer
+    // waits for) is published before this CTA blocks on its own tile's
+    // arrivals.  Without the deferral the waits chain CTA c -> c+1 -> c+2 ...
+    // one link per member and the chain surfaces at the end of the launch.
+    int pend_g = -1, pend_mt = 0, pend_cnt = 0, pend_cfirst = 0, pend_clast = 0;
+    auto run_pending = [&]() {
+      if (pend_g < 0) return;
+      const GemmEpi& e = grp.m[pend_g].e;
+      const int n = grp.m[pend_g].n;
+      const int* arrive = e.counters;
+      const int mt = pend_mt, cnt = pend_cnt, cfirst = pend_cfirst, clast = pend_clast;
+      const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
+      const int E = cend - cfirst + 1, rank = c - cfirst;
+      if (et == 0) {  // counters only grow: this launch's arrivals are complete at (epoch+1)*cnt
+        const int target = (e.epoch + 1) * cnt;
+        while (ld_acquire(&arrive[mt]) < target) __nanosleep(32);
+        __threadfence();
+      }
+      epi_bar();
+      reduce_apply(e, p, n, mt, cnt, n * rank / E, n * (rank + 1) / E, ew, lane);
+      epi_bar();
+      pend_g = -1;
+    };
     int seg = 0;
     for (int g = 0; g < grp.count; ++g) {
       const GemmEpi& e = grp.m[g].e;
       const int n = grp.m[g].n, npad = grp.m[g].n_pad;
       int* arrive = e.counters;
-      int* done = e.counters + p.mtiles;
       int t = t0;
       while (t < t1) {
         const int mt = t / p.KB;
@@ -431,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
+          run_pending();
         } else {
           // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
           float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * n) * kBM + r;
@@ -444,37 +469,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
-          __threadfence();
           epi_bar();
-          if (et == 0) atomicAdd(&arrive[mt], 1);
+          if (et == 0) {  // barrier + one gpu-scope fence publishes every epilogue thread's stores
+            __threadfence();
+            atomicAdd(&arrive[mt], 1);
+          }
+          run_pending();  // the previous segment's reduction, now that this partial is out
           // ... and, if this segment ends the CTA's range of this member, reduce a
-          // slice of the tile's nodes once every partial is in.  The contributors
-          // whose ranges end inside the tile finish together; splitting the nodes
-          // among them keeps the fix-up short (one CTA reducing a whole tile was
-          // measured 2x slower on the o / down projections).  The tile's other
-          // contributor (at most one: the CTA whose range *starts* in the tile)
-          // published early in its pass over this member.  Waits only ever point
-          // at an earlier (member, position), so the chain cannot cycle.
+          // slice of the tile's nodes once every partial is in (deferred, above).
+          // The contributors whose ranges end inside the tile finish together;
+          // splitting the nodes among them keeps the fix-up short (one CTA
+          // reducing a whole tile was measured 2x slower on the o / down
+          // projections).  Waits only ever point at an earlier (member,
+          // position) or at a partial published before any wait: no cycle.
           if (fixup_mode == 0 && t1 <= (mt + 1) * p.KB) {
-            const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
-            const int E = cend - cfirst + 1, rank = c - cfirst;
-            if (et == 0) {
-              while (ld_acquire(&arrive[mt]) < cnt) __nanosleep(64);
-              __threadfence();
-            }
-            epi_bar();
-            reduce_apply(e, p, n, mt, cnt, n * rank / E, n * (rank + 1) / E, ew, lane);
-            epi_bar();
-            if (et == 0 && atomicAdd(&done[mt], 1) == E - 1) {  // every reducer is past its wait
-              arrive[mt] = 0;
-              done[mt] = 0;
-            }
+            pend_g = g;
+            pend_mt = mt;
+            pend_cnt = cnt;
+            pend_cfirst = cfirst;
+            pend_clast = clast;
           }
         }
         t = seg_end;
         ++seg;
       }
     }
+    run_pending();
   }
   __syncthreads();
   if (warp == 1) {
@@ -494,7 +514,36 @@ static std::vector<ProfRec> g_prof;
 static bool g_prof_on = false;
 static std::mutex g_prof_mu;
 
-int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st) {
+// Launch epochs of every arrival-counter array (keyed by its device address):
+// counters are never reset, a launch waits for (epoch+1)*cnt arrivals per tile.
+static std::mutex g_epoch_mu;
+static std::unordered_map<const int*, int> g_epochs;
+
+void sk_counters_forget(const void* base, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_epoch_mu);
+  const char* lo = static_cast<const char*>(base);
+  for (auto it = g_epochs.begin(); it != g_epochs.end();) {
+    const char* k = reinterpret_cast<const char*>(it->first);
+    if (k >= lo && k < lo + bytes)
+      it = g_epochs.erase(it);
+    else
+      ++it;
+  }
+}
+
+int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
+  GemmGroup grp = grp_in;
+  {
+    std::lock_guard<std::mutex> lk(g_epoch_mu);
+    for (int g = 0; g < grp.count; ++g) {
+      int& ep = g_epochs[grp.m[g].e.counters];
+      if ((int64_t)(ep + 2) * p.max_contrib >= (1 << 30)) {  // ~7M launches: restart the count
+        TP_CUDA(cudaMemsetAsync(grp.m[g].e.counters, 0, (size_t)p.mtiles * sizeof(int), st));
+        ep = 0;
+      }
+      grp.m[g].e.epoch = ep++;
+    }
+  }
   TP_CHECK(grp.count >= 1 && grp.count <= kMaxGroup, TP_ECONFIG, "GEMM group size outside [1, 8]");
   int mx = 16;
   for (int g = 0; g < grp.count; ++g) {
@@ -620,6 +669,7 @@ extern "C" int tp_debug_gemm_group_timed(int32_t device, int32_t count, const vo
     pg.n = n[g];
     TP_CUDA(cudaMalloc((void**)&m.e.part, sk_part_floats(pg) * 4));
     TP_CUDA(cudaMalloc((void**)&m.e.counters, 2 * p.mtiles * 4));
+    sk_counters_forget(m.e.counters, 2 * p.mtiles * 4);
     TP_CUDA(cudaMemsetAsync(m.e.counters, 0, 2 * p.mtiles * 4, st));
     bufs.push_back(m.e.part);
     bufs.push_back(m.e.counters);
@@ -657,6 +707,7 @@ extern "C" int tp_debug_gemm(int32_t device, const void* w_dev, const void* x_de
   e.out_ld = n_out;
   TP_CUDA(cudaMallocAsync((void**)&e.part, sk_part_floats(p) * 4, st));
   TP_CUDA(cudaMallocAsync((void**)&e.counters, 2 * p.mtiles * 4, st));
+  sk_counters_forget(e.counters, 2 * p.mtiles * 4);
   TP_CUDA(cudaMemsetAsync(e.counters, 0, 2 * p.mtiles * 4, st));
   TP_TRY(sk_gemm(&ma, &mb, p, e, st));
   TP_CUDA(cudaFreeAsync(e.part, st));
@@ -681,6 +732,7 @@ extern "C" int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void
   e.out_ld = n_out;
   TP_CUDA(cudaMalloc((void**)&e.part, sk_part_floats(p) * 4));
   TP_CUDA(cudaMalloc((void**)&e.counters, 2 * p.mtiles * 4));
+  sk_counters_forget(e.counters, 2 * p.mtiles * 4);
   TP_CUDA(cudaMemsetAsync(e.counters, 0, 2 * p.mtiles * 4, st));
   TP_TRY(sk_gemm(&ma, &mb, p, e, st));  // warm-up
   cudaEvent_t a, b;

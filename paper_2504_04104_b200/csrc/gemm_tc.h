@@ -54,7 +54,8 @@ struct GemmEpi {
   int f = 0;
   // stream-K fix-up state
   float* part = nullptr;  // [mtiles][max_contrib][n][128]
-  int* counters = nullptr;  // [2][mtiles] arrivals | reducers done; zero between launches (self-resetting)
+  int* counters = nullptr;  // [mtiles] arrival counters, monotonic across launches (see epoch)
+  int epoch = 0;            // launches that used `counters` before this one (set by sk_gemm_group)
 };
 
 // A grouped launch: up to kMaxGroup GEMMs of the SAME (N_out, K) shape — e.g. the
@@ -87,6 +88,9 @@ inline size_t sk_part_floats(const SkPlan& p) { return (size_t)p.mtiles * p.max_
 int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st);
 // Grouped launch (members share p's shape; p.n / p.n_pad are ignored).
 int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st);
+// Forget the launch epochs of counter arrays in [base, base+bytes) (call whenever
+// such memory is (re)allocated and zeroed).
+void sk_counters_forget(const void* base, size_t bytes);
 
 
 }  // namespace tp

@@ -283,6 +283,7 @@ static int ws_get(tp_model* m, int g, int min_chunks, LlamaWs** out) {
     e->ctr_stride = 2 * mt;  // arrivals | reducers done, per GEMM kind
     TP_CUDA(cudaMalloc(&e->counters, (size_t)kCtrKinds * e->ctr_stride * 4));
     TP_CUDA(cudaMemset(e->counters, 0, (size_t)kCtrKinds * e->ctr_stride * 4));
+    sk_counters_forget(e->counters, (size_t)kCtrKinds * e->ctr_stride * 4);
     TP_TRY(make_tmap_kmajor(&e->mXd, e->Xd, np, d, 16));
     TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
     TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));

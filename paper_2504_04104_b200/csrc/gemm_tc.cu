@@ -242,11 +242,11 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
   for (int c = lo + ew; c < hi; c += 2 * kEpiWarps) {
     const int c2 = c + kEpiWarps;
     const bool two = c2 < hi;
-    const float4 y0 = sum_partials(base, slot, cnt, c, f);
-    const float4 y1 = two ? sum_partials(base, slot, cnt, c2, f) : y0;
-    EpiAux x0{}, x1{};
+    EpiAux x0{}, x1{};  // operands of the op first: their loads overlap the partial loads
     epi_aux(e, mt, f, c, x0);
     if (two) epi_aux(e, mt, f, c2, x1);
+    const float4 y0 = sum_partials(base, slot, cnt, c, f);
+    const float4 y1 = two ? sum_partials(base, slot, cnt, c2, f) : y0;
     epi_finish(e, mt, lane, c, y0, x0);
     if (two) epi_finish(e, mt, lane, c2, y1, x1);
   }

@@ -55,6 +55,14 @@ __device__ __forceinline__ uint32_t pack_f32(float lo, float hi) {
   return pack_bf16(__float2bfloat16_rn(lo), __float2bfloat16_rn(hi));
 }
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// exp(x) as one MUFU op: 2^(x*log2 e) with ex2.approx (flush-to-zero; every
+// attention path — shared chunks, per-node tail, tile, merges — uses this same
+// function, so batch invariance is unaffected).
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(x, 1.4426950408889634f)));
+  return y;
+}
 __device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -143,7 +151,7 @@ __device__ __forceinline__ void chunk_softmax(float (&s)[8][4], const int (&lim)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int h = e >> 1;
-      const float p = s[nt][e] == -INFINITY ? 0.f : expf(__fsub_rn(s[nt][e], mc[h]));
+      const float p = s[nt][e] == -INFINITY ? 0.f : fast_exp(__fsub_rn(s[nt][e], mc[h]));
       s[nt][e] = p;
       rs[h] = __fadd_rn(rs[h], p);
     }
@@ -191,8 +199,8 @@ __device__ __forceinline__ void chunk_pv(const uint32_t (&pa)[4][4], const __nv_
 // Online merge of a chunk partial (mc, lc, oc) into the running (M, L, O).
 __device__ __forceinline__ void merge_scale(float& M, float& L, float mc, float lc, float& sa, float& sb) {
   const float mn = fmaxf(M, mc);
-  sa = M == -INFINITY ? 0.f : expf(__fsub_rn(M, mn));
-  sb = expf(__fsub_rn(mc, mn));
+  sa = M == -INFINITY ? 0.f : fast_exp(__fsub_rn(M, mn));
+  sb = fast_exp(__fsub_rn(mc, mn));
   L = __fmaf_rn(L, sa, __fmul_rn(lc, sb));
   M = mn;
 }

@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-perfect", action="store_true", help="skip the perfect-draft TBT field")
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--db-model", default="13b", choices=["7b", "13b", "70b", "tiny"])
     ap.add_argument("--db-batches", default="1,16", help="SpecPipe-DB batch sizes (empty: skip)")
@@ -422,6 +423,31 @@ def run_ours(args, rank, world):
         ms, info = cpu_step_estimate(cfg, node_layers / max(1, len(resident)), 1.0, args.prompt_len)
         line["cpu_baseline"] = {"value": round(ms * steps_per_token, 2), "unit": UNIT, "cores": os.cpu_count(),
                                 "kind": "port", "sample": info["sample"]}
+    if args.draft == "paper" and not args.no_perfect:
+        # the same engine with a perfect draft (every verification hits): steps/token -> 1,
+        # isolating system overhead against the one-token-per-pipeline-step bound
+        pdraft = tp.SyntheticDraft(draft_cfg("perfect"), cfg.vocab)
+        pdraft.bind_reference(tuple(prompt) + tuple(ref))
+        pr = fresh(pdraft)
+        for _ in range(args.warmup):
+            pr.decode_step()
+        sync_all()
+        pt0 = len(pr.emitted)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(streams[0])
+        nsteps = min(args.steps, max(8, len(ref) - len(pr.emitted) - args.stages - 2))
+        for _ in range(nsteps):
+            pr.decode_step()
+        f1.record(streams[0])
+        sync_all()
+        ptok = len(pr.emitted) - pt0
+        assert pr.emitted == ref[: len(pr.emitted)]
+        line["perfect_draft"] = {"tbt_ms_per_token": round(f0.elapsed_time(f1) / max(1, ptok), 4),
+                                 "steps": nsteps, "tokens": ptok,
+                                 "ms_per_step": round(f0.elapsed_time(f1) / nsteps, 4),
+                                 "ideal_ms_per_step_all_stages_occupied": round(
+                                     (args.stages * (cfg.layers // args.stages) * layer_w + head_w) / (peak * 1e6), 4)}
+        pr.close()
     if rank == 0 and ngpu == 1 and args.db_batches:
         line["specpipe_db"] = run_db(args)
     print(json.dumps(line), flush=True)

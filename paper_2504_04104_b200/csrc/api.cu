@@ -287,8 +287,26 @@ int tp_model_create(const tp_model_config* cfg, tp_model** out) {
   return TP_OK;
 }
 
+static void stage_release(tp_stage* s);
+static void model_free_now(tp_model* m);
+
 int tp_model_destroy(tp_model* m) {
   if (!m) return TP_OK;
+  std::vector<tp_stage*> parked;
+  bool now;
+  {
+    std::lock_guard<std::mutex> lk(m->pool_mu);
+    parked.swap(m->stage_pool);
+    now = m->live_stages == 0;
+    m->destroy_pending = !now;
+  }
+  cudaSetDevice(m->cfg.device);
+  for (tp_stage* s : parked) stage_release(s);
+  if (now) model_free_now(m);
+  return TP_OK;
+}
+
+static void model_free_now(tp_model* m) {
   cudaSetDevice(m->cfg.device);
   if (m->embed) cudaFree(m->embed);
   if (m->head) cudaFree(m->head);
@@ -298,7 +316,6 @@ int tp_model_destroy(tp_model* m) {
   if (!is_toy(m)) llama_model_free(m);
   call_ring_free(m);
   delete m;
-  return TP_OK;
 }
 
 int tp_model_init_lcg(tp_model* m, uint64_t seed, void* stream) {
@@ -375,12 +392,27 @@ int tp_model_read_tensor(const tp_model* m, int32_t which, int32_t layer, void* 
   return TP_OK;
 }
 
+static void stage_release(tp_stage* s);
+
 int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t capacity_rows, tp_stage** out) {
   TP_CHECK(m && out, TP_ECONFIG, "null argument");
   TP_CHECK(m->cfg.layer_lo <= layer_lo && layer_lo <= layer_hi && layer_hi <= m->cfg.layer_hi, TP_ECONFIG,
            "stage layers must be hosted by the model");
   TP_CHECK(capacity_rows >= 1, TP_ECONFIG, "capacity must be positive");
   TP_CUDA(cudaSetDevice(m->cfg.device));
+  {  // reuse a parked stage of the same shape (no allocation, no device sync)
+    std::lock_guard<std::mutex> lk(m->pool_mu);
+    for (size_t i = 0; i < m->stage_pool.size(); ++i) {
+      tp_stage* p = m->stage_pool[i];
+      if (p->lo == layer_lo && p->hi == layer_hi && p->cap >= capacity_rows && p->cap <= 4 * capacity_rows) {
+        m->stage_pool.erase(m->stage_pool.begin() + (long)i);
+        p->rows = 0;
+        ++m->live_stages;
+        *out = p;
+        return TP_OK;
+      }
+    }
+  }
   tp_stage* s = new tp_stage();
   s->m = m;
   s->lo = layer_lo;
@@ -398,7 +430,7 @@ int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t cap
   }
   int rc = alloc_kv(s, capacity_rows);
   if (rc != TP_OK) {
-    tp_stage_destroy(s);
+    stage_release(s);  // partially built: free, never park
     return rc;
   }
   TP_CUDA(cudaMalloc((void**)&s->ws, s->ws_bytes));
@@ -415,16 +447,37 @@ int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t cap
   if (!is_toy(m)) {
     rc = llama_stage_init(s);
     if (rc != TP_OK) {
-      tp_stage_destroy(s);
+      stage_release(s);
       return rc;
     }
+  }
+  {
+    std::lock_guard<std::mutex> lk(m->pool_mu);
+    ++m->live_stages;
   }
   *out = s;
   return TP_OK;
 }
 
+static void stage_release(tp_stage* s);
+
 int tp_stage_destroy(tp_stage* s) {
   if (!s) return TP_OK;
+  tp_model* m = s->m;
+  bool release, free_model = false;
+  {
+    std::lock_guard<std::mutex> lk(m->pool_mu);
+    --m->live_stages;
+    release = m->destroy_pending;
+    if (!release) m->stage_pool.push_back(s);  // parked: reused, or freed with the model
+    free_model = release && m->live_stages == 0;
+  }
+  if (release) stage_release(s);
+  if (free_model) model_free_now(m);
+  return TP_OK;
+}
+
+static void stage_release(tp_stage* s) {
   cudaSetDevice(s->m->cfg.device);
   for (void* p : s->k) cudaFree(p);
   for (void* p : s->v) cudaFree(p);
@@ -440,7 +493,6 @@ int tp_stage_destroy(tp_stage* s) {
   if (s->logits) cudaFree(s->logits);
   if (!is_toy(s->m)) llama_stage_free(s);
   delete s;
-  return TP_OK;
 }
 
 int tp_stage_rows(const tp_stage* s, int32_t* rows) {

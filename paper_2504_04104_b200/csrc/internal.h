@@ -1,6 +1,7 @@
 // Internal object layout shared by the C-ABI (api.cu) and the kernel files.
 #pragma once
 
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -22,6 +23,16 @@ struct tp_model {
   // llama: tensor maps for TMA live beside the weights (filled lazily)
   void* tma_cache = nullptr;
   void* call_ring = nullptr;  // staging ring for multi-level / multi-stage calls (api.cu)
+  // Destroyed stages are parked here and reused by tp_stage_create (same layer
+  // range, enough capacity): cudaFree / cudaFreeHost synchronise the device, and
+  // a request finishing mid-stream (SpecPipe-DB) must not stall every other one.
+  std::vector<tp_stage*> stage_pool;
+  std::mutex pool_mu;
+  // Stages keep their model alive: Python may finalise a model before its
+  // caches (cyclic GC), so tp_model_destroy defers the free until the last
+  // live stage is destroyed.
+  int live_stages = 0;
+  bool destroy_pending = false;
 };
 
 struct tp_stage {

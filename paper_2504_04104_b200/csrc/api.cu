@@ -52,6 +52,7 @@ extern "C" int tp_debug_attn_tile(int32_t on) {
 extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
   if (knob == 0) tp::attn_set_tile(value != 0);
   else if (knob == 1) tp::attn_set_shared_run(value);
+  else if (knob == 2) tp::attn_set_tail2(value != 0);
   else return TP_ECONFIG;
   return TP_OK;
 }

@@ -42,6 +42,7 @@ constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ld
 constexpr int kCtaNodes = 64;
 constexpr int kWarps = 4;
 constexpr int kTileElems = kAttnChunk * kPad;
+static bool g_attn_tail2 = false;  // shared-prefix tail for uniform levels (knob 2): bit-exact, measured no faster
 static bool g_attn_tile = false;  // measured slower than the per-node tail on the bench workload  // tp_debug_attn_tile(0) forces the per-node path (tests)
 constexpr size_t kTailSmem = (size_t)kWarps * kTileElems * 2;
 
@@ -123,6 +124,42 @@ __device__ __forceinline__ void tile_qk(const uint32_t (&qa)[8][4], const __nv_b
       mma16816(s[nt], qa[2 * k2 + 1], b[2], b[3]);
     }
   }
+}
+
+// The same MMA sequences with per-slot row pointers (rows gathered from a CTA
+// tile, a per-warp own-row buffer and a zero row): identical fragments, so
+// identical results.
+template <typename RowK>
+__device__ __forceinline__ void tile_qk_rows(const uint32_t (&qa)[8][4], RowK rowK, float (&s)[8][4], int lane) {
+  const int mi = lane >> 3, mr = lane & 7;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+    const __nv_bfloat16* rp = rowK(nt * 8 + mr);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      uint32_t b[4];
+      ldsm4(su32(rp + 32 * k2 + 8 * mi), b);
+      mma16816(s[nt], qa[2 * k2], b[0], b[1]);
+      mma16816(s[nt], qa[2 * k2 + 1], b[2], b[3]);
+    }
+  }
+}
+
+template <typename RowV>
+__device__ __forceinline__ void chunk_pv_rows(const uint32_t (&pa)[4][4], RowV rowV, float (&o)[16][4], int lane) {
+  const int mi = lane >> 3, mr = lane & 7;
+#pragma unroll
+  for (int nd = 0; nd < 16; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+#pragma unroll
+  for (int n2 = 0; n2 < 8; ++n2)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t b[4];
+      ldsm4t(su32(rowV(16 * kk + 8 * (mi & 1) + mr) + 16 * n2 + 8 * (mi >> 1)), b);
+      mma16816(o[2 * n2], pa[kk], b[0], b[1]);
+      mma16816(o[2 * n2 + 1], pa[kk], b[2], b[3]);
+    }
 }
 
 // Chunk softmax of the raw scores: rows g / g+8 see slots [0, lim); returns the
@@ -214,7 +251,10 @@ __device__ __forceinline__ size_t part_idx(const AttnArgs& a, int node, int h, i
 
 // kind: 0 shared, 1 per-node tail, 2 tile
 __device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
-  auto start = [&](int g) { return kind == 0 ? G.m[g].cta_shared : (kind == 1 ? G.m[g].cta_tail : G.m[g].cta_tile); };
+  auto start = [&](int g) {
+    return kind == 0 ? G.m[g].cta_shared
+                     : (kind == 1 ? G.m[g].cta_tail : (kind == 2 ? G.m[g].cta_tile : G.m[g].cta_tail2));
+  };
   int gi = 0;
   while (gi + 1 < G.count && b >= start(gi + 1)) ++gi;
   return gi;
@@ -709,11 +749,151 @@ __global__ void __launch_bounds__(kWarps * 32) attn_tile_kernel(const __grid_con
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Per-node tail for uniform tree levels (every node: prefix P, A ancestors):
+// a CTA's 4 warps are 4 nodes of one (member, head), so the tail chunk's
+// prefix rows [64c, P) are staged ONCE per CTA; each warp stages only its own
+// <= kOwnMax rows (ancestors + self).  The chunk math reads fragments through
+// per-slot row pointers — the same bytes in the same MMA order as the per-node
+// path, hence the same bits.
+constexpr int kOwnMax = 16;
+constexpr size_t kTail2Smem = (size_t)2 * kTileElems * 2 + (size_t)kWarps * 2 * kOwnMax * kPad * 2 +
+                              (size_t)kPad * 2 + (size_t)kWarps * 128 * 4;
+
+__global__ void __launch_bounds__(kWarps * 32, 3) attn_tail2_kernel(const __grid_constant__ AttnGroup G) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int gi = member_of(G, blockIdx.x, 3);
+  const AttnArgs& a = G.m[gi].a;
+  const LevelDev& lv = G.m[gi].lv;
+  const int local = blockIdx.x - G.m[gi].cta_tail2;
+  const int h = local % a.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int i = (local / a.H) * kWarps + warp;
+  const bool valid = i < lv.n;
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(dsm);
+  __nv_bfloat16* sV = sK + kTileElems;
+  __nv_bfloat16* oK = sV + kTileElems + (size_t)warp * 2 * kOwnMax * kPad;
+  __nv_bfloat16* oV = oK + kOwnMax * kPad;
+  __nv_bfloat16* zrow = sV + kTileElems + (size_t)kWarps * 2 * kOwnMax * kPad;
+  float* xo = reinterpret_cast<float*>(zrow + kPad) + warp * 128;
+  for (int e = threadIdx.x; e < kPad; e += blockDim.x) zrow[e] = __float2bfloat16_rn(0.f);
+  const int kh = h / (a.H / a.KV);
+  const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
+  const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
+  const int c_start = G.m[gi].c_shared;
+  const int P = lv.min_p, A = lv.uniform_a, T = P + A + 1;
+  const int ic = valid ? i : 0;
+  const size_t pbase = part_idx(a, ic, h, 0);
+  float pm_l = -INFINITY, pl_l = 0.f;
+  if (valid && lane < c_start) {
+    pm_l = __ldcg(a.pm + pbase + lane);
+    pl_l = __ldcg(a.pl + pbase + lane);
+  }
+  const int32_t* anc = lv.anc_rows + (size_t)ic * lv.anc_stride;
+  const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)ic * a.KV + kh) * kAttnHeadDim
+                                       : Kh + (size_t)(lv.row0 + ic) * kAttnHeadDim;
+  const __nv_bfloat16* vself = a.vself ? a.vself + ((size_t)ic * a.KV + kh) * kAttnHeadDim
+                                       : Vh + (size_t)(lv.row0 + ic) * kAttnHeadDim;
+  uint32_t q1[8][4];
+  const __nv_bfloat16* qr = a.q + (size_t)ic * a.q_stride + h * kAttnHeadDim;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    q1[kk][0] = (valid && g == 0) ? ld_b32(qr + 16 * kk + 2 * tig) : 0u;
+    q1[kk][1] = 0u;
+    q1[kk][2] = (valid && g == 0) ? ld_b32(qr + 16 * kk + 8 + 2 * tig) : 0u;
+    q1[kk][3] = 0u;
+  }
+  float M = -INFINITY, L = 0.f;
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    const float* po = a.po + pbase * kAttnHeadDim + 4 * lane;
+    float4 nxt = c_start > 0 ? __ldcg(reinterpret_cast<const float4*>(po)) : O;
+    for (int c = 0; c < c_start; ++c) {
+      if (c > 0 && (c & 31) == 0) {
+        pm_l = c + lane < c_start ? __ldcg(a.pm + pbase + c + lane) : -INFINITY;
+        pl_l = c + lane < c_start ? __ldcg(a.pl + pbase + c + lane) : 0.f;
+      }
+      const float4 cur = nxt;
+      if (c + 1 < c_start) nxt = __ldcg(reinterpret_cast<const float4*>(po + (size_t)(c + 1) * kAttnHeadDim));
+      float sa, sb;
+      merge_scale(M, L, __shfl_sync(0xffffffffu, pm_l, c & 31), __shfl_sync(0xffffffffu, pl_l, c & 31), sa, sb);
+      O.x = merge_val(O.x, cur.x, sa, sb);
+      O.y = merge_val(O.y, cur.y, sa, sb);
+      O.z = merge_val(O.z, cur.z, sa, sb);
+      O.w = merge_val(O.w, cur.w, sa, sb);
+    }
+  }
+  const int c_end = (T + kAttnChunk - 1) / kAttnChunk;
+  const int part = lane & 15, rsub = lane >> 4;
+  for (int c = c_start; c < c_end; ++c) {
+    const int j0 = c * kAttnChunk;
+    const int np = min(max(P - j0, 0), kAttnChunk);  // prefix rows of this chunk (shared by the CTA)
+    const int nt = min(T - j0, kAttnChunk);
+    __syncthreads();  // everybody is done with the previous chunk's rows
+    for (int e = threadIdx.x; e < np * 16; e += kWarps * 32) {
+      const int row = e >> 4, pt = e & 15;
+      cp16(sK + row * kPad + pt * 8, Kh + (size_t)(j0 + row) * kAttnHeadDim + pt * 8, 16);
+      cp16(sV + row * kPad + pt * 8, Vh + (size_t)(j0 + row) * kAttnHeadDim + pt * 8, 16);
+    }
+    if (valid) {
+      for (int row = np + rsub; row < nt; row += 2) {  // own rows: ancestors, then self
+        const int j = j0 + row, o = j - P;
+        const bool is_anc = j < P + A;
+        const __nv_bfloat16* ks = is_anc ? Kh + (size_t)anc[o] * kAttnHeadDim : kself;
+        const __nv_bfloat16* vs = is_anc ? Vh + (size_t)anc[o] * kAttnHeadDim : vself;
+        cp16(oK + o * kPad + part * 8, ks + part * 8, 16);
+        cp16(oV + o * kPad + part * 8, vs + part * 8, 16);
+      }
+    }
+    cp_wait_all();
+    __syncthreads();
+    if (!valid) continue;
+    auto rowK = [&](int slot) -> const __nv_bfloat16* {
+      const int j = j0 + slot;
+      return j < P ? sK + slot * kPad : (j < T ? oK + (j - P) * kPad : zrow);
+    };
+    auto rowV = [&](int slot) -> const __nv_bfloat16* {
+      const int j = j0 + slot;
+      return j < P ? sV + slot * kPad : (j < T ? oV + (j - P) * kPad : zrow);
+    };
+    const int lim[2] = {g == 0 ? nt : 0, 0};
+    float s[8][4], m[2], l[2], o[16][4];
+    uint32_t pa[4][4];
+    tile_qk_rows(q1, rowK, s, lane);
+    chunk_softmax(s, lim, a.scale, m, l, pa, lane);
+    chunk_pv_rows(pa, rowV, o, lane);
+    if (g == 0) {
+#pragma unroll
+      for (int nd = 0; nd < 16; ++nd)
+        *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
+    }
+    __syncwarp();
+    const float4 oc = *reinterpret_cast<const float4*>(xo + 4 * lane);
+    __syncwarp();
+    float sa, sb;
+    merge_scale(M, L, __shfl_sync(0xffffffffu, m[0], 0), __shfl_sync(0xffffffffu, l[0], 0), sa, sb);
+    O.x = merge_val(O.x, oc.x, sa, sb);
+    O.y = merge_val(O.y, oc.y, sa, sb);
+    O.z = merge_val(O.z, oc.z, sa, sb);
+    O.w = merge_val(O.w, oc.w, sa, sb);
+  }
+  if (!valid) return;
+  __nv_bfloat16* out = a.out + (size_t)i * a.out_stride + h * kAttnHeadDim + 4 * lane;
+  uint2 u;
+  u.x = pack_f32(__fdiv_rn(O.x, L), __fdiv_rn(O.y, L));
+  u.y = pack_f32(__fdiv_rn(O.z, L), __fdiv_rn(O.w, L));
+  *reinterpret_cast<uint2*>(out) = u;
+}
+
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
   TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 64]");
   AttnGroup G;
   G.count = count;
-  int cs = 0, ct = 0, cg = 0;
+  int cs = 0, ct = 0, cg = 0, c2 = 0;
   for (int g = 0; g < count; ++g) {
     AttnMember& m = G.m[g];
     m.a = a[g];
@@ -723,18 +903,24 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     const int c_max = (lv[g].max_t + kAttnChunk - 1) / kAttnChunk;
     TP_CHECK(c_max <= a[g].max_chunks, TP_ESHAPE, "attention chunks exceed scratch");
     const bool tiled = g_attn_tile && lv[g].uniform_a >= 0 && lv[g].uniform_a + 1 <= kTileOwn && lv[g].n >= 4;
+    const bool tail2 = !tiled && g_attn_tail2 && lv[g].uniform_a >= 0 && lv[g].uniform_a + 1 <= kOwnMax &&
+                       lv[g].n >= 2;
     m.cta_shared = cs;
     m.cta_tail = ct;
     m.cta_tile = cg;
+    m.cta_tail2 = c2;
     cs += a[g].H * ((m.c_shared + g_shared_run - 1) / g_shared_run) * m.zt;
     if (tiled)
       cg += a[g].H * m.zt;
+    else if (tail2)
+      c2 += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
     else
       ct += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
   }
   G.ctas_shared = cs;
   G.ctas_tail = ct;
   G.ctas_tile = cg;
+  G.ctas_tail2 = c2;
   static bool attr_set[64] = {false};  // per device
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
@@ -742,6 +928,7 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     TP_CUDA(cudaFuncSetAttribute(attn_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailSmem));
     TP_CUDA(cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
     TP_CUDA(cudaFuncSetAttribute(attn_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSharedSmem));
+    TP_CUDA(cudaFuncSetAttribute(attn_tail2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTail2Smem));
     attr_set[dev & 63] = true;
   }
   if (cs > 0) {
@@ -757,6 +944,12 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tile", st);
   }
+  if (c2 > 0) {
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(attn_tail2_kernel, dim3(c2), dim3(kWarps * 32), kTail2Smem, st, G));
+    TP_CUDA(cudaGetLastError());
+    timeline_mark("attn_tail2", st);
+  }
   if (ct > 0) {
     ::tp::count_launch();
     TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kWarps * 32), kTailSmem, st, G));
@@ -769,6 +962,7 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st) { return attn_tree_group(&a, &lv, 1, st); }
 
 void attn_set_tile(bool on) { g_attn_tile = on; }
+void attn_set_tail2(bool on) { g_attn_tail2 = on; }
 void attn_set_shared_run(int n) { g_shared_run = n < 1 ? 1 : (n > kSharedRunMax ? kSharedRunMax : n); }
 
 }  // namespace tp

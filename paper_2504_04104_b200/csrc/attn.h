@@ -37,17 +37,19 @@ struct AttnMember {
   int cta_shared;  // first CTA of this member in the shared launch
   int cta_tail;    // first CTA of this member in the per-node tail launch (empty range if tiled)
   int cta_tile;    // first CTA of this member in the 16-node tile launch (empty range if per-node)
+  int cta_tail2;   // first CTA of this member in the shared-prefix tail launch (uniform levels)
 };
 
 struct AttnGroup {
   AttnMember m[kAttnMaxGroup];
   int count;
-  int ctas_shared, ctas_tail, ctas_tile;
+  int ctas_shared, ctas_tail, ctas_tile, ctas_tail2;
 };
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
 void attn_set_tile(bool on);
 void attn_set_shared_run(int n);
+void attn_set_tail2(bool on);
 // members[0..count) -> two launches (shared chunks, then per-node tail + ordered combine)
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st);
 

@@ -267,8 +267,9 @@ def test_llama_long_context_invariance_and_oracle():
 
 @pytest.mark.parametrize("w,k", [(16, 4), (24, 8)])
 def test_tile_attention_equals_per_node_path(w, k):
-    """The 16-node tile path of K1 (uniform tree levels) is bit-identical to the
-    per-node path on every stage output of a wide-tree pipeline run."""
+    """The 16-node tile path and the shared-prefix tail of K1 (uniform tree
+    levels) are bit-identical to the plain per-node path on every stage output
+    of a wide-tree pipeline run."""
     cfg, m, _ = tiny_model(layers=4)
     prompt = [int(t) for t in np.random.default_rng(6).integers(0, cfg.vocab, 150)]
     ref = tp.sequential_decode(m, prompt, 40)
@@ -285,9 +286,12 @@ def test_tile_attention_equals_per_node_path(w, k):
     assert rec.emitted == ref[: len(rec.emitted)]
     lib = _lib.lib()
     runs = {}
+    # (tile, tail2): 16-node tile path, shared-prefix tail, plain per-node tail
+    modes = {"tile": (1, 0), "tail2": (0, 1), "per_node": (0, 0)}
     try:
-        for tile in (1, 0):
-            _lib.check(lib.tp_debug_attn_tile(tile))
+        for name, (tile, tail2) in modes.items():
+            _lib.check(lib.tp_debug_attn_knob(0, tile))
+            _lib.check(lib.tp_debug_attn_knob(2, tail2))
             _lib.check(lib.tp_debug_attn_knob(1, 3 if tile else 1))  # multi-chunk shared CTAs too
             r = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=w, k=k), None,
                                collect_trace=False)
@@ -297,15 +301,17 @@ def test_tile_attention_equals_per_node_path(w, k):
                 r.launch_compute()
                 outs.append([None if s.out is None else s.out.cpu().clone() for s in r.stages])
                 r.step(ch)
-            runs[tile] = outs
+            runs[name] = outs
     finally:
-        _lib.check(lib.tp_debug_attn_tile(0))
+        _lib.check(lib.tp_debug_attn_knob(0, 0))
+        _lib.check(lib.tp_debug_attn_knob(2, 0))
         _lib.check(lib.tp_debug_attn_knob(1, 1))
     wide = 0
-    for a_, b_ in zip(runs[1], runs[0]):
-        for x, y in zip(a_, b_):
-            assert (x is None) == (y is None)
-            if x is not None:
-                assert torch.equal(x, y)
-                wide += x.shape[0] >= 4
+    for other in ("tile", "tail2"):
+        for a_, b_ in zip(runs[other], runs["per_node"]):
+            for x, y in zip(a_, b_):
+                assert (x is None) == (y is None)
+                if x is not None:
+                    assert torch.equal(x, y), other
+                    wide += x.shape[0] >= 4
     assert wide > 5

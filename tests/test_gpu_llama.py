@@ -315,3 +315,26 @@ def test_tile_attention_equals_per_node_path(w, k):
                     assert torch.equal(x, y), other
                     wide += x.shape[0] >= 4
     assert wide > 5
+
+
+def test_kv_capacity_growth_mid_decode_lossless():
+    """Caches that start far too small grow by doubling (tp_stage_reserve:
+    planes re-allocated and copied, attention scratch regrown) in the middle of
+    a SpecPipe decode; the output stays identical to the greedy decode."""
+    cfg, m, _ = tiny_model(layers=4)
+    prompt = [int(t) for t in np.random.default_rng(12).integers(0, cfg.vocab, 40)]
+    want = tp.sequential_decode(m, prompt, 24)
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.7, rank_decay=0.5, miss_prob=0.05, seed=8),
+                              cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(want))
+    from paper_2504_04104_b200.pipeline import PipelineRunner
+
+    r = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=12, k=4), draft, collect_trace=False,
+                       kv_capacity=8)
+    r.prefill(prompt)  # already grows 8 -> 64 rows
+    caps0 = [s.kv._cap for s in r.stages]
+    assert all(c >= len(prompt) for c in caps0)
+    while len(r.emitted) < 24:
+        r.decode_step()
+    assert r.emitted[:24] == want
+    assert any(s.kv._cap > c for s, c in zip(r.stages, caps0))  # and again while decoding

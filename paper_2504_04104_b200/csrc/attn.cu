@@ -252,8 +252,11 @@ __device__ __forceinline__ size_t part_idx(const AttnArgs& a, int node, int h, i
 // kind: 0 shared, 1 per-node tail, 2 tile
 __device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
   auto start = [&](int g) {
-    return kind == 0 ? G.m[g].cta_shared
-                     : (kind == 1 ? G.m[g].cta_tail : (kind == 2 ? G.m[g].cta_tile : G.m[g].cta_tail2));
+    return kind == 0   ? G.m[g].cta_shared
+           : kind == 1 ? G.m[g].cta_tail
+           : kind == 2 ? G.m[g].cta_tile
+           : kind == 3 ? G.m[g].cta_tail2
+                       : G.m[g].cta_gqa;
   };
   int gi = 0;
   while (gi + 1 < G.count && b >= start(gi + 1)) ++gi;
@@ -276,20 +279,24 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
   const AttnArgs& a = G.m[gi].a;
   const LevelDev& lv = G.m[gi].lv;
   const int runs = (G.m[gi].c_shared + run_len - 1) / run_len;
+  // one CTA per (member, KV head, run of chunks, 64-node block): the K/V chunk is
+  // staged once for every query head of the GQA group (MHA: group of 1)
   int local = blockIdx.x - G.m[gi].cta_shared;
-  const int h = local % a.H;
-  local /= a.H;
+  const int kh = local % a.KV;
+  local /= a.KV;
   const int run = local % runs, base = (local / runs) * kCtaNodes;
   const int c0 = run * run_len, c1 = min(G.m[gi].c_shared, c0 + run_len);
-  const int kh = h / (a.H / a.KV);
+  const int grp = a.H / a.KV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int nreal = min(kCtaNodes, lv.n - base);
-  __nv_bfloat16* tiles = reinterpret_cast<__nv_bfloat16*>(dsm);  // [2][K | V][kTileElems]
+  const int rows = nreal * grp;  // (query head, node) pairs, head-major
+  const int tiles = (rows + 15) / 16;
+  __nv_bfloat16* smt = reinterpret_cast<__nv_bfloat16*>(dsm);  // [2][K | V][kTileElems]
   auto stage = [&](int c, int buf) {
     const __nv_bfloat16* Kh = a.k + ((size_t)kh * a.cap + (size_t)c * kAttnChunk) * kAttnHeadDim;
     const __nv_bfloat16* Vh = a.v + ((size_t)kh * a.cap + (size_t)c * kAttnChunk) * kAttnHeadDim;
-    __nv_bfloat16* sK = tiles + (size_t)buf * 2 * kTileElems;
+    __nv_bfloat16* sK = smt + (size_t)buf * 2 * kTileElems;
     __nv_bfloat16* sV = sK + kTileElems;
 #pragma unroll
     for (int e = threadIdx.x; e < kAttnChunk * 16; e += kWarps * 32) {
@@ -300,23 +307,6 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
     cp_commit();
   };
   stage(c0, 0);
-  const int r0 = warp * 16;
-  const bool active = r0 < nreal;
-  const int ia = base + r0 + g, ib = ia + 8;
-  const bool va = active && r0 + g < nreal, vb = active && r0 + g + 8 < nreal;
-  uint32_t qa[8][4];
-  {
-    const __nv_bfloat16* qra = a.q + (size_t)ia * a.q_stride + h * kAttnHeadDim;
-    const __nv_bfloat16* qrb = a.q + (size_t)ib * a.q_stride + h * kAttnHeadDim;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      qa[kk][0] = va ? ld_b32(qra + 16 * kk + 2 * tig) : 0u;
-      qa[kk][1] = vb ? ld_b32(qrb + 16 * kk + 2 * tig) : 0u;
-      qa[kk][2] = va ? ld_b32(qra + 16 * kk + 8 + 2 * tig) : 0u;
-      qa[kk][3] = vb ? ld_b32(qrb + 16 * kk + 8 + 2 * tig) : 0u;
-    }
-  }
-  const int lim[2] = {va ? kAttnChunk : 0, vb ? kAttnChunk : 0};
   for (int c = c0; c < c1; ++c) {
     const int buf = (c - c0) & 1;
     if (c + 1 < c1) {
@@ -326,8 +316,23 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
       cp_wait_group<0>();
     }
     __syncthreads();
-    if (active) {
-      const __nv_bfloat16* sK = tiles + (size_t)buf * 2 * kTileElems;
+    const __nv_bfloat16* sK = smt + (size_t)buf * 2 * kTileElems;
+    for (int t = warp; t < tiles; t += kWarps) {
+      const int ra = 16 * t + g, rb = ra + 8;
+      const bool va = ra < rows, vb = rb < rows;
+      const int ia = base + (va ? ra % nreal : 0), ib = base + (vb ? rb % nreal : 0);
+      const int ha = kh * grp + (va ? ra / nreal : 0), hb = kh * grp + (vb ? rb / nreal : 0);
+      uint32_t qa[8][4];
+      const __nv_bfloat16* qra = a.q + (size_t)ia * a.q_stride + ha * kAttnHeadDim;
+      const __nv_bfloat16* qrb = a.q + (size_t)ib * a.q_stride + hb * kAttnHeadDim;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        qa[kk][0] = va ? ld_b32(qra + 16 * kk + 2 * tig) : 0u;
+        qa[kk][1] = vb ? ld_b32(qrb + 16 * kk + 2 * tig) : 0u;
+        qa[kk][2] = va ? ld_b32(qra + 16 * kk + 8 + 2 * tig) : 0u;
+        qa[kk][3] = vb ? ld_b32(qrb + 16 * kk + 8 + 2 * tig) : 0u;
+      }
+      const int lim[2] = {va ? kAttnChunk : 0, vb ? kAttnChunk : 0};
       float m[2], l[2], o[16][4];
       uint32_t pa[4][4];
       chunk_scores(qa, sK, lim, a.scale, m, l, pa, lane);
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         if (!(hh ? vb : va)) continue;
-        const size_t idx = part_idx(a, hh ? ib : ia, h, c);
+        const size_t idx = part_idx(a, hh ? ib : ia, hh ? hb : ha, c);
         float* po = a.po + idx * kAttnHeadDim;
 #pragma unroll
         for (int nd = 0; nd < 16; ++nd)
@@ -889,11 +894,129 @@ __global__ void __launch_bounds__(kWarps * 32, 3) attn_tail2_kernel(const __grid
   *reinterpret_cast<uint2*>(out) = u;
 }
 
+
+// ---------------------------------------------------------------------------
+// Per-node tail for GQA (H/KV >= 4, e.g. the 70B shape): one CTA per (node, KV
+// head) with one warp per query head of the group.  The node's chunk rows
+// (prefix tail, ancestors, self, zeros) are staged ONCE for the whole group;
+// each warp runs the node's row-0 MMAs with its own query — the same
+// fragments and order as the per-node kernel, hence the same bits.
+constexpr int kGqaWarps = 8;
+constexpr size_t kTailGqaSmem = (size_t)2 * kTileElems * 2 + (size_t)kGqaWarps * 128 * 4;
+
+__global__ void __launch_bounds__(kGqaWarps * 32, 2) attn_tail_gqa_kernel(const __grid_constant__ AttnGroup G) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int gi = member_of(G, blockIdx.x, 4);
+  const AttnArgs& a = G.m[gi].a;
+  const LevelDev& lv = G.m[gi].lv;
+  const int local = blockIdx.x - G.m[gi].cta_gqa;
+  const int kh = local % a.KV, i = local / a.KV;
+  const int grp = a.H / a.KV;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const bool active = warp < grp;
+  const int h = kh * grp + (active ? warp : 0);
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(dsm);
+  __nv_bfloat16* sV = sK + kTileElems;
+  float* xo = reinterpret_cast<float*>(sV + kTileElems) + warp * 128;
+  const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
+  const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
+  const int c_start = G.m[gi].c_shared;
+  const size_t pbase = part_idx(a, i, h, 0);
+  float pm_l = -INFINITY, pl_l = 0.f;
+  if (active && lane < c_start) {
+    pm_l = __ldcg(a.pm + pbase + lane);
+    pl_l = __ldcg(a.pl + pbase + lane);
+  }
+  const int A = lv.anc_cnt[i];
+  const int32_t* anc = lv.anc_rows + (size_t)i * lv.anc_stride;
+  const int P = lv.prefix_rows[i];
+  const int T = P + A + 1;
+  const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)i * a.KV + kh) * kAttnHeadDim
+                                       : Kh + (size_t)(lv.row0 + i) * kAttnHeadDim;
+  const __nv_bfloat16* vself = a.vself ? a.vself + ((size_t)i * a.KV + kh) * kAttnHeadDim
+                                       : Vh + (size_t)(lv.row0 + i) * kAttnHeadDim;
+  uint32_t q1[8][4];
+  const __nv_bfloat16* qr = a.q + (size_t)i * a.q_stride + h * kAttnHeadDim;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    q1[kk][0] = (active && g == 0) ? ld_b32(qr + 16 * kk + 2 * tig) : 0u;
+    q1[kk][1] = 0u;
+    q1[kk][2] = (active && g == 0) ? ld_b32(qr + 16 * kk + 8 + 2 * tig) : 0u;
+    q1[kk][3] = 0u;
+  }
+  float M = -INFINITY, L = 0.f;
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (active) {
+    const float* po = a.po + pbase * kAttnHeadDim + 4 * lane;
+    float4 nxt = c_start > 0 ? __ldcg(reinterpret_cast<const float4*>(po)) : O;
+    for (int c = 0; c < c_start; ++c) {
+      if (c > 0 && (c & 31) == 0) {
+        pm_l = c + lane < c_start ? __ldcg(a.pm + pbase + c + lane) : -INFINITY;
+        pl_l = c + lane < c_start ? __ldcg(a.pl + pbase + c + lane) : 0.f;
+      }
+      const float4 cur = nxt;
+      if (c + 1 < c_start) nxt = __ldcg(reinterpret_cast<const float4*>(po + (size_t)(c + 1) * kAttnHeadDim));
+      float sa, sb;
+      merge_scale(M, L, __shfl_sync(0xffffffffu, pm_l, c & 31), __shfl_sync(0xffffffffu, pl_l, c & 31), sa, sb);
+      O.x = merge_val(O.x, cur.x, sa, sb);
+      O.y = merge_val(O.y, cur.y, sa, sb);
+      O.z = merge_val(O.z, cur.z, sa, sb);
+      O.w = merge_val(O.w, cur.w, sa, sb);
+    }
+  }
+  const int c_end = (T + kAttnChunk - 1) / kAttnChunk;
+  for (int c = c_start; c < c_end; ++c) {
+    const int j0 = c * kAttnChunk;
+    __syncthreads();  // every warp is done with the previous chunk's rows
+    for (int e = threadIdx.x; e < kAttnChunk * 16; e += kGqaWarps * 32) {
+      const int row = e >> 4, part = e & 15, j = j0 + row;
+      const __nv_bfloat16* ks = j < P ? Kh + (size_t)j * kAttnHeadDim
+                                      : (j < P + A ? Kh + (size_t)anc[j - P] * kAttnHeadDim : kself);
+      const __nv_bfloat16* vs = j < P ? Vh + (size_t)j * kAttnHeadDim
+                                      : (j < P + A ? Vh + (size_t)anc[j - P] * kAttnHeadDim : vself);
+      const int nb = j < T ? 16 : 0;
+      cp16(sK + row * kPad + part * 8, (nb ? ks : Kh) + part * 8, nb);
+      cp16(sV + row * kPad + part * 8, (nb ? vs : Vh) + part * 8, nb);
+    }
+    cp_wait_all();
+    __syncthreads();
+    if (!active) continue;
+    const int lim[2] = {g == 0 ? min(T - j0, kAttnChunk) : 0, 0};
+    float m[2], l[2], o[16][4];
+    uint32_t pa[4][4];
+    chunk_scores(q1, sK, lim, a.scale, m, l, pa, lane);
+    chunk_pv(pa, sV, o, lane);
+    if (g == 0) {
+#pragma unroll
+      for (int nd = 0; nd < 16; ++nd)
+        *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
+    }
+    __syncwarp();
+    const float4 oc = *reinterpret_cast<const float4*>(xo + 4 * lane);
+    __syncwarp();
+    float sa, sb;
+    merge_scale(M, L, __shfl_sync(0xffffffffu, m[0], 0), __shfl_sync(0xffffffffu, l[0], 0), sa, sb);
+    O.x = merge_val(O.x, oc.x, sa, sb);
+    O.y = merge_val(O.y, oc.y, sa, sb);
+    O.z = merge_val(O.z, oc.z, sa, sb);
+    O.w = merge_val(O.w, oc.w, sa, sb);
+  }
+  if (!active) return;
+  __nv_bfloat16* out = a.out + (size_t)i * a.out_stride + h * kAttnHeadDim + 4 * lane;
+  uint2 u;
+  u.x = pack_f32(__fdiv_rn(O.x, L), __fdiv_rn(O.y, L));
+  u.y = pack_f32(__fdiv_rn(O.z, L), __fdiv_rn(O.w, L));
+  *reinterpret_cast<uint2*>(out) = u;
+}
+
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
   TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 64]");
   AttnGroup G;
   G.count = count;
-  int cs = 0, ct = 0, cg = 0, c2 = 0;
+  int cs = 0, ct = 0, cg = 0, c2 = 0, cq = 0;
   for (int g = 0; g < count; ++g) {
     AttnMember& m = G.m[g];
     m.a = a[g];
@@ -909,11 +1032,16 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     m.cta_tail = ct;
     m.cta_tile = cg;
     m.cta_tail2 = c2;
-    cs += a[g].H * ((m.c_shared + g_shared_run - 1) / g_shared_run) * m.zt;
+    m.cta_gqa = cq;
+    const int grp = a[g].H / a[g].KV;
+    const bool gqa = !tiled && !tail2 && grp >= 4 && grp <= kGqaWarps;
+    cs += a[g].KV * ((m.c_shared + g_shared_run - 1) / g_shared_run) * m.zt;
     if (tiled)
       cg += a[g].H * m.zt;
     else if (tail2)
       c2 += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
+    else if (gqa)
+      cq += a[g].KV * lv[g].n;
     else
       ct += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
   }
@@ -929,6 +1057,8 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     TP_CUDA(cudaFuncSetAttribute(attn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
     TP_CUDA(cudaFuncSetAttribute(attn_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSharedSmem));
     TP_CUDA(cudaFuncSetAttribute(attn_tail2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTail2Smem));
+    TP_CUDA(cudaFuncSetAttribute(attn_tail_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTailGqaSmem));
     attr_set[dev & 63] = true;
   }
   if (cs > 0) {
@@ -943,6 +1073,12 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     TP_CUDA(launch_pdl(attn_tile_kernel, dim3(cg), dim3(kWarps * 32), kTileSmem, st, G));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tile", st);
+  }
+  if (cq > 0) {
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(attn_tail_gqa_kernel, dim3(cq), dim3(kGqaWarps * 32), kTailGqaSmem, st, G));
+    TP_CUDA(cudaGetLastError());
+    timeline_mark("attn_tail_gqa", st);
   }
   if (c2 > 0) {
     ::tp::count_launch();

@@ -38,6 +38,7 @@ struct AttnMember {
   int cta_tail;    // first CTA of this member in the per-node tail launch (empty range if tiled)
   int cta_tile;    // first CTA of this member in the 16-node tile launch (empty range if per-node)
   int cta_tail2;   // first CTA of this member in the shared-prefix tail launch (uniform levels)
+  int cta_gqa;     // first CTA of this member in the GQA tail launch (one CTA per node and KV head)
 };
 
 struct AttnGroup {

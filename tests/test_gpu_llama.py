@@ -338,3 +338,37 @@ def test_kv_capacity_growth_mid_decode_lossless():
         r.decode_step()
     assert r.emitted[:24] == want
     assert any(s.kv._cap > c for s, c in zip(r.stages, caps0))  # and again while decoding
+
+
+def test_gqa_attention_paths():
+    """GQA (8 query heads over 2 KV heads): the group-staged shared-chunk and
+    tail kernels keep batch invariance (siblings together == alone, bitwise),
+    agree with the float32 oracle, and SpecPipe stays lossless."""
+    shape = dict(vocab=512, hidden=256, layers=2, heads=8, kv_heads=2, ffn=512)
+    cfg = LlamaConfig(**shape)
+    m = LlamaModel(cfg, max_nodes=64)
+    o = LlamaOracle(**shape)
+    rng = np.random.default_rng(31)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, 150)]
+
+    def fresh():
+        c = KvCache(cfg.layers, cfg.hidden, capacity=256)
+        tp.model.prefill_rows(m, c, prompt)
+        return c
+
+    P = len(prompt)
+    nodes = [(10 + i, int(rng.integers(cfg.vocab)), P, frozenset({10 + i})) for i in range(9)]
+    together = forward_tree(m, fresh(), nodes).cpu()
+    for i, nd in enumerate(nodes[:4]):
+        assert torch.equal(forward_tree(m, fresh(), [nd]).cpu()[0], together[i]), i
+    okv = o.new_kv()
+    x = None
+    for pos, tok in enumerate(prompt + [nodes[0][1]]):
+        x = o.run_position(o.embed(tok, pos), okv, list(range(len(okv))), pos=pos, prefix=True)
+    assert float(np.abs(together[0].numpy() - x).max()) <= TOL * max(1.0, float(np.abs(x).max()))
+    want = tp.sequential_decode(m, prompt[:30], 16)
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.7, rank_decay=0.5, miss_prob=0.05, seed=3),
+                              cfg.vocab)
+    res = tp.run(m, tp.PipelineConfig(num_stages=2), tp.BeamConfig(w=8, k=4), draft, prompt[:30], 16,
+                 collect_trace=False)
+    assert res.tokens == want

@@ -68,6 +68,14 @@ typedef struct tp_level {
   int32_t bits_base;          /* cache row addressed by bit 0                 */
   const uint64_t* anc_bits;   /* host [n*words], self bit excluded           */
   int32_t layer_lo, layer_hi; /* sub-range of the stage's layers (0,0 = all)  */
+  /* Tree form (optional; prefix_rows / anc_bits may then be NULL): node i is
+   * tree node tree_lo + i; it attends rows [0, tree_prefix) and, for every
+   * ancestor t >= tree_off in its packed ancestor-or-self tree row
+   * tree_bits[(tree_lo+i)*words ...] (self excluded), row tree_prefix - tree_off + t.
+   * This is invariant I1/I2 of the reference cache evaluated here
+   * instead of in Python for every stage and request.                          */
+  const uint64_t* tree_bits;
+  int32_t tree_lo, tree_off, tree_prefix;
 } tp_level;
 
 const char* tp_last_error(void);

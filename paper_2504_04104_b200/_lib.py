@@ -44,6 +44,7 @@ class Level(C.Structure):
         ("n", C.c_int32), ("append", C.c_int32), ("tokens", C.c_void_p), ("positions", C.c_void_p),
         ("prefix_rows", C.c_void_p), ("words", C.c_int32), ("bits_base", C.c_int32),
         ("anc_bits", C.c_void_p), ("layer_lo", C.c_int32), ("layer_hi", C.c_int32),
+        ("tree_bits", C.c_void_p), ("tree_lo", C.c_int32), ("tree_off", C.c_int32), ("tree_prefix", C.c_int32),
     ]
 
 

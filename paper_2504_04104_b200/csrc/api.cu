@@ -513,6 +513,38 @@ int tp_stage_reserve(tp_stage* s, int32_t capacity_rows) {
 
 // Validate one level against its stage, upload its metadata (one pinned-host ->
 // device copy) and describe it for the kernels.
+// Tree-form levels: derive prefix_rows / anc_bits from the tree's packed rows
+// (self bit cleared, promoted ancestors below tree_off masked) into `store`.
+struct LevelStore {
+  std::vector<int32_t> pre;
+  std::vector<uint64_t> bits;
+};
+static const tp_level* materialize(const tp_level* L, tp_level* tmp, LevelStore* store) {
+  if (!L->tree_bits) return L;
+  *tmp = *L;
+  const int n = L->n, W = L->words;
+  store->pre.assign(n, L->tree_prefix);
+  store->bits.assign((size_t)n * W, 0ull);
+  for (int i = 0; i < n; ++i) {
+    const int node = L->tree_lo + i;
+    const uint64_t* src = L->tree_bits + (size_t)node * W;
+    uint64_t* dst = store->bits.data() + (size_t)i * W;
+    for (int w = 0; w < W; ++w) {
+      uint64_t v = src[w];
+      if (w == (node >> 6)) v &= ~(1ull << (node & 63));  // self
+      const int lo_bit = L->tree_off - 64 * w;            // tree nodes below tree_off live in the prefix
+      if (lo_bit >= 64) v = 0;
+      else if (lo_bit > 0) v &= ~((1ull << lo_bit) - 1ull);
+      dst[w] = v;
+    }
+  }
+  tmp->prefix_rows = store->pre.data();
+  tmp->anc_bits = W ? store->bits.data() : nullptr;
+  tmp->bits_base = L->tree_prefix - L->tree_off;
+  tmp->tree_bits = nullptr;
+  return tmp;
+}
+
 // Validate one level against its stage and describe it for the kernels; the
 // metadata blob (tokens | positions | prefix | anc bits | anc counts | anc rows)
 // is laid out by level_write into caller-provided staging memory.
@@ -683,6 +715,9 @@ int tp_stage_forward(tp_stage* s, const tp_level* L, const void* hidden_in, void
   tp_model* m = s->m;
   TP_CUDA(cudaSetDevice(m->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
+  tp_level tmp;
+  LevelStore store;
+  L = materialize(L, &tmp, &store);
   LevelDev lv;
   TP_TRY(prepare_level(s, L, hidden_in, hidden_out, st, &lv));
   int rc = is_toy(m) ? toy_forward(s, lv, hidden_in, hidden_out, st) : llama_forward(s, lv, hidden_in, hidden_out, st);
@@ -718,17 +753,21 @@ int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_
   timeline_mark("host_gap", st);  // GPU time since the previous mark: idle or other work
   std::vector<LevelDev> lv(n_items);
   std::vector<size_t> off(n_items + 1, 0);
+  std::vector<tp_level> tmp(n_items);
+  std::vector<LevelStore> store(n_items);
+  std::vector<const tp_level*> lvl(n_items);
   for (int i = 0; i < n_items; ++i) {
+    lvl[i] = materialize(&items[i].level, &tmp[i], &store[i]);
     size_t b;
-    TP_TRY(level_validate(items[i].stage, &items[i].level, items[i].hidden_in, member_hidden_out[items[i].member],
-                          &lv[i], &b));
+    TP_TRY(level_validate(items[i].stage, lvl[i], items[i].hidden_in, member_hidden_out[items[i].member], &lv[i],
+                          &b));
     off[i + 1] = off[i] + b;
   }
   {  // every item's metadata in one upload
     char *h, *dm;
     int slot;
     TP_TRY(call_slot(m0, off[n_items], &h, &dm, &slot));
-    for (int i = 0; i < n_items; ++i) level_write(&items[i].level, &lv[i], h + off[i], dm + off[i]);
+    for (int i = 0; i < n_items; ++i) level_write(lvl[i], &lv[i], h + off[i], dm + off[i]);
     TP_TRY(call_push(m0, slot, off[n_items], st));
   }
   if (is_toy(m0)) {

@@ -195,19 +195,26 @@ def cpu_step_estimate(cfg, node_layers_per_step, head_per_token, prompt_len, sam
 
 def run_reference(args):
     cfg = model_cfg(args.model)
-    # node-layers per step measured on the GPU run of this config (mean over the
-    # timed window; probe in SURVEY §8: sum of mean resident nodes ~169 at m=8,w=64)
+    # node-layers per step and steps per token of this workload as measured on the
+    # GPU arm (same synthetic draft, same tree process): 650 node-layers/step and
+    # 2.0 steps/token at 7B / 8 stages / w=64 (SURVEY §8 probe: ~169 resident nodes
+    # per step summed over stages); override with TP_NODE_LAYERS_PER_STEP /
+    # TP_STEPS_PER_TOKEN for other configs
     nl = float(os.environ.get("TP_NODE_LAYERS_PER_STEP", 169.3 * cfg.layers / args.stages))
+    spt = float(os.environ.get("TP_STEPS_PER_TOKEN", 2.0))
     cores = os.cpu_count()
     samples = []
     for _ in range(max(1, min(args.steps, 3))):
         ms, info = cpu_step_estimate(cfg, nl, 1.0, args.prompt_len)
         samples.append(ms)
-    value = float(np.median(samples))
+    step_ms = float(np.median(samples))
+    value = step_ms * spt
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]},
+            "steps_per_token": spt,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": info["sample"] + f"; x {spt} steps/token"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

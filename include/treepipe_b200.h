@@ -150,6 +150,10 @@ typedef struct tp_item {
   int32_t member;
 } tp_item;
 int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_hidden_out, void* stream);
+/* The same with the model's scratch workspaces taken from slot ws_base on: two
+ * calls with disjoint slot ranges may run concurrently on two streams.        */
+int tp_items_forward_ws(int32_t n_items, const tp_item* items, void* const* member_hidden_out, int32_t ws_base,
+                        void* stream);
 /* Pruning propagation (KvCache.promote/prune/_restrict/drop_speculative,
  * model.py:169-194): rows < first_row stay; of rows [first_row, first_row+count)
  * those with keep bit set are compacted stably to follow them; the rest and

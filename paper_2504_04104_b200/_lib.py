@@ -76,6 +76,7 @@ _SIGS = {
     "tp_stage_forward": (C.c_int, [_P, C.POINTER(Level), _P, _P, _P]),
     "tp_stages_forward": (C.c_int, [_I, _P, _P, _P, _P, _P]),
     "tp_items_forward": (C.c_int, [_I, _P, _P, _P]),
+    "tp_items_forward_ws": (C.c_int, [_I, _P, _P, _I, _P]),
     "tp_model_greedy_rows_async": (C.c_int, [_P, _P, _I, _P, _P]),
     "tp_model_greedy_rows_wait": (C.c_int, [_P, _I, _P]),
     "tp_stage_compact": (C.c_int, [_P, _I, _I, _P, _P]),

@@ -735,6 +735,12 @@ int tp_stages_forward(int32_t count, tp_stage* const* stages, const tp_level* le
 }
 
 int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_hidden_out, void* stream) {
+  return tp_items_forward_ws(n_items, items, member_hidden_out, 0, stream);
+}
+
+int tp_items_forward_ws(int32_t n_items, const tp_item* items, void* const* member_hidden_out, int32_t ws_base,
+                        void* stream) {
+  TP_CHECK(ws_base >= 0 && ws_base <= 64, TP_ECONFIG, "workspace base outside [0, 64]");
   TP_CHECK(n_items >= 1 && items && member_hidden_out, TP_ECONFIG, "null argument");
   tp_model* m0 = items[0].stage ? items[0].stage->m : nullptr;
   TP_CHECK(m0, TP_ECONFIG, "null stage");
@@ -782,7 +788,7 @@ int tp_items_forward(int32_t n_items, const tp_item* items, void* const* member_
     for (int g = 0; g < n_members; ++g)
       mem[g] = FwdMember{per[g].data(), (int)per[g].size(), (float*)member_hidden_out[g]};
     for (int g0 = 0; g0 < n_members; g0 += kMaxGroup)
-      TP_TRY(llama_forward_members(mem.data() + g0, std::min(kMaxGroup, n_members - g0), st));
+      TP_TRY(llama_forward_members(mem.data() + g0, std::min(kMaxGroup, n_members - g0), st, ws_base));
   }
   for (int i = 0; i < n_items; ++i)
     if (items[i].level.append) items[i].stage->rows += items[i].level.n;

@@ -112,7 +112,8 @@ struct FwdMember {
   int count;
   float* x;  // [sum n, hidden] residual stream of the member
 };
-int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st);
+// ws_base: first model workspace slot used (concurrent calls on two streams use disjoint slots)
+int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int ws_base = 0);
 int llama_greedy_rows_async(tp_model* m, int n, const float* x, float* logits, cudaStream_t st);
 int llama_greedy_rows_wait(tp_model* m, int n, int32_t* out);
 void timeline_mark(const char* tag, cudaStream_t st);  // no-op unless enabled

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __gri
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
   FwdItem it{s, lv, hidden_in};
   FwdMember mb{&it, 1, (float*)hidden_out};
-  return llama_forward_members(&mb, 1, st);
+  return llama_forward_members(&mb, 1, st, 0);
 }
 
 // Members of a grouped forward run layer slot by layer slot: slot j runs layer
@@ -424,7 +424,7 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
 // one request each (SpecPipe-DB) — that share the member's layers: their node
 // rows are concatenated for the GEMMs (weights streamed once for all requests),
 // K/V rows are scattered to each request's cache, and attention runs per item.
-int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
+int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int ws_base) {
   TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "member group size outside [1, 8]");
   tp_model* m0 = mem[0].items[0].s->m;
   TP_TRY(build_model_ext(m0));
@@ -460,7 +460,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st) {
     }
     TP_CHECK(n <= c.max_nodes, TP_ESHAPE, "ragged member exceeds max_nodes");
     ntot[g] = n;
-    TP_TRY(ws_get(m0, g, chunks_for_cap(cap_max), &ws[g]));
+    TP_TRY(ws_get(m0, ws_base + g, chunks_for_cap(cap_max), &ws[g]));
     for (int r = 0; r < M.count; ++r) {
       const FwdItem& it = M.items[r];
       float* x = M.x + (size_t)offs[g][r] * d;

@@ -11,9 +11,12 @@
 //   * stream-K: the m-tile x k-block space is cut into one contiguous range
 //     per CTA (grid = #SMs), so every SM streams the same weight bytes;
 //   * warp-specialised: warp 0 = TMA producer (weights evict-first, node rows
-//     evict-last), warp 1 = single-thread MMA issuer, warps 2-5 = epilogue
-//     (double-buffered TMEM accumulators: the next segment's MMAs overlap the
-//     previous segment's epilogue);
+//     evict-last), warp 1 = single-thread MMA issuer, warps 2-5 = TMEM drain
+//     (up to 4 TMEM accumulator buffers: the next segments' MMAs overlap the
+//     previous segment's drain), warps 6-13 = stream-K reducers fed by a
+//     shared-memory queue, so a fix-up waiting on other CTAs never stalls the
+//     drain (measured: the o-projection lost 16 us of 55 to fix-ups on the
+//     drain warps);
 //   * programmatic dependent launch: barrier init, TMEM allocation and the
 //     first ring-full of *weight* tiles are issued before griddepcontrol.wait,
 //     i.e. while the previous kernel is still finishing;
@@ -46,8 +49,14 @@ using namespace sm100;
 constexpr int kBM = 128, kBK = 64;
 constexpr int kMaxStages = 16;
 constexpr int kMaxTmemBufs = 4;  // accumulator buffers: the MMA may run this many segments ahead
-constexpr int kEpiWarps = 8;  // two per TMEM lane quarter: the stream-K fix-up is epilogue-throughput bound
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kDrainWarps = 4;  // one per TMEM lane quarter: drain accumulators, publish partials, sole-owner epilogue
+constexpr int kRedWarps = 8;    // stream-K fix-up reducers, fed through a shared-memory queue
+constexpr int kThreads = 64 + 32 * (kDrainWarps + kRedWarps);
+constexpr int kRedSlots = kMaxGroup + 1;  // <= one reduction per member per CTA, plus the end sentinel
+constexpr int kBarBytes = 1024;           // mbarriers, TMEM holder, reduction queue
+struct RedItem {
+  int g, mt, cnt, cfirst, clast;
+};
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kXchNodes = 32;           // epilogue exchange tile: 32 nodes x 128 features
 constexpr int kXchLd = 132;
@@ -109,19 +118,20 @@ SkPlan sk_plan(int n_out, int k, int n) {
 // Tuning knobs (tp_debug_gemm_knob): ring depth cap and smem budget.
 static int g_knob_max_stages = 8;
 static int g_knob_smem_kb = 200;
-static int g_knob_fixup = 0;  // diagnostics only: 1 skips the reduction, 2 also the partial publish (WRONG results)
+static int g_knob_fixup = 0;  // diagnostics only: 1 skips the reduction, 2 also the partial publish, 3 reduces without waiting for arrivals (WRONG results)
 
 static int stages_for(int n_pad) {
   const int per = kABytes + n_pad * 128;
-  return std::min(std::min(kMaxStages, g_knob_max_stages), (g_knob_smem_kb * 1024 - kXchBytes - 1024 - 512) / per);
+  return std::min(std::min(kMaxStages, g_knob_max_stages), (g_knob_smem_kb * 1024 - kXchBytes - 1024 - kBarBytes) / per);
 }
 
 static size_t smem_for(int n_pad) {
-  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + 512 /*barriers*/;  // 2*16 + 2*4 mbarriers + holder
+  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + kBarBytes;
 }
 
 // ---- device --------------------------------------------------------------------
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+__device__ __forceinline__ void drain_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kDrainWarps) : "memory"); }
+__device__ __forceinline__ void red_bar() { asm volatile("bar.sync 2, %0;" ::"n"(32 * kRedWarps) : "memory"); }
 
 // ---- epilogue: one warp per node row, lane l owns features 4l..4l+3 of the m-tile.
 // RoPE pairs feature r with r^64 and SwiGLU gate r with up r+64: both are lane^16.
@@ -232,15 +242,16 @@ __device__ __forceinline__ float4 sum_partials(const float* base, size_t slot, i
   return acc;
 }
 
-// Reduce + apply nodes [lo, hi) of m-tile mt from the global partials; the 4
-// epilogue warps take nodes round-robin, two per warp in flight.
+// Reduce + apply nodes [lo, hi) of m-tile mt from the global partials; the NW
+// reducer warps take nodes round-robin, two per warp in flight.
+template <int NW>
 __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int n, int mt, int cnt, int lo,
                                              int hi, int ew, int lane) {
   const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
   const size_t slot = (size_t)n * kBM;
   const int f = lane * 4;
-  for (int c = lo + ew; c < hi; c += 2 * kEpiWarps) {
-    const int c2 = c + kEpiWarps;
+  for (int c = lo + ew; c < hi; c += 2 * NW) {
+    const int c2 = c + NW;
     const bool two = c2 < hi;
     EpiAux x0{}, x1{};  // operands of the op first: their loads overlap the partial loads
     epi_aux(e, mt, f, c, x0);
@@ -253,11 +264,12 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
 }
 
 // Apply nodes c0 .. c0+cn-1 staged in xch[node][feature] (sole-contributor path).
+template <int NW>
 __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int cn, const float* xch, int ew,
                                            int lane) {
   const int f = lane * 4;
-  for (int cc = ew; cc < cn; cc += 2 * kEpiWarps) {
-    const int cc2 = cc + kEpiWarps;
+  for (int cc = ew; cc < cn; cc += 2 * NW) {
+    const int cc2 = cc + NW;
     const bool two = cc2 < cn;
     const float4 y0 = *reinterpret_cast<const float4*>(xch + cc * kXchLd + f);
     const float4 y1 = two ? *reinterpret_cast<const float4*>(xch + cc2 * kXchLd + f) : y0;
@@ -292,7 +304,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kMaxStages;
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + kMaxTmemBufs;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + kMaxTmemBufs);
+  uint64_t* rfull = tempty + kMaxTmemBufs;
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(rfull + kRedSlots);
+  RedItem* rq = reinterpret_cast<RedItem*>(tholder + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ncols = 32;
   while (ncols < (uint32_t)(nbuf * grp.max_npad)) ncols <<= 1;
@@ -304,8 +318,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < nbuf; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], kEpiWarps);
+      mbar_init(&tempty[b], kDrainWarps);
     }
+    for (int q = 0; q < kRedSlots; ++q) mbar_init(&rfull[q], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tholder, ncols);
@@ -391,37 +406,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 2 + kDrainWarps) {
+    // Drain warps: TMEM -> partial (or, for a sole-owner tile, straight through
+    // the epilogue op), then free the accumulator buffer.  They never wait for
+    // other CTAs: a tile this CTA must reduce is queued for the reducer warps,
+    // so the MMA keeps streaming while the fix-up waits on its arrivals.
     const int quarter = warp & 3;  // TMEM lanes this warp may touch
     const int r = quarter * 32 + lane;
-    const int ew = warp - 2;  // epilogue warp 0..kEpiWarps-1 (node-parallel phases)
-    const int chalf = ew >> 2;  // the two warps on a TMEM lane quarter split its 16-column groups
+    const int ew = warp - 2;
     const int et = threadIdx.x - 64;
-    // A reduction is deferred by one segment: the next segment's partial (often
-    // the first segment of the next member, which a neighbouring CTA's reducer
-    // waits for) is published before this CTA blocks on its own tile's
-    // arrivals.  Without the deferral the waits chain CTA c -> c+1 -> c+2 ...
-    // one link per member and the chain surfaces at the end of the launch.
-    int pend_g = -1, pend_mt = 0, pend_cnt = 0, pend_cfirst = 0, pend_clast = 0;
-    auto run_pending = [&]() {
-      if (pend_g < 0) return;
-      const GemmEpi& e = grp.m[pend_g].e;
-      const int n = grp.m[pend_g].n;
-      const int* arrive = e.counters;
-      const int mt = pend_mt, cnt = pend_cnt, cfirst = pend_cfirst, clast = pend_clast;
-      const int cend = sk_begin(p, clast + 1) <= (mt + 1) * p.KB ? clast : clast - 1;
-      const int E = cend - cfirst + 1, rank = c - cfirst;
-      if (et == 0) {  // counters only grow: this launch's arrivals are complete at (epoch+1)*cnt
-        const int target = (e.epoch + 1) * cnt;
-        while (ld_acquire(&arrive[mt]) < target) __nanosleep(32);
-        __threadfence();
-      }
-      epi_bar();
-      reduce_apply(e, p, n, mt, cnt, n * rank / E, n * (rank + 1) / E, ew, lane);
-      epi_bar();
-      pend_g = -1;
-    };
-    int seg = 0;
+    int seg = 0, nq = 0;
     for (int g = 0; g < grp.count; ++g) {
       const GemmEpi& e = grp.m[g].e;
       const int n = grp.m[g].n, npad = grp.m[g].n_pad;
@@ -441,25 +435,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cnt == 1) {
           for (int c0 = 0; c0 < n; c0 += kXchNodes) {
             const int cn = min(kXchNodes, n - c0);
-            for (int col0 = c0 + 16 * chalf; col0 < min(c0 + kXchNodes, npad); col0 += 32) {
+            for (int col0 = c0; col0 < min(c0 + kXchNodes, npad); col0 += 16) {
               float v[16];
               tmem_ld_x16(tbase + col0, v);
 #pragma unroll
               for (int i = 0; i < 16; ++i)
                 if (col0 + i < n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
             }
-            epi_bar();
-            smem_apply(e, mt, c0, cn, xch, ew, lane);
-            epi_bar();
+            drain_bar();
+            smem_apply<kDrainWarps>(e, mt, c0, cn, xch, ew, lane);
+            drain_bar();
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
-          run_pending();
         } else {
-          // stream-K fix-up: publish this CTA's fp32 partial of the m-tile ...
+          // stream-K fix-up: publish this CTA's fp32 partial of the m-tile
           float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * n) * kBM + r;
-          for (int col0 = 16 * chalf; col0 < (fixup_mode == 2 ? 0 : npad); col0 += 32) {
+          for (int col0 = 0; col0 < (fixup_mode == 2 ? 0 : npad); col0 += 16) {
             float v[16];
             tmem_ld_x16(tbase + col0, v);
 #pragma unroll
@@ -469,32 +462,51 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
-          epi_bar();
-          if (et == 0) {  // barrier + one gpu-scope fence publishes every epilogue thread's stores
+          drain_bar();
+          if (et == 0) {  // barrier + one gpu-scope fence publishes every drain thread's stores
             __threadfence();
             atomicAdd(&arrive[mt], 1);
-          }
-          run_pending();  // the previous segment's reduction, now that this partial is out
-          // ... and, if this segment ends the CTA's range of this member, reduce a
-          // slice of the tile's nodes once every partial is in (deferred, above).
-          // The contributors whose ranges end inside the tile finish together;
-          // splitting the nodes among them keeps the fix-up short (one CTA
-          // reducing a whole tile was measured 2x slower on the o / down
-          // projections).  Waits only ever point at an earlier (member,
-          // position) or at a partial published before any wait: no cycle.
-          if (fixup_mode == 0 && t1 <= (mt + 1) * p.KB) {
-            pend_g = g;
-            pend_mt = mt;
-            pend_cnt = cnt;
-            pend_cfirst = cfirst;
-            pend_clast = clast;
+            // the contributors whose ranges end inside the tile reduce it, each a
+            // slice of the nodes (they finish together; one CTA reducing a whole
+            // tile was measured 2x slower on the o / down projections)
+            if ((fixup_mode == 0 || fixup_mode == 3) && t1 <= (mt + 1) * p.KB) {
+              rq[nq] = RedItem{g, mt, cnt, cfirst, clast};
+              mbar_arrive(&rfull[nq]);
+              ++nq;
+            }
           }
         }
         t = seg_end;
         ++seg;
       }
     }
-    run_pending();
+    if (et == 0) {
+      rq[nq].g = -1;
+      mbar_arrive(&rfull[nq]);
+    }
+  } else {
+    // Reducer warps: for each queued tile, wait for all of its partials, then
+    // sum this CTA's node slice in contributor order and apply the epilogue op.
+    // A wait only ever points at partials that drain warps publish without
+    // waiting on anything but their own MMA: no cycle.
+    const int rw = warp - 2 - kDrainWarps;
+    const int rt = threadIdx.x - 64 - 32 * kDrainWarps;
+    for (int q = 0;; ++q) {
+      mbar_wait(&rfull[q], 0);
+      const RedItem it = rq[q];
+      if (it.g < 0) break;
+      const GemmEpi& e = grp.m[it.g].e;
+      const int n = grp.m[it.g].n;
+      const int cend = sk_begin(p, it.clast + 1) <= (it.mt + 1) * p.KB ? it.clast : it.clast - 1;
+      const int E = cend - it.cfirst + 1, rank = c - it.cfirst;
+      if (rt == 0 && fixup_mode != 3) {  // counters only grow: this launch's arrivals are complete at (epoch+1)*cnt
+        const int target = (e.epoch + 1) * it.cnt;
+        while (ld_acquire(&e.counters[it.mt]) < target) __nanosleep(32);
+        __threadfence();
+      }
+      red_bar();
+      reduce_apply<kRedWarps>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane);
+    }
   }
   __syncthreads();
   if (warp == 1) {

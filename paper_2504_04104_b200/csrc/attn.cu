@@ -387,13 +387,42 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
   }
   const int A = lv.anc_cnt[i];
   const int32_t* anc = lv.anc_rows + (size_t)i * lv.anc_stride;  // decoded on the host, row order
+  const int anc_l = lane < A ? __ldg(anc + lane) : 0;  // first 32 ancestors in lane registers
   const int P = lv.prefix_rows[i];
   const int T = P + A + 1;
   const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)i * a.KV + kh) * kAttnHeadDim
                                        : Kh + (size_t)(lv.row0 + i) * kAttnHeadDim;
   const __nv_bfloat16* vself = a.vself ? a.vself + ((size_t)i * a.KV + kh) * kAttnHeadDim
                                        : Vh + (size_t)(lv.row0 + i) * kAttnHeadDim;
-  uint32_t q1[8][4];
+  // running state, lane layout: dims 4*lane .. 4*lane+3
+  float M = -INFINITY, L = 0.f;
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  {  // shared chunks' partials, 8 chunk rows in flight per batch (one L2 round trip per batch)
+    constexpr int kPre = 8;
+    const float4* po = reinterpret_cast<const float4*>(a.po + pbase * kAttnHeadDim) + lane;
+    for (int c0 = 0; c0 < c_start; c0 += kPre) {
+      if (c0 > 0 && (c0 & 31) == 0) {  // next block of 32 chunk scalars
+        pm_l = c0 + lane < c_start ? __ldcg(a.pm + pbase + c0 + lane) : -INFINITY;
+        pl_l = c0 + lane < c_start ? __ldcg(a.pl + pbase + c0 + lane) : 0.f;
+      }
+      float4 blk[kPre];
+#pragma unroll
+      for (int j = 0; j < kPre; ++j)
+        blk[j] = c0 + j < c_start ? __ldcg(po + (size_t)(c0 + j) * (kAttnHeadDim / 4)) : O;
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) {
+        const int c = c0 + j;
+        if (c >= c_start) break;
+        float sa, sb;
+        merge_scale(M, L, __shfl_sync(0xffffffffu, pm_l, c & 31), __shfl_sync(0xffffffffu, pl_l, c & 31), sa, sb);
+        O.x = merge_val(O.x, blk[j].x, sa, sb);
+        O.y = merge_val(O.y, blk[j].y, sa, sb);
+        O.z = merge_val(O.z, blk[j].z, sa, sb);
+        O.w = merge_val(O.w, blk[j].w, sa, sb);
+      }
+    }
+  }
+  uint32_t q1[8][4];  // loaded after the merge: in flight during the first K staging
   const __nv_bfloat16* qr = a.q + (size_t)i * a.q_stride + h * kAttnHeadDim;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
@@ -401,27 +430,6 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
     q1[kk][1] = 0u;
     q1[kk][2] = g == 0 ? ld_b32(qr + 16 * kk + 8 + 2 * tig) : 0u;
     q1[kk][3] = 0u;
-  }
-  // running state, lane layout: dims 4*lane .. 4*lane+3
-  float M = -INFINITY, L = 0.f;
-  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-  {
-    const float* po = a.po + pbase * kAttnHeadDim + 4 * lane;
-    float4 nxt = c_start > 0 ? __ldcg(reinterpret_cast<const float4*>(po)) : O;
-    for (int c = 0; c < c_start; ++c) {
-      if (c > 0 && (c & 31) == 0) {  // next block of 32 chunk scalars
-        pm_l = c + lane < c_start ? __ldcg(a.pm + pbase + c + lane) : -INFINITY;
-        pl_l = c + lane < c_start ? __ldcg(a.pl + pbase + c + lane) : 0.f;
-      }
-      const float4 cur = nxt;
-      if (c + 1 < c_start) nxt = __ldcg(reinterpret_cast<const float4*>(po + (size_t)(c + 1) * kAttnHeadDim));
-      float sa, sb;
-      merge_scale(M, L, __shfl_sync(0xffffffffu, pm_l, c & 31), __shfl_sync(0xffffffffu, pl_l, c & 31), sa, sb);
-      O.x = merge_val(O.x, cur.x, sa, sb);
-      O.y = merge_val(O.y, cur.y, sa, sb);
-      O.z = merge_val(O.z, cur.z, sa, sb);
-      O.w = merge_val(O.w, cur.w, sa, sb);
-    }
   }
   const int c_end = (T + kAttnChunk - 1) / kAttnChunk;
   const int part = lane & 15, rsub = lane >> 4;  // this lane stages 16-byte piece `part` of rows rsub, rsub+2, ...
@@ -431,10 +439,15 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
     const int nt = min(T - j0, kAttnChunk);           // rows holding keys
     const __nv_bfloat16* pre = plane + (size_t)j0 * kAttnHeadDim + part * 8;
     for (int row = rsub; row < np; row += 2) cp16(buf + row * kPad + part * 8, pre + (size_t)row * kAttnHeadDim, 16);
-    for (int row = np + rsub; row < nt; row += 2) {
-      const int j = j0 + row;  // P <= j < T
-      const __nv_bfloat16* src = j < P + A ? plane + (size_t)anc[j - P] * kAttnHeadDim : self;
-      cp16(buf + row * kPad + part * 8, src + part * 8, 16);
+    for (int r0 = np; r0 < nt; r0 += 2) {  // warp-uniform trip count (the shuffle below)
+      const int row = r0 + rsub;
+      const int ai = j0 + row - P;  // ancestor index, A = self
+      const int av = __shfl_sync(0xffffffffu, anc_l, ai & 31);
+      if (row < nt) {
+        const __nv_bfloat16* src =
+            ai < A ? plane + (size_t)(ai < 32 ? av : __ldg(anc + ai)) * kAttnHeadDim : self;
+        cp16(buf + row * kPad + part * 8, src + part * 8, 16);
+      }
     }
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
     for (int row = max(nt, 0) + rsub; row < kAttnChunk; row += 2)

@@ -214,10 +214,12 @@ int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, in
 int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
                               const int32_t* n, int32_t n_out, int32_t k, void* const* out_dev, int32_t iters,
                               float* ms_per_launch, void* stream);
-/* K1 routing (tests): 0 forces the per-node tail path for every level, 1 (default)
- * runs uniform tree levels through the 16-node tile path.                      */
+/* K1 routing (tests): 1 runs uniform tree levels through the 16-node tile path,
+ * 0 (default) the per-node tail path.                                          */
 int tp_debug_attn_tile(int32_t on);
-/* K1 knobs: 0 = tile path on/off (as above), 1 = shared-prefix chunks per CTA (1..4). */
+/* K1 knobs: 0 = tile path on/off (as above), 1 = shared-prefix chunks per CTA (1..4),
+ * 2 = shared-prefix tail for uniform levels on/off, 3 = diagnostic skip mask for the
+ * Llama layer loop (bit 1 attention, 2 RMSNorm, 4 GEMMs; results WRONG while set). */
 int tp_debug_attn_knob(int32_t knob, int32_t value);
 /* GPU timeline (diagnostics): while enabled, CUDA events between kernel groups;
  * _read returns "tag=ms;..." (GPU time since the previous mark on the stream,

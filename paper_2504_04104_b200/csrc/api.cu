@@ -44,6 +44,10 @@ void timeline_mark(const char* tag, cudaStream_t st) {
 }
 }  // namespace tp
 
+namespace tp {
+extern int g_dbg_skip;
+}
+
 extern "C" int tp_debug_attn_tile(int32_t on) {
   tp::attn_set_tile(on != 0);
   return TP_OK;
@@ -53,6 +57,7 @@ extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
   if (knob == 0) tp::attn_set_tile(value != 0);
   else if (knob == 1) tp::attn_set_shared_run(value);
   else if (knob == 2) tp::attn_set_tail2(value != 0);
+  else if (knob == 3) tp::g_dbg_skip = value;
   else return TP_ECONFIG;
   return TP_OK;
 }

@@ -355,12 +355,22 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
   }
 }
 
-// One warp per (node, head): ordered merge of the shared chunks, then the
-// node's remaining chunks, then the bf16 output row.  The running state lives
-// in "lane layout" (lane l owns dims 4l..4l+3); a chunk computed on the tensor
+// One warp per (node, head): the node's own chunks (prefix tail, ancestors,
+// self), then the ordered merge of the shared chunks' partials followed by its
+// own chunks' partials, then the bf16 output row.  The running state lives in
+// "lane layout" (lane l owns dims 4l..4l+3); a chunk computed on the tensor
 // cores (row 0 of the tile, fragment layout) is handed over through smem.
-__global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(const __grid_constant__ AttnGroup G) {
-  pdl_wait();
+//
+// `early` (an attention kernel precedes this one in the stream, so the QKV
+// GEMM has completed before this grid is launched): up to kEarly own chunks
+// are computed BEFORE griddepcontrol.wait, i.e. while the shared-prefix kernel
+// is still running; only the merge waits for its partials.  Loads issued
+// before the wait bypass L1 (.cg).  The merge order — shared chunks, then own
+// chunks, each in chunk order — and every chunk's arithmetic are unchanged.
+constexpr int kEarly = 2;
+__global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB)
+    attn_tail_kernel(const __grid_constant__ AttnGroup G, int early) {
+  if (!early) pdl_wait();
   pdl_trigger();  // the O-projection GEMM may start streaming its weights
   extern __shared__ __align__(16) uint8_t dsm[];
   const int gi = member_of(G, blockIdx.x, 1);
@@ -371,65 +381,33 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int i = (local / a.H) * kWarps + warp;
-  if (i >= lv.n) return;
+  const bool live = i < lv.n;
   __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)warp * kTileElems;
   float* xo = reinterpret_cast<float*>(buf);  // 128-float hand-over row (aliases the tile between chunks)
   const int kh = h / (a.H / a.KV);
   const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
   const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
   const int c_start = G.m[gi].c_shared;
-  // issue the loads of the first 32 shared chunks' (max, sum) early: lane c holds chunk c
-  const size_t pbase = part_idx(a, i, h, 0);
-  float pm_l = -INFINITY, pl_l = 0.f;
-  if (lane < c_start) {
-    pm_l = __ldcg(a.pm + pbase + lane);
-    pl_l = __ldcg(a.pl + pbase + lane);
-  }
-  const int A = lv.anc_cnt[i];
-  const int32_t* anc = lv.anc_rows + (size_t)i * lv.anc_stride;  // decoded on the host, row order
-  const int anc_l = lane < A ? __ldg(anc + lane) : 0;  // first 32 ancestors in lane registers
-  const int P = lv.prefix_rows[i];
+  const int ii = live ? i : 0;
+  const int A = __ldcg(lv.anc_cnt + ii);
+  const int32_t* anc = lv.anc_rows + (size_t)ii * lv.anc_stride;  // decoded on the host, row order
+  const int anc_l = lane < A ? __ldcg(anc + lane) : 0;            // first 32 ancestors in lane registers
+  const int P = __ldcg(lv.prefix_rows + ii);
   const int T = P + A + 1;
-  const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)i * a.KV + kh) * kAttnHeadDim
-                                       : Kh + (size_t)(lv.row0 + i) * kAttnHeadDim;
-  const __nv_bfloat16* vself = a.vself ? a.vself + ((size_t)i * a.KV + kh) * kAttnHeadDim
-                                       : Vh + (size_t)(lv.row0 + i) * kAttnHeadDim;
-  // running state, lane layout: dims 4*lane .. 4*lane+3
-  float M = -INFINITY, L = 0.f;
-  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-  {  // shared chunks' partials, 8 chunk rows in flight per batch (one L2 round trip per batch)
-    constexpr int kPre = 8;
-    const float4* po = reinterpret_cast<const float4*>(a.po + pbase * kAttnHeadDim) + lane;
-    for (int c0 = 0; c0 < c_start; c0 += kPre) {
-      if (c0 > 0 && (c0 & 31) == 0) {  // next block of 32 chunk scalars
-        pm_l = c0 + lane < c_start ? __ldcg(a.pm + pbase + c0 + lane) : -INFINITY;
-        pl_l = c0 + lane < c_start ? __ldcg(a.pl + pbase + c0 + lane) : 0.f;
-      }
-      float4 blk[kPre];
+  const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)ii * a.KV + kh) * kAttnHeadDim
+                                       : Kh + (size_t)(lv.row0 + ii) * kAttnHeadDim;
+  const __nv_bfloat16* vself = a.vself ? a.vself + ((size_t)ii * a.KV + kh) * kAttnHeadDim
+                                       : Vh + (size_t)(lv.row0 + ii) * kAttnHeadDim;
+  uint32_t q1[8][4];
+  {
+    const uint32_t* qr = reinterpret_cast<const uint32_t*>(a.q + (size_t)ii * a.q_stride + h * kAttnHeadDim);
 #pragma unroll
-      for (int j = 0; j < kPre; ++j)
-        blk[j] = c0 + j < c_start ? __ldcg(po + (size_t)(c0 + j) * (kAttnHeadDim / 4)) : O;
-#pragma unroll
-      for (int j = 0; j < kPre; ++j) {
-        const int c = c0 + j;
-        if (c >= c_start) break;
-        float sa, sb;
-        merge_scale(M, L, __shfl_sync(0xffffffffu, pm_l, c & 31), __shfl_sync(0xffffffffu, pl_l, c & 31), sa, sb);
-        O.x = merge_val(O.x, blk[j].x, sa, sb);
-        O.y = merge_val(O.y, blk[j].y, sa, sb);
-        O.z = merge_val(O.z, blk[j].z, sa, sb);
-        O.w = merge_val(O.w, blk[j].w, sa, sb);
-      }
+    for (int kk = 0; kk < 8; ++kk) {
+      q1[kk][0] = g == 0 ? __ldcg(qr + 8 * kk + tig) : 0u;
+      q1[kk][1] = 0u;
+      q1[kk][2] = g == 0 ? __ldcg(qr + 8 * kk + 4 + tig) : 0u;
+      q1[kk][3] = 0u;
     }
-  }
-  uint32_t q1[8][4];  // loaded after the merge: in flight during the first K staging
-  const __nv_bfloat16* qr = a.q + (size_t)i * a.q_stride + h * kAttnHeadDim;
-#pragma unroll
-  for (int kk = 0; kk < 8; ++kk) {
-    q1[kk][0] = g == 0 ? ld_b32(qr + 16 * kk + 2 * tig) : 0u;
-    q1[kk][1] = 0u;
-    q1[kk][2] = g == 0 ? ld_b32(qr + 16 * kk + 8 + 2 * tig) : 0u;
-    q1[kk][3] = 0u;
   }
   const int c_end = (T + kAttnChunk - 1) / kAttnChunk;
   const int part = lane & 15, rsub = lane >> 4;  // this lane stages 16-byte piece `part` of rows rsub, rsub+2, ...
@@ -445,7 +423,7 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
       const int av = __shfl_sync(0xffffffffu, anc_l, ai & 31);
       if (row < nt) {
         const __nv_bfloat16* src =
-            ai < A ? plane + (size_t)(ai < 32 ? av : __ldg(anc + ai)) * kAttnHeadDim : self;
+            ai < A ? plane + (size_t)(ai < 32 ? av : __ldcg(anc + ai)) * kAttnHeadDim : self;
         cp16(buf + row * kPad + part * 8, src + part * 8, 16);
       }
     }
@@ -455,7 +433,8 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
     cp_wait_all();
     __syncwarp();
   };
-  for (int c = c_start; c < c_end; ++c) {
+  // one own chunk -> its partial (mc, lc warp-uniform; oc in lane layout)
+  auto run_chunk = [&](int c, float& mc, float& lc, float4& oc) {
     const int j0 = c * kAttnChunk;
     __syncwarp();  // previous chunk's hand-over row has been read
     stage(Kh, kself, j0);
@@ -473,13 +452,59 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB) attn_tail_kernel(co
         *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
     }
     __syncwarp();
-    const float4 oc = *reinterpret_cast<const float4*>(xo + 4 * lane);
+    oc = *reinterpret_cast<const float4*>(xo + 4 * lane);
+    mc = __shfl_sync(0xffffffffu, m[0], 0);
+    lc = __shfl_sync(0xffffffffu, l[0], 0);
+  };
+  // running state, lane layout: dims 4*lane .. 4*lane+3
+  float M = -INFINITY, L = 0.f;
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto merge_in = [&](float mc, float lc, float4 oc) {
     float sa, sb;
-    merge_scale(M, L, __shfl_sync(0xffffffffu, m[0], 0), __shfl_sync(0xffffffffu, l[0], 0), sa, sb);
+    merge_scale(M, L, mc, lc, sa, sb);
     O.x = merge_val(O.x, oc.x, sa, sb);
     O.y = merge_val(O.y, oc.y, sa, sb);
     O.z = merge_val(O.z, oc.z, sa, sb);
     O.w = merge_val(O.w, oc.w, sa, sb);
+  };
+  const int n_early = early && live ? min(c_end - c_start, kEarly) : 0;
+  float em[kEarly], el[kEarly];
+  float4 eo[kEarly];
+#pragma unroll
+  for (int k = 0; k < kEarly; ++k)
+    if (k < n_early) run_chunk(c_start + k, em[k], el[k], eo[k]);
+  if (early) pdl_wait();  // the shared-prefix partials are complete from here on
+  if (!live) return;
+  {  // shared chunks' partials, 8 chunk rows in flight per batch (one L2 round trip per batch)
+    constexpr int kPre = 8;
+    const size_t pbase = part_idx(a, i, h, 0);
+    const float4* po = reinterpret_cast<const float4*>(a.po + pbase * kAttnHeadDim) + lane;
+    float pm_l = -INFINITY, pl_l = 0.f;  // lane c holds chunk c0 + c's (max, sum)
+    for (int c0 = 0; c0 < c_start; c0 += kPre) {
+      if ((c0 & 31) == 0) {
+        pm_l = c0 + lane < c_start ? __ldcg(a.pm + pbase + c0 + lane) : -INFINITY;
+        pl_l = c0 + lane < c_start ? __ldcg(a.pl + pbase + c0 + lane) : 0.f;
+      }
+      float4 blk[kPre];
+#pragma unroll
+      for (int j = 0; j < kPre; ++j)
+        blk[j] = c0 + j < c_start ? __ldcg(po + (size_t)(c0 + j) * (kAttnHeadDim / 4)) : O;
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) {
+        const int c = c0 + j;
+        if (c >= c_start) break;
+        merge_in(__shfl_sync(0xffffffffu, pm_l, c & 31), __shfl_sync(0xffffffffu, pl_l, c & 31), blk[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kEarly; ++k)
+    if (k < n_early) merge_in(em[k], el[k], eo[k]);
+  for (int c = c_start + n_early; c < c_end; ++c) {
+    float mc, lc;
+    float4 oc;
+    run_chunk(c, mc, lc, oc);
+    merge_in(mc, lc, oc);
   }
   __nv_bfloat16* out = a.out + (size_t)i * a.out_stride + h * kAttnHeadDim + 4 * lane;
   uint2 u;
@@ -1101,7 +1126,8 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
   }
   if (ct > 0) {
     ::tp::count_launch();
-    TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kWarps * 32), kTailSmem, st, G));
+    TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kWarps * 32), kTailSmem, st, G,
+                       (cs + cg + cq + c2) > 0 ? 1 : 0));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tail", st);
   }

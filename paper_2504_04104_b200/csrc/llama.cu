@@ -424,6 +424,11 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
 // one request each (SpecPipe-DB) — that share the member's layers: their node
 // rows are concatenated for the GEMMs (weights streamed once for all requests),
 // K/V rows are scattered to each request's cache, and attention runs per item.
+// Diagnostics only (tp_debug_attn_knob 3): skip kernel classes in the layer loop
+// to measure each one's marginal cost inside the PDL chain — results are WRONG
+// while set.  Bits: 1 attention, 2 RMSNorm, 4 GEMMs.
+int g_dbg_skip = 0;
+
 int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int ws_base) {
   TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "member group size outside [1, 8]");
   tp_model* m0 = mem[0].items[0].s->m;
@@ -621,26 +626,28 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       }
     }
     gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
-    if (j == 0) {
+    if (j == 0 && !(g_dbg_skip & 2)) {
       ::tp::count_launch();
       TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
       TP_CUDA(cudaGetLastError());
     }
-    TP_TRY(sk_gemm_group(gq, pqkv, st));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gq, pqkv, st));
     timeline_mark("gemm_qkv", st);
-    for (size_t a0 = 0; a0 < aa.size(); a0 += kAttnMaxGroup) {
+    for (size_t a0 = 0; a0 < aa.size() && !(g_dbg_skip & 1); a0 += kAttnMaxGroup) {
       const int cnt = (int)std::min<size_t>(kAttnMaxGroup, aa.size() - a0);
       TP_TRY(attn_tree_group(aa.data() + a0, al.data() + a0, cnt, st));
     }
-    TP_TRY(sk_gemm_group(go, po, st));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(go, po, st));
     timeline_mark("gemm_o", st);
-    ::tp::count_launch();
-    TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
-    TP_CUDA(cudaGetLastError());
+    if (!(g_dbg_skip & 2)) {
+      ::tp::count_launch();
+      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
+      TP_CUDA(cudaGetLastError());
+    }
     timeline_mark("rmsnorm", st);
-    TP_TRY(sk_gemm_group(ggu, pgu, st));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(ggu, pgu, st));
     timeline_mark("gemm_gate_up", st);
-    TP_TRY(sk_gemm_group(gdn, pdn, st));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gdn, pdn, st));
     timeline_mark("gemm_down", st);
     // input norm of the next slot, for the members that continue
     int nc = 0, maxc = 0;
@@ -653,7 +660,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
         maxc = std::max(maxc, ng.n[a]);
         ++nc;
       }
-    if (nc) {
+    if (nc && !(g_dbg_skip & 2)) {
       ::tp::count_launch();
       TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxc, nc), dim3(kNormThreads), 0, st, nn, d, c.norm_eps));
       TP_CUDA(cudaGetLastError());

@@ -60,7 +60,6 @@ def parse():
     ap.add_argument("--db-model", default="13b", choices=["7b", "13b", "70b", "tiny"])
     ap.add_argument("--db-batches", default="1,16", help="SpecPipe-DB batch sizes (empty: skip)")
     ap.add_argument("--db-new", type=int, default=24)
-    ap.add_argument("--attn-knobs", default="", help="tile,shared_run (K1 tuning; default built-in)")
     return ap.parse_args()
 
 
@@ -246,10 +245,6 @@ def run_ours(args, rank, world):
 
     ngpu = args.gpus
     torch.cuda.set_device(0)
-    if args.attn_knobs:
-        tile, run = (int(x) for x in args.attn_knobs.split(","))
-        _lib.check(_lib.load().tp_debug_attn_knob(0, tile))
-        _lib.check(_lib.load().tp_debug_attn_knob(1, run))
     cfg = model_cfg(args.model)
     t0 = time.perf_counter()
     shards, splits = build_shards(cfg, args.stages, ngpu, max_nodes=max(64, args.w))

@@ -49,17 +49,18 @@ extern int g_dbg_skip;
 }
 
 extern "C" int tp_debug_attn_tile(int32_t on) {
-  tp::attn_set_tile(on != 0);
-  return TP_OK;
+  // the experimental 16-node tile path was removed (measured slower); only "off" remains valid
+  return on ? TP_ECONFIG : TP_OK;
 }
 
 extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
-  if (knob == 0) tp::attn_set_tile(value != 0);
-  else if (knob == 1) tp::attn_set_shared_run(value);
-  else if (knob == 2) tp::attn_set_tail2(value != 0);
-  else if (knob == 3) tp::g_dbg_skip = value;
-  else return TP_ECONFIG;
-  return TP_OK;
+  if (knob == 3) {
+    tp::g_dbg_skip = value;
+    return TP_OK;
+  }
+  if (knob == 1) return tp::attn_set_run(value);
+  // knobs 0 (tile path) and 2 (shared-prefix tail) were removed
+  return (knob == 0 || knob == 2) && value == 0 ? TP_OK : TP_ECONFIG;
 }
 
 extern "C" int tp_timeline_enable(int32_t on) {

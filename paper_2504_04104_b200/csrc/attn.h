@@ -20,9 +20,9 @@ struct AttnArgs {
   const __nv_bfloat16* vself;
   int H, KV;
   float scale;
-  float* pm;  // [n][H][max_chunks] per-chunk max          (shared chunks only)
-  float* pl;  // per-chunk sum
-  float* po;  // [n][H][max_chunks][128] per-chunk unnormalised output
+  float* pm;  // [n][H][max_chunks] per-run max          (shared runs only)
+  float* pl;  // per-run sum
+  float* po;  // [n][H][max_chunks][128] per-run unnormalised output
   int max_chunks;
   __nv_bfloat16* out;  // [n][H*128]
   int out_stride;
@@ -33,24 +33,21 @@ struct AttnMember {
   AttnArgs a;
   LevelDev lv;
   int c_shared;    // chunks inside every node's verified prefix
-  int zt;          // 64-node blocks
+  int zt;          // row blocks of the shared launch (64 rows; 16-row tiles when `small`)
+  int small;       // few rows: the run's chunks in parallel across warps
   int cta_shared;  // first CTA of this member in the shared launch
-  int cta_tail;    // first CTA of this member in the per-node tail launch (empty range if tiled)
-  int cta_tile;    // first CTA of this member in the 16-node tile launch (empty range if per-node)
-  int cta_tail2;   // first CTA of this member in the shared-prefix tail launch (uniform levels)
+  int cta_tail;    // first CTA of this member in the per-node tail launch (empty range for GQA)
   int cta_gqa;     // first CTA of this member in the GQA tail launch (one CTA per node and KV head)
 };
 
 struct AttnGroup {
   AttnMember m[kAttnMaxGroup];
   int count;
-  int ctas_shared, ctas_tail, ctas_tile, ctas_tail2;
+  int run;  // canonical chunks per run
 };
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
-void attn_set_tile(bool on);
-void attn_set_shared_run(int n);
-void attn_set_tail2(bool on);
+int attn_set_run(int run);
 // members[0..count) -> two launches (shared chunks, then per-node tail + ordered combine)
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st);
 

@@ -24,6 +24,8 @@ ap.add_argument("--model", default="7b")
 ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--prefix", type=int, default=512)
 ap.add_argument("--n", default="45,35,29,23,17,11,3")
+ap.add_argument("--run", type=int, default=0, help="attention chunks per run (knob 1; 0 = built-in)")
+ap.add_argument("--masks", default="1,2,3,4,7")
 args = ap.parse_args()
 cfg = model_cfg(args.model)
 m = LlamaModel(cfg, max_nodes=64)
@@ -43,6 +45,8 @@ for s, n in zip(r.stages, ns):
     items.append((s.kv, m, x, None, (args.prefix + d).tolist(), s.layer_range, False, list(range(n)), False,
                   (pre, args.prefix, 1, bits)))
 lib = _lib.lib()
+if args.run:
+    _lib.check(lib.tp_debug_attn_knob(1, args.run))
 
 
 def timed(members, mask):
@@ -64,6 +68,6 @@ labels = {0: "full", 1: "-attention", 2: "-rmsnorm", 3: "-attn-norm", 4: "-gemm"
 for name, members in (("group of %d" % len(ns), [[it] for it in items]), ("single (n=1)", [[items[-1]]])):
     base = timed(members, 0)
     print(f"{name}: full forward {base:8.1f} us", flush=True)
-    for mask in (1, 2, 3, 4, 7):
+    for mask in [int(x) for x in args.masks.split(",") if x]:
         t = timed(members, mask)
         print(f"  {labels[mask]:15s} {t:8.1f} us   (saves {base - t:7.1f} us)", flush=True)

@@ -265,56 +265,29 @@ def test_llama_long_context_invariance_and_oracle():
     assert float(np.abs(got - x).max()) <= TOL * max(1.0, float(np.abs(x).max()))
 
 
-@pytest.mark.parametrize("w,k", [(16, 4), (24, 8)])
-def test_tile_attention_equals_per_node_path(w, k):
-    """The 16-node tile path and the shared-prefix tail of K1 (uniform tree
-    levels) are bit-identical to the plain per-node path on every stage output
-    of a wide-tree pipeline run."""
-    cfg, m, _ = tiny_model(layers=4)
-    prompt = [int(t) for t in np.random.default_rng(6).integers(0, cfg.vocab, 150)]
-    ref = tp.sequential_decode(m, prompt, 40)
-    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.7, rank_decay=0.5, miss_prob=0.05, seed=9),
-                              cfg.vocab)
-    draft.bind_reference(tuple(prompt) + tuple(ref))
-    from paper_2504_04104_b200.pipeline import PipelineRunner
-
-    rec = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=w, k=k), draft, collect_trace=False)
-    rec.children_log = []
-    rec.prefill(prompt)
-    while len(rec.emitted) < 16:
-        rec.decode_step()
-    assert rec.emitted == ref[: len(rec.emitted)]
-    lib = _lib.lib()
-    runs = {}
-    # (tile, tail2): 16-node tile path, shared-prefix tail, plain per-node tail
-    modes = {"tile": (1, 0), "tail2": (0, 1), "per_node": (0, 0)}
-    try:
-        for name, (tile, tail2) in modes.items():
-            _lib.check(lib.tp_debug_attn_knob(0, tile))
-            _lib.check(lib.tp_debug_attn_knob(2, tail2))
-            _lib.check(lib.tp_debug_attn_knob(1, 3 if tile else 1))  # multi-chunk shared CTAs too
-            r = PipelineRunner(m, tp.PipelineConfig(num_stages=4), tp.BeamConfig(w=w, k=k), None,
-                               collect_trace=False)
-            r.prefill(prompt)
-            outs = []
-            for ch in rec.children_log:
-                r.launch_compute()
-                outs.append([None if s.out is None else s.out.cpu().clone() for s in r.stages])
-                r.step(ch)
-            runs[name] = outs
-    finally:
-        _lib.check(lib.tp_debug_attn_knob(0, 0))
-        _lib.check(lib.tp_debug_attn_knob(2, 0))
-        _lib.check(lib.tp_debug_attn_knob(1, 1))
-    wide = 0
-    for other in ("tile", "tail2"):
-        for a_, b_ in zip(runs[other], runs["per_node"]):
-            for x, y in zip(a_, b_):
-                assert (x is None) == (y is None)
-                if x is not None:
-                    assert torch.equal(x, y), other
-                    wide += x.shape[0] >= 4
-    assert wide > 5
+def test_attention_run_boundaries_ragged_prefixes():
+    """Canonical runs of 8 chunks: nodes of ONE level with ragged verified
+    prefixes (the shared kernel stops mid-run at floor(min P / 64); the tail
+    continues that run and crosses further run boundaries with the prefix
+    tails of the longer nodes), with scattered ancestor rows, are bit-identical
+    to each node computed alone (its own c_shared, its own run split)."""
+    cfg, m, _ = tiny_model()
+    rng = np.random.default_rng(33)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, 1700)]
+    cache = KvCache(cfg.layers, cfg.hidden, capacity=1792)
+    tp.model.prefill_rows(m, cache, prompt)
+    prefixes = [600, 1100, 1530, 513, 1024, 1650]
+    rows, pos = [], []
+    for P in prefixes:
+        extra = sorted(rng.choice(np.arange(P + 1, 1700), size=5, replace=False).tolist())
+        rows.append(np.concatenate([np.arange(P), np.asarray(extra)]).astype(np.int64))
+        pos.append(P + len(extra))
+    toks = [int(t) for t in rng.integers(0, cfg.vocab, len(prefixes))]
+    uids = list(range(len(prefixes)))
+    together = cache._forward(m, rows, None, toks, pos, None, False, uids, False).cpu()
+    for i in range(len(prefixes)):
+        alone = cache._forward(m, [rows[i]], None, [toks[i]], [pos[i]], None, False, [uids[i]], False).cpu()
+        assert torch.equal(alone[0], together[i]), (i, prefixes[i])
 
 
 def test_kv_capacity_growth_mid_decode_lossless():

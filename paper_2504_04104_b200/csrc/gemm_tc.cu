@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -50,7 +51,10 @@ constexpr int kBM = 128, kBK = 64;
 constexpr int kMaxStages = 16;
 constexpr int kMaxTmemBufs = 4;  // accumulator buffers: the MMA may run this many segments ahead
 constexpr int kDrainWarps = 4;  // one per TMEM lane quarter: drain accumulators, publish partials, sole-owner epilogue
-constexpr int kRedWarps = 8;    // stream-K fix-up reducers, fed through a shared-memory queue
+#ifndef TP_RED_WARPS
+#define TP_RED_WARPS 8
+#endif
+constexpr int kRedWarps = TP_RED_WARPS;  // stream-K fix-up reducers, fed through a shared-memory queue
 constexpr int kThreads = 64 + 32 * (kDrainWarps + kRedWarps);
 constexpr int kRedSlots = kMaxGroup + 1;  // <= one reduction per member per CTA, plus the end sentinel
 constexpr int kBarBytes = 1024;           // mbarriers, TMEM holder, reduction queue
@@ -117,7 +121,7 @@ SkPlan sk_plan(int n_out, int k, int n) {
 
 // Tuning knobs (tp_debug_gemm_knob): ring depth cap and smem budget.
 static int g_knob_max_stages = 8;
-static int g_knob_smem_kb = 200;
+static int g_knob_smem_kb = getenv("TP_GEMM_SMEM_KB") ? atoi(getenv("TP_GEMM_SMEM_KB")) : 200;
 static int g_knob_fixup = 0;  // diagnostics only: 1 skips the reduction, 2 also the partial publish, 3 reduces without waiting for arrivals (WRONG results)
 
 static int stages_for(int n_pad) {
@@ -290,7 +294,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // Work items are (member g, k-block t) for g = 0..count-1, t in [t0, t1):
 // the TMA producer, the MMA issuer and the epilogue warps walk the same
 // sequence, the smem ring and the TMEM double buffer continuing across members.
+#ifdef TP_GEMM_MAXNREG
+__global__ void __maxnreg__(TP_GEMM_MAXNREG)
+#else
 __global__ void __launch_bounds__(kThreads, 1)
+#endif
     sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages, int nbuf, int fixup_mode) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

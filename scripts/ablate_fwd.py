@@ -26,6 +26,7 @@ ap.add_argument("--prefix", type=int, default=512)
 ap.add_argument("--n", default="45,35,29,23,17,11,3")
 ap.add_argument("--run", type=int, default=0, help="attention chunks per run (knob 1; 0 = built-in)")
 ap.add_argument("--masks", default="1,2,3,4,7")
+ap.add_argument("--sib", type=float, default=0.0, help="mean sibling-group size (0: every node its own chain)")
 args = ap.parse_args()
 cfg = model_cfg(args.model)
 m = LlamaModel(cfg, max_nodes=64)
@@ -39,6 +40,12 @@ rng = np.random.default_rng(2)
 items = []
 for s, n in zip(r.stages, ns):
     d = rng.integers(0, depth, n)  # node i: ancestors = rows prefix .. prefix+d_i-1 (a chain), then itself
+    if args.sib > 0:  # consecutive siblings share the parent's chain (groups ~ geometric, mean args.sib)
+        i = 0
+        while i < n:
+            gsz = int(min(16, n - i, rng.geometric(1.0 / args.sib)))
+            d[i : i + gsz] = d[i]
+            i += gsz
     pre = np.full(n, args.prefix, dtype=np.int32)
     bits = ((np.uint64(1) << d.astype(np.uint64)) - np.uint64(1)).reshape(n, 1).astype(np.uint64)
     x = (torch.randn(n, cfg.hidden, device="cuda") * 0.5).to(torch.bfloat16)

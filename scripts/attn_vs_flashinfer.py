@@ -1,0 +1,76 @@
+"""SURVEY 8(d) comparator: K1 (tree-masked attention, one grouped launch pair
+per layer slot) vs FlashInfer 0.6.11 batched ragged prefill with custom masks
+on the same shapes: 7 stages' tree levels of the 7B bench (n = 45..3 nodes,
+32 heads, head_dim 128), a 512-row verified prefix, ancestor chains of depth
+< 24, self last.  K1 is measured in situ (one grouped phase-1 forward of the
+7 stages with and without attention, PDL chain intact: the per-slot
+difference); FlashInfer as one `run` per layer slot over the 7 requests.
+
+    python scripts/attn_vs_flashinfer.py [--prefix 512]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import torch
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--prefix", type=int, default=512)
+ap.add_argument("--n", default="45,35,29,23,17,11,3")
+ap.add_argument("--iters", type=int, default=50)
+args = ap.parse_args()
+ns = [int(x) for x in args.n.split(",")]
+H = KV = 32
+D = 128
+depth = 24
+rng = np.random.default_rng(2)
+
+import flashinfer  # noqa: E402
+
+qo_indptr, kv_indptr, masks = [0], [0], []
+for n in ns:
+    d = rng.integers(0, depth, n)
+    kv_len = args.prefix + depth + n  # prefix, tree rows, the level's own rows
+    m = np.zeros((n, kv_len), dtype=bool)
+    m[:, : args.prefix] = True
+    for i in range(n):
+        m[i, args.prefix : args.prefix + d[i]] = True  # ancestors (a chain)
+        m[i, args.prefix + depth + i] = True  # self
+    masks.append(m.reshape(-1))
+    qo_indptr.append(qo_indptr[-1] + n)
+    kv_indptr.append(kv_indptr[-1] + kv_len)
+dev = "cuda"
+q = (torch.randn(qo_indptr[-1], H, D, device=dev) * 0.5).to(torch.bfloat16)
+k = (torch.randn(kv_indptr[-1], KV, D, device=dev) * 0.5).to(torch.bfloat16)
+v = (torch.randn(kv_indptr[-1], KV, D, device=dev) * 0.5).to(torch.bfloat16)
+mask = torch.from_numpy(np.concatenate(masks)).to(dev)
+ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+w = flashinfer.BatchPrefillWithRaggedKVCacheWrapper(ws, "NHD")
+w.plan(torch.tensor(qo_indptr, dtype=torch.int32, device=dev), torch.tensor(kv_indptr, dtype=torch.int32, device=dev),
+       H, KV, D, custom_mask=mask, q_data_type=torch.bfloat16)
+for _ in range(5):
+    w.run(q, k, v)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(args.iters):
+    w.run(q, k, v)
+e1.record()
+torch.cuda.synchronize()
+fi_us = e0.elapsed_time(e1) * 1e3 / args.iters
+
+# K1 in situ: ablation of one grouped forward (4 layer slots)
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+out = subprocess.run([sys.executable, os.path.join(root, "scripts", "ablate_fwd.py"), "--prefix", str(args.prefix),
+                      "--n", args.n, "--masks", "1"], capture_output=True, text=True, check=True).stdout
+full = float(out.split("full forward")[1].split("us")[0])
+noattn = float(out.split("-attention")[1].split("us")[0])
+k1_us = (full - noattn) / 4
+print(json.dumps({"comparator": "K1 vs FlashInfer batched ragged prefill (custom mask)", "prefix": args.prefix,
+                  "nodes_per_stage": ns, "heads": H, "head_dim": D,
+                  "k1_us_per_layer_slot_in_situ": round(k1_us, 1),
+                  "flashinfer_us_per_layer_slot": round(fi_us, 1),
+                  "flashinfer_version": flashinfer.__version__}))

@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-comparators", action="store_true", help="skip the vanilla-PP / cuBLAS comparators")
     ap.add_argument("--no-perfect", action="store_true", help="skip the perfect-draft TBT field")
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--db-model", default="13b", choices=["7b", "13b", "70b", "tiny"])
@@ -251,7 +252,7 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t0
     prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, args.prompt_len)]
-    n_ref = args.warmup + args.steps + args.profile_steps + 2 * args.stages + 8
+    n_ref = args.warmup + args.steps + args.profile_steps + 2 * args.stages + 16
     ref = sequential_decode_staged(shards if ngpu > 1 else shards[0], splits, prompt, n_ref)
     pcfg = PipelineConfig(num_stages=args.stages, layer_splits=tuple(splits))
     beam = tp.BeamConfig(w=args.w, k=args.k)
@@ -297,7 +298,7 @@ def run_ours(args, rank, world):
     e2e_host["loop_wall"] = round(t_wall * 1e3 / args.steps, 4)
     launches = _lib.launch_count() - l0
     io1 = _lib.io_bytes()
-    for _ in range(args.profile_steps):  # untimed: levels for the profiled replay below
+    for _ in range(args.profile_steps + 8):  # untimed: levels for the timeline (8) and profiled replays below
         runner.decode_step()
     resident = []
     children = runner.children_log
@@ -450,9 +451,70 @@ def run_ours(args, rank, world):
                                  "ideal_ms_per_step_all_stages_occupied": round(
                                      (args.stages * (cfg.layers // args.stages) * layer_w + head_w) / (peak * 1e6), 4)}
         pr.close()
+    if not args.no_comparators:
+        line["comparators"] = comparators(args, cfg, model_arg, splits, prompt, sync_all)
     if rank == 0 and ngpu == 1 and args.db_batches:
         line["specpipe_db"] = run_db(args)
     print(json.dumps(line), flush=True)
+
+
+def comparators(args, cfg, model_arg, splits, prompt, sync_all):
+    """SURVEY 8(d) GPU comparators on the same box and kernels:
+    * vanilla PP (`run_vanilla` semantics, reference `pipeline.py:616-662`): one token
+      in flight through every stage = steady-state GPU greedy decode of the staged
+      model, timed as the difference of two decode lengths (the prefill cancels);
+    * K2 vs cuBLAS (torch bf16 matmul) at the same tiny M: each layer GEMM of the
+      model for the stage-1 mean node count and for the lone verify node."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2504_04104_b200 import _lib
+    from paper_2504_04104_b200.pipeline import sequential_decode_staged
+
+    out = {}
+    lens = (8, 40)
+    ts = []
+    for n_tok in lens:
+        sync_all()
+        t = time.perf_counter()
+        sequential_decode_staged(model_arg, splits, prompt, n_tok)
+        sync_all()
+        ts.append(time.perf_counter() - t)
+    out["vanilla_pp"] = {"ms_per_token": round((ts[1] - ts[0]) * 1e3 / (lens[1] - lens[0]), 4),
+                         "note": "same kernels at n=1, one token in flight through all stages (wall clock, "
+                                 "synchronised, difference of a %d- and a %d-token decode)" % lens}
+    lib = _lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    d, f = cfg.hidden, cfg.ffn
+    q = cfg.heads * 128
+    kvd = cfg.kv_heads * 128
+    shapes = [("qkv", q + 2 * kvd, d), ("o", d, q), ("gate_up", 2 * f, d), ("down", d, f)]
+    rows = []
+    for n in (45, 1):
+        for name, n_out, k in shapes:
+            w = (torch.randn(n_out, k, device="cuda") * 0.02).to(torch.bfloat16)
+            x = torch.randn(n, k, device="cuda").to(torch.bfloat16)
+            y = torch.empty(n, n_out, device="cuda")
+            ms = C.c_float()
+            arr = lambda t: (C.c_void_p * 1)(t.data_ptr())  # noqa: E731
+            _lib.check(lib.tp_debug_gemm_group_timed(0, 1, arr(w), arr(x), (C.c_int32 * 1)(n), n_out, k, arr(y),
+                                                     20, C.byref(ms), st))
+            for _ in range(3):
+                torch.matmul(x, w.t())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                torch.matmul(x, w.t())
+            e1.record()
+            torch.cuda.synchronize()
+            by = n_out * k * 2 + n * k * 2
+            rows.append({"gemm": name, "n": n, "k2_us": round(ms.value * 1e3, 1),
+                         "cublas_us": round(e0.elapsed_time(e1) * 1e3 / 20, 1),
+                         "k2_gbs": round(by / ms.value / 1e6), "cublas_gbs": round(by / (e0.elapsed_time(e1) / 20) / 1e6)})
+            del w, x, y
+    out["k2_vs_cublas"] = rows
+    return out
 
 
 def run_db(args):

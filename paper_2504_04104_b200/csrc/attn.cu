@@ -49,7 +49,7 @@ namespace tp {
 constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ldmatrix)
 constexpr int kWarps = 4;
 constexpr int kTileElems = kAttnChunk * kPad;
-constexpr size_t kTailSmem = (size_t)kWarps * kTileElems * 2;
+constexpr size_t kTailSmem = (size_t)kWarps * (kTileElems * 2 + 128 * 4);  // per warp: chunk tile + hand-over row
 
 __device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) {
   return *reinterpret_cast<const uint32_t*>(p);
@@ -549,7 +549,8 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB)
   const int i = (local / a.H) * kWarps + warp;
   const bool live = i < lv.n;
   __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)warp * kTileElems;
-  float* xo = reinterpret_cast<float*>(buf);  // 128-float hand-over row (aliases the tile between chunks)
+  float* xo = reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)kWarps * kTileElems) +
+              warp * 128;  // 128-float hand-over row (its own: PV halves are handed over one at a time)
   const int kh = h / (a.H / a.KV);
   const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
   const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
@@ -610,15 +611,21 @@ __global__ void __launch_bounds__(kWarps * 32, TP_TAIL_MINB)
     chunk_scores(q1, buf, lim, a.scale, m, l, pa, lane);
     __syncwarp();
     stage(Vh, vself, j0);
-    float o0[8][4], o1[8][4];
-    chunk_pv_half<0>(pa, buf, o0, lane);
-    chunk_pv_half<1>(pa, buf, o1, lane);
-    __syncwarp();  // every lane is done reading the tile: reuse it for the hand-over row
-    if (g == 0) {
+    {
+      float o[8][4];
+      chunk_pv_half<0>(pa, buf, o, lane);
+      if (g == 0) {
 #pragma unroll
-      for (int nd = 0; nd < 8; ++nd) {
-        *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o0[nd][0], o0[nd][1]);
-        *reinterpret_cast<float2*>(xo + 64 + nd * 8 + 2 * tig) = make_float2(o1[nd][0], o1[nd][1]);
+        for (int nd = 0; nd < 8; ++nd) *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
+      }
+    }
+    {
+      float o[8][4];
+      chunk_pv_half<1>(pa, buf, o, lane);
+      if (g == 0) {
+#pragma unroll
+        for (int nd = 0; nd < 8; ++nd)
+          *reinterpret_cast<float2*>(xo + 64 + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
       }
     }
     __syncwarp();

@@ -35,6 +35,8 @@
 // kernel and continued in the tail goes through the same merge sequence).  A
 // node computed inside a 64-node tree level is therefore bit-identical to the
 // same position decoded alone (GPU pipeline == GPU greedy decode).
+#include <type_traits>
+
 #include "attn.h"
 #include "gemm_tc.h"
 
@@ -209,24 +211,30 @@ __device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
   return gi;
 }
 
-// o = P . V over the dims [64 * HALF, 64 * HALF + 64) (n-tiles 8*HALF .. 8*HALF+7
-// of chunk_pv: the same MMAs in the same k order, half the live accumulators).
-template <int HALF>
-__device__ __forceinline__ void chunk_pv_half(const uint32_t (&pa)[4][4], const __nv_bfloat16* sV, float (&o)[8][4],
-                                              int lane) {
+// o = P . V over the dims [128 / NP * PART, 128 / NP * (PART + 1)) — n-tiles of
+// the full P . V in the same k order (the same MMAs per output element), with
+// 1/NP of the accumulators live.
+template <int PART, int NP>
+__device__ __forceinline__ void chunk_pv_part(const uint32_t (&pa)[4][4], const __nv_bfloat16* sV,
+                                              float (&o)[16 / NP][4], int lane) {
   const int mi = lane >> 3, mr = lane & 7;
 #pragma unroll
-  for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+  for (int nd = 0; nd < 16 / NP; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
 #pragma unroll
-  for (int n2l = 0; n2l < 4; ++n2l)
+  for (int n2l = 0; n2l < 8 / NP; ++n2l)
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
-      const int n2 = 4 * HALF + n2l;
+      const int n2 = (8 / NP) * PART + n2l;
       uint32_t b[4];
       ldsm4t(su32(sV + (16 * kk + 8 * (mi & 1) + mr) * kPad + 16 * n2 + 8 * (mi >> 1)), b);
       mma16816(o[2 * n2l], pa[kk], b[0], b[1]);
       mma16816(o[2 * n2l + 1], pa[kk], b[2], b[3]);
     }
+}
+template <int HALF>
+__device__ __forceinline__ void chunk_pv_half(const uint32_t (&pa)[4][4], const __nv_bfloat16* sV, float (&o)[8][4],
+                                              int lane) {
+  chunk_pv_part<HALF, 2>(pa, sV, o, lane);
 }
 
 // Merge a partial (mc, lc, oc) into a lane-layout state (M, L, O).
@@ -486,22 +494,20 @@ __global__ void __launch_bounds__(kWarps * 32, TP_SHARED_MINB) attn_shared_kerne
       chunk_scores(qa, sK, lim, a.scale, m, l, pa, lane);
       merge_scale(M[0], L[0], m[0], l[0], sa[0], sb[0]);
       merge_scale(M[1], L[1], m[1], l[1], sa[1], sb[1]);
-      {
-        float o[8][4];
-        chunk_pv_half<0>(pa, sK + kTileElems, o, lane);
+      auto merge_part = [&](auto part_tag) {  // PV a quarter of the dims at a time, merged at once
+        constexpr int P = decltype(part_tag)::value;
+        float o[4][4];
+        chunk_pv_part<P, 4>(pa, sK + kTileElems, o, lane);
 #pragma unroll
-        for (int nd = 0; nd < 8; ++nd)
+        for (int nd = 0; nd < 4; ++nd)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) O[nd][e] = merge_val(O[nd][e], o[nd][e], sa[e >> 1], sb[e >> 1]);
-      }
-      {
-        float o[8][4];
-        chunk_pv_half<1>(pa, sK + kTileElems, o, lane);
-#pragma unroll
-        for (int nd = 0; nd < 8; ++nd)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) O[8 + nd][e] = merge_val(O[8 + nd][e], o[nd][e], sa[e >> 1], sb[e >> 1]);
-      }
+          for (int e = 0; e < 4; ++e)
+            O[4 * P + nd][e] = merge_val(O[4 * P + nd][e], o[nd][e], sa[e >> 1], sb[e >> 1]);
+      };
+      merge_part(std::integral_constant<int, 0>{});
+      merge_part(std::integral_constant<int, 1>{});
+      merge_part(std::integral_constant<int, 2>{});
+      merge_part(std::integral_constant<int, 3>{});
     }
     __syncthreads();  // buffer `buf` is restaged for chunk c + 2
   }
@@ -735,14 +741,21 @@ __global__ void __launch_bounds__(kGqaWarps * 32, 2) attn_tail_gqa_kernel(const 
     float m[2], l[2];
     uint32_t pa[4][4];
     chunk_scores(q1, sK, lim, a.scale, m, l, pa, lane);
-    float o0[8][4], o1[8][4];
-    chunk_pv_half<0>(pa, sV, o0, lane);
-    chunk_pv_half<1>(pa, sV, o1, lane);
-    if (g == 0) {
+    {
+      float o[8][4];
+      chunk_pv_half<0>(pa, sV, o, lane);
+      if (g == 0) {
 #pragma unroll
-      for (int nd = 0; nd < 8; ++nd) {
-        *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o0[nd][0], o0[nd][1]);
-        *reinterpret_cast<float2*>(xo + 64 + nd * 8 + 2 * tig) = make_float2(o1[nd][0], o1[nd][1]);
+        for (int nd = 0; nd < 8; ++nd) *reinterpret_cast<float2*>(xo + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
+      }
+    }
+    {
+      float o[8][4];
+      chunk_pv_half<1>(pa, sV, o, lane);
+      if (g == 0) {
+#pragma unroll
+        for (int nd = 0; nd < 8; ++nd)
+          *reinterpret_cast<float2*>(xo + 64 + nd * 8 + 2 * tig) = make_float2(o[nd][0], o[nd][1]);
       }
     }
     __syncwarp();

@@ -12,6 +12,6 @@ for what in "$@"; do
     hostprof) timeout 600 python scripts/host_profile.py > gpurun_out/hostprof.log 2>&1; head -60 gpurun_out/hostprof.log ;;
     sweep) timeout 600 python scripts/gemm_sweep.py > gpurun_out/gemm_sweep.log 2>&1; cat gpurun_out/gemm_sweep.log ;;
     launches) timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py --steps 4 > gpurun_out/prof.log 2>&1; echo "ncu rc=$?"; python scripts/launch_summary.py gpurun_out/launches.csv 4 | tee gpurun_out/launch_summary.txt ;;
-    full) timeout 1200 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:sk_gemm -c 3 -o gpurun_out/gemm_full -f python scripts/profile_step.py --steps 1 > gpurun_out/full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/full.log ;;
+    full) timeout 1200 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:sk_gemm -s 5 -c 3 -o gpurun_out/gemm_full -f python scripts/profile_step.py --steps 2 > gpurun_out/full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/full.log ;;
   esac
 done

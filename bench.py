@@ -26,6 +26,7 @@ reference's single-process design); other ranks only join the barriers.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -284,6 +285,8 @@ def run_ours(args, rank, world):
     l0 = _lib.launch_count()
     io0 = _lib.io_bytes()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    gc.collect()  # as timeit does: no cyclic-GC pause (or finaliser run) inside a timed loop
+    gc.disable()
     with ClockSampler(0) as clocks:
         t_wall = time.perf_counter()
         ev[0].record(streams[0])
@@ -292,6 +295,7 @@ def run_ours(args, rank, world):
         ev[1].record(streams[-1] if ngpu > 1 else streams[0])
         sync_all()
         t_wall = time.perf_counter() - t_wall
+    gc.enable()
     e2e_tokens = len(runner.emitted) - tok0
     e2e_ms = t_wall * 1e3 / max(1, e2e_tokens)
     e2e_host = {k: round(v * 1e3 / args.steps, 4) for k, v in runner.host_s.items()}
@@ -320,6 +324,8 @@ def run_ours(args, rank, world):
     head_w = 2.0 * cfg.vocab * cfg.hidden
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     replay.host_s = {k: 0.0 for k in replay.host_s}
+    gc.collect()
+    gc.disable()
     th = time.perf_counter()
     clocks.__enter__()
     e0.record(streams[0])
@@ -341,6 +347,7 @@ def run_ours(args, rank, world):
     e1.record(streams[0])
     host_loop_s = time.perf_counter() - th
     sync_all()
+    gc.enable()
     clocks.__exit__()
     host_diag = {k: round(v * 1e3 / args.steps, 4) for k, v in replay.host_s.items()}
     host_diag["loop_wall"] = round(host_loop_s * 1e3 / args.steps, 4)
@@ -437,12 +444,15 @@ def run_ours(args, rank, world):
         sync_all()
         pt0 = len(pr.emitted)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
         f0.record(streams[0])
         nsteps = min(args.steps, max(8, len(ref) - len(pr.emitted) - args.stages - 2))
         for _ in range(nsteps):
             pr.decode_step()
         f1.record(streams[0])
         sync_all()
+        gc.enable()
         ptok = len(pr.emitted) - pt0
         assert pr.emitted == ref[: len(pr.emitted)]
         line["perfect_draft"] = {"tbt_ms_per_token": round(f0.elapsed_time(f1) / max(1, ptok), 4),

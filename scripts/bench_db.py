@@ -5,6 +5,7 @@ ragged GPU tick.  Prints one JSON object per batch size.
     python scripts/bench_db.py [--model 13b] [--batches 1,8,32] [--new 24]
 """
 import argparse
+import gc
 import json
 import os
 import sys
@@ -38,6 +39,8 @@ def measure_db(model, batch, prompt_len, new_tokens, total_width=64, k=16, stage
     admit_s = time.perf_counter() - t_all
     tok0 = sum(len(s.runner.emitted) for s in sched.active)
     ticks = 0
+    gc.collect()  # no cyclic-GC pause inside the timed ticks (as timeit)
+    gc.disable()
     t1 = time.perf_counter()
     # steady state: the full batch stays active until the first request finishes
     while len(sched.active) == batch and ticks < 10 * new_tokens:
@@ -45,6 +48,7 @@ def measure_db(model, batch, prompt_len, new_tokens, total_width=64, k=16, stage
         ticks += 1
     torch.cuda.synchronize()
     steady_s = time.perf_counter() - t1
+    gc.enable()
     tokens = sum(len(s.runner.emitted) for s in sched.active + sched.finished) - tok0
     metrics = sched.run()
     torch.cuda.synchronize()

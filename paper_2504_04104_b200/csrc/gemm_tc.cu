@@ -285,6 +285,10 @@ __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int
   }
 }
 
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -472,8 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
           drain_bar();
           if (et == 0) {  // barrier + one gpu-scope fence publishes every drain thread's stores
-            __threadfence();
-            atomicAdd(&arrive[mt], 1);
+            red_release_add(&arrive[mt], 1);  // release: every drain thread's partial stores (ordered by the barrier)
             // the contributors whose ranges end inside the tile reduce it, each a
             // slice of the nodes (they finish together; one CTA reducing a whole
             // tile was measured 2x slower on the o / down projections)
@@ -509,8 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int E = cend - it.cfirst + 1, rank = c - it.cfirst;
       if (rt == 0 && fixup_mode != 3) {  // counters only grow: this launch's arrivals are complete at (epoch+1)*cnt
         const int target = (e.epoch + 1) * it.cnt;
-        while (ld_acquire(&e.counters[it.mt]) < target) __nanosleep(32);
-        __threadfence();
+        while (ld_acquire(&e.counters[it.mt]) < target) {
+        }
       }
       red_bar();
       reduce_apply<kRedWarps>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane);

@@ -50,6 +50,41 @@ for _ in range(args.ticks):
     walls.append((time.perf_counter() - t) * 1e3)
     gpus.append(e0.elapsed_time(e1))
 print(f"batch {args.batch}: wall {np.mean(walls):.3f} ms/tick, GPU span {np.mean(gpus):.3f} ms/tick (synchronised ticks)")
+# host phases of an unsynchronised tick (wrappers around the tick's parts)
+import paper_2504_04104_b200.batching as B  # noqa: E402
+import paper_2504_04104_b200.model as M  # noqa: E402
+
+acc = {}
+
+
+def timed(name, fn):
+    def w(*a, **k):
+        t = time.perf_counter()
+        try:
+            return fn(*a, **k)
+        finally:
+            acc[name] = acc.get(name, 0.0) + time.perf_counter() - t
+    return w
+
+
+sched._combined_compute = timed("combined_compute", sched._combined_compute)
+for slot in sched.active:
+    slot.runner.decode_step = timed("decode_step", slot.runner.decode_step)
+    slot.runner.step = timed("step", slot.runner.step)
+M._launch_restrict = timed("flush_restrict", M._launch_restrict)
+M._launch_rows = timed("flush_rows", M._launch_rows)
+import gc  # noqa: E402
+
+gc.collect()
+gc.disable()
+t = time.perf_counter()
+for _ in range(args.ticks):
+    sched.tick()
+torch.cuda.synchronize()
+tot = time.perf_counter() - t
+gc.enable()
+print(f"unsynchronised: {tot * 1e3 / args.ticks:.3f} ms/tick; host phases ms/tick:",
+      {k: round(v * 1e3 / args.ticks, 3) for k, v in acc.items()})
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(args.ticks):

@@ -73,7 +73,9 @@ def main():
 
     torch.cuda.set_device(0)
     model = LlamaModel(model_cfg(args.model), max_nodes=64)
-    for b in [int(x) for x in args.batches.split(",")]:
+    batches = [int(x) for x in args.batches.split(",")]
+    measure_db(model, max(batches), args.prompt_len, 8, combined=not args.uncombined)  # untimed warm-up
+    for b in batches:
         print(json.dumps(measure_db(model, b, args.prompt_len, args.new, combined=not args.uncombined)), flush=True)
 
 

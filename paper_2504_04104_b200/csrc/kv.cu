@@ -151,6 +151,29 @@ __device__ __forceinline__ bool better(T a, int ia, T b, int ib) {
   return a > b || (a == b && ia < ib);
 }
 
+// Per-thread best of a row: 16 independent loads per round trip (`better` is a
+// strict total order, so the visiting order cannot change the winner).
+template <typename T>
+__device__ __forceinline__ void scan_best(const T* __restrict__ row, int V, T& best, int& bi) {
+  constexpr int U = 16;
+  for (int base = threadIdx.x; base < V; base += blockDim.x * U) {
+    T xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = base + u * (int)blockDim.x;
+      xv[u] = v < V ? row[v] : row[0];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = base + u * (int)blockDim.x;
+      if (v < V && better(xv[u], v, best, bi)) {
+        best = xv[u];
+        bi = v;
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(1024) argmax_match_kernel(const T* __restrict__ logits, int V,
                                                             const int32_t* __restrict__ children,
@@ -159,15 +182,12 @@ __global__ void __launch_bounds__(1024) argmax_match_kernel(const T* __restrict_
   pdl_trigger();
   __shared__ T sv[32];
   __shared__ int si[32];
+  __shared__ int s_ib, s_child;
+  // the candidate children, one per thread, loaded alongside the scan (not in a serial loop at the end)
+  const int my_child = (int)threadIdx.x < n_children ? children[threadIdx.x] : -1;
   T best = logits[0];
   int bi = 0;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    T x = logits[v];
-    if (better(x, v, best, bi)) {
-      best = x;
-      bi = v;
-    }
-  }
+  scan_best(logits, V, best, bi);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     T ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -191,25 +211,30 @@ __global__ void __launch_bounds__(1024) argmax_match_kernel(const T* __restrict_
         b = sv[k];
         ib = si[k];
       }
-    int child = -1;
-    for (int c = 0; c < n_children; ++c)
-      if (children[c] == ib) {
-        child = c;
-        break;
-      }
+    s_ib = ib;
+    s_child = 0x7fffffff;
+  }
+  __syncthreads();
+  const int ib = s_ib;
+  if (my_child == ib) atomicMin(&s_child, (int)threadIdx.x);  // first matching child (BFS order)
+  for (int c = threadIdx.x + blockDim.x; c < n_children; c += blockDim.x)
+    if (children[c] == ib) atomicMin(&s_child, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
     result[0] = ib;
-    result[1] = child;
+    result[1] = s_child == 0x7fffffff ? -1 : s_child;
   }
 }
 
 int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_children, int n_children,
                  int32_t* d_result, cudaStream_t st) {
+  ::tp::count_launch();
   if (is_f64)
-    ::tp::count_launch(), argmax_match_kernel<double><<<1, 1024, 0, st>>>((const double*)logits, vocab, d_children, n_children,
-                                                    d_result);
+    TP_CUDA(launch_pdl(argmax_match_kernel<double>, dim3(1), dim3(1024), 0, st, (const double*)logits, vocab, d_children,
+                       n_children, d_result));
   else
-    ::tp::count_launch(), argmax_match_kernel<float><<<1, 1024, 0, st>>>((const float*)logits, vocab, d_children, n_children,
-                                                   d_result);
+    TP_CUDA(launch_pdl(argmax_match_kernel<float>, dim3(1), dim3(1024), 0, st, (const float*)logits, vocab, d_children,
+                       n_children, d_result));
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }
@@ -224,13 +249,7 @@ __global__ void __launch_bounds__(1024) argmax_rows_kernel(const float* __restri
   const float* row = logits + (size_t)blockIdx.x * V;
   float best = row[0];
   int bi = 0;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    const float x = row[v];
-    if (better(x, v, best, bi)) {
-      best = x;
-      bi = v;
-    }
-  }
+  scan_best(row, V, best, bi);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, best, o);

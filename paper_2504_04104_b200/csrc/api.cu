@@ -63,6 +63,30 @@ extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
   return (knob == 0 || knob == 2) && value == 0 ? TP_OK : TP_ECONFIG;
 }
 
+// K4 on caller logits (tests): n_rows == 1 with children -> argmax + first matching
+// child (argmax_match_kernel); otherwise the per-row first argmax (fp32 only).
+extern "C" int tp_debug_argmax(int32_t device, const void* logits_dev, int32_t is_f64, int32_t vocab, int32_t n_rows,
+                               const int32_t* children_host, int32_t n_children, int32_t* out_host) {
+  TP_CUDA(cudaSetDevice(device));
+  TP_CHECK(logits_dev && out_host && vocab >= 1 && n_rows >= 1, TP_ECONFIG, "bad argmax arguments");
+  int32_t* d = nullptr;
+  const size_t words = (size_t)std::max(n_rows, 2) + (size_t)std::max(n_children, 0);
+  TP_CUDA(cudaMalloc(&d, words * 4));
+  int rc = TP_OK;
+  if (children_host && n_rows == 1) {
+    int32_t* dch = d + 2;
+    if (n_children > 0) TP_CUDA(cudaMemcpy(dch, children_host, (size_t)n_children * 4, cudaMemcpyHostToDevice));
+    rc = tp::argmax_match(logits_dev, is_f64, vocab, dch, n_children, d, 0);
+    if (rc == TP_OK) TP_CUDA(cudaMemcpy(out_host, d, 8, cudaMemcpyDeviceToHost));
+  } else {
+    TP_CHECK(!is_f64, TP_ECONFIG, "per-row argmax is fp32");
+    rc = tp::argmax_rows(logits_dev, vocab, n_rows, d, 0);
+    if (rc == TP_OK) TP_CUDA(cudaMemcpy(out_host, d, (size_t)n_rows * 4, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(d);
+  return rc;
+}
+
 extern "C" int tp_timeline_enable(int32_t on) {
   tp::g_tl_on = on != 0;
   return TP_OK;

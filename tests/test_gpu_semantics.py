@@ -123,3 +123,53 @@ def test_llama_stalls_lossless():
                  collect_trace=False)
     assert res.tokens == want
     assert res.metrics.stalls > 0
+
+
+@pytest.mark.gpu
+def test_k4_argmax_first_max_nan_and_child_match():
+    """K4 semantics on crafted logits, against numpy (the reference's greedy_token
+    is np.argmax: first maximum, a NaN counts as the maximum and the first NaN
+    wins; the matched child is the first level-1 node with that token,
+    `pipeline.py:333-339`): ties, NaN, duplicate child tokens, >1024 children,
+    vocab sizes that are not multiples of the block, and the per-row kernel."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2504_04104_b200 import _lib
+
+    lib = _lib.lib()
+    rng = np.random.default_rng(7)
+
+    def match(lg, children):
+        t = torch.from_numpy(lg).cuda()
+        out = np.zeros(2, dtype=np.int32)
+        ch = np.asarray(children, dtype=np.int32)
+        _lib.check(lib.tp_debug_argmax(0, C.c_void_p(t.data_ptr()), int(lg.dtype == np.float64), lg.size, 1,
+                                       ch.ctypes.data, ch.size, out.ctypes.data))
+        return int(out[0]), int(out[1])
+
+    for vocab in (1, 7, 1000, 32000, 50257):
+        for dtype in (np.float32, np.float64):
+            lg = rng.standard_normal(vocab).astype(dtype)
+            if vocab > 10:
+                lg[vocab // 3] = lg[vocab // 2] = lg[-1] = lg.max() + 1  # three-way tie: lowest id wins
+            ref = int(np.argmax(lg))
+            kids = [int(x) for x in rng.integers(0, vocab, 20)] + [ref, ref]  # duplicates: first one wins
+            tok, child = match(lg, kids)
+            assert tok == ref, (vocab, dtype)
+            assert child == kids.index(ref)
+            assert match(lg, [t for t in kids if t != ref])[1] == -1
+    lg = rng.standard_normal(5000).astype(np.float32)
+    lg[123] = np.nan
+    lg[77] = np.nan
+    assert match(lg, [3, 77])[0] == int(np.argmax(lg)) == 77
+    many = [int(x) for x in rng.permutation(5000)[:2000]]  # > 1024 children: the strided match loop
+    lg = rng.standard_normal(5000).astype(np.float32)
+    assert match(lg, many) == (int(np.argmax(lg)), many.index(int(np.argmax(lg))) if int(np.argmax(lg)) in many else -1)
+    rows = rng.standard_normal((9, 32000)).astype(np.float32)
+    rows[4, 10] = rows[4, 20] = rows[4].max() + 2
+    t = torch.from_numpy(rows).cuda()
+    out = np.zeros(9, dtype=np.int32)
+    _lib.check(lib.tp_debug_argmax(0, C.c_void_p(t.data_ptr()), 0, 32000, 9, None, 0, out.ctypes.data))
+    assert out.tolist() == [int(np.argmax(r)) for r in rows]

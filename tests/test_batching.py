@@ -70,15 +70,17 @@ def test_sequential_decode_batch_equals_solo():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("stages,max_batch", [(4, 3), (2, 5)])
+@pytest.mark.parametrize("stages,max_batch", [(4, 3), (2, 5), (8, 12)])
 def test_llama_combined_tick_equals_solo(stages, max_batch):
     """The combined ragged step (one launch sequence per tick for all requests)
-    emits each request's own greedy continuation, identical to uncombined stepping."""
-    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=4, heads=2, kv_heads=1, ffn=512)
+    emits each request's own greedy continuation, identical to uncombined stepping.
+    (8, 12): 96 caches per tick, so the deferred KV pruning and row filters of a
+    tick exceed one 64-set launch and are split."""
+    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=max(4, stages), heads=2, kv_heads=1, ffn=512)
     m = tp.LlamaModel(cfg, max_nodes=64)
     rng = np.random.default_rng(11)
     reqs = [tp.Request(i, int(rng.integers(0, 3)), tuple(int(t) for t in rng.integers(0, 512, 9 + 7 * i)), 10)
-            for i in range(6)]
+            for i in range(max(6, max_batch))]
     refs = dict(enumerate(tp.sequential_decode_batch(m, [list(r.prompt) for r in reqs], 10)))
     out = {}
     for combined in (True, False):

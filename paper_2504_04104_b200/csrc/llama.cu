@@ -137,6 +137,21 @@ struct RowCopyGroup {
   float* dst[kMaxBatchItems];
   int rows[kMaxBatchItems];
 };
+// token rows of several items -> their residual-stream rows (fp32), one launch
+struct EmbedGroup {
+  const int32_t* tok[kMaxBatchItems];
+  float* out[kMaxBatchItems];
+  int n[kMaxBatchItems];
+};
+__global__ void embed_group_kernel(const __nv_bfloat16* __restrict__ E, const __grid_constant__ EmbedGroup g, int d) {
+  pdl_wait();
+  pdl_trigger();
+  const int k = blockIdx.y, c = blockIdx.x;
+  if (c >= g.n[k]) return;
+  const __nv_bfloat16* e = E + (size_t)g.tok[k][c] * d;
+  float* x = g.out[k] + (size_t)c * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) x[j] = __bfloat162float(e[j]);
+}
 // hidden rows handed over from the previous stage -> the member's residual stream
 __global__ void copy_rows_kernel(const __grid_constant__ RowCopyGroup G, int d) {
   pdl_wait();
@@ -446,6 +461,12 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     int rows;
   };
   std::vector<Copy> copies;
+  struct Embed {
+    const int32_t* tok;
+    float* out;
+    int n;
+  };
+  std::vector<Embed> embeds;
   int ntot[kMaxGroup], lo[kMaxGroup], hi[kMaxGroup];
   int slots = 0;
   for (int g = 0; g < count; ++g) {
@@ -472,10 +493,23 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       if (it.hin) {
         if (it.hin != x) copies.push_back({(const float*)it.hin, x, it.lv.n});
       } else {
-        TP_TRY(llama_embed(m0, it.lv.n, it.lv.tokens, x, st));
+        TP_CHECK(m0->embed, TP_ECONFIG, "model has no embedding table");
+        embeds.push_back({it.lv.tokens, x, it.lv.n});
       }
     }
     slots = std::max(slots, hi[g] - lo[g]);
+  }
+  for (size_t c0 = 0; c0 < embeds.size(); c0 += kMaxBatchItems) {  // every item's token embedding, one launch
+    EmbedGroup eg;
+    int mr = 0, cnt = (int)std::min<size_t>(kMaxBatchItems, embeds.size() - c0);
+    for (int k = 0; k < cnt; ++k) {
+      eg.tok[k] = embeds[c0 + k].tok;
+      eg.out[k] = embeds[c0 + k].out;
+      eg.n[k] = embeds[c0 + k].n;
+      mr = std::max(mr, eg.n[k]);
+    }
+    ::tp::count_launch();
+    TP_CUDA(launch_pdl(embed_group_kernel, dim3(mr, cnt), dim3(256), 0, st, (const __nv_bfloat16*)m0->embed, eg, d));
   }
   for (size_t c0 = 0; c0 < copies.size(); c0 += kMaxBatchItems) {
     RowCopyGroup cg;

@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="13b")
 ap.add_argument("--batch", type=int, default=16)
 ap.add_argument("--ticks", type=int, default=20)
+ap.add_argument("--ncu-window", type=int, default=0, help="only run N ticks between cudaProfilerStart/Stop, then exit")
 args = ap.parse_args()
 cfg = model_cfg(args.model)
 m = LlamaModel(cfg, max_nodes=64)
@@ -39,6 +40,14 @@ sched.queue.sort(key=lambda r: (r.arrival_tick, r.request_id))
 for _ in range(6):
     sched.tick()
 torch.cuda.synchronize()
+if args.ncu_window:
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    for _ in range(args.ncu_window):
+        sched.tick()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    sys.exit(0)
 walls, gpus = [], []
 for _ in range(args.ticks):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -345,3 +345,39 @@ def test_gqa_attention_paths():
     res = tp.run(m, tp.PipelineConfig(num_stages=2), tp.BeamConfig(w=8, k=4), draft, prompt[:30], 16,
                  collect_trace=False)
     assert res.tokens == want
+
+
+@pytest.mark.gpu
+def test_sharded_models_pipeline_lossless():
+    """The `bench.py --gpus N` placement emulated on one GPU: per-stage shard model
+    objects (layer ranges, embedding only on the first, head only on the last,
+    LCG jump-ahead to their layers) driven as one pipeline, grouped per shard;
+    tokens equal the single model's greedy decode and the staged oracle."""
+    from paper_2504_04104_b200.pipeline import PipelineRunner, sequential_decode_staged, split_layers
+
+    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=6, heads=2, kv_heads=1, ffn=512)
+    full = tp.LlamaModel(cfg, max_nodes=64)
+    stages = 6
+    splits = split_layers(cfg.layers, stages)
+    owner = [0, 0, 0, 1, 1, 1]  # two shards of three stages each
+    shards = {}
+    for o in sorted(set(owner)):
+        mine = [splits[s] for s in range(stages) if owner[s] == o]
+        lo, hi = mine[0][0], mine[-1][1]
+        shards[o] = tp.LlamaModel(cfg, max_nodes=64, layer_range=(lo, hi), with_embed=lo == 0,
+                                  with_head=hi == cfg.layers)
+    per_stage = [shards[owner[s]] for s in range(stages)]
+    prompt = [int(t) for t in np.random.default_rng(13).integers(0, cfg.vocab, 60)]
+    ref = tp.sequential_decode(full, prompt, 30)
+    assert sequential_decode_staged(per_stage, splits, prompt, 30) == ref
+    for grouped in (True, False):
+        draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.7, rank_decay=0.5, miss_prob=0.05, seed=4),
+                                  cfg.vocab)
+        draft.bind_reference(tuple(prompt) + tuple(ref))
+        r = PipelineRunner(per_stage, tp.PipelineConfig(num_stages=stages, layer_splits=tuple(splits)),
+                           tp.BeamConfig(w=8, k=4), draft, collect_trace=False, grouped=grouped)
+        r.prefill(prompt)
+        while len(r.emitted) < 20:
+            r.decode_step()
+        assert r.emitted[:20] == ref[:20], grouped
+        r.close()

@@ -118,18 +118,6 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __re
   }
 }
 
-// cos/sin of every (node position, rotary pair) for the QKV epilogue; angle in fp64.
-__global__ void rope_table_kernel(const int32_t* __restrict__ pos, double theta, float* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  const int c = blockIdx.x, i = threadIdx.x;  // i in [0, 64)
-  const double inv = pow(theta, -2.0 * (double)i / 128.0);
-  double sn, cs;
-  sincos((double)pos[c] * inv, &sn, &cs);
-  out[((size_t)c * 64 + i) * 2] = (float)cs;
-  out[((size_t)c * 64 + i) * 2 + 1] = (float)sn;
-}
-
 // Batched per-item helpers of a forward call (one launch each instead of one per item).
 constexpr int kMaxBatchItems = 64;
 struct RowCopyGroup {
@@ -143,41 +131,53 @@ struct EmbedGroup {
   float* out[kMaxBatchItems];
   int n[kMaxBatchItems];
 };
-__global__ void embed_group_kernel(const __nv_bfloat16* __restrict__ E, const __grid_constant__ EmbedGroup g, int d) {
-  pdl_wait();
-  pdl_trigger();
-  const int k = blockIdx.y, c = blockIdx.x;
-  if (c >= g.n[k]) return;
-  const __nv_bfloat16* e = E + (size_t)g.tok[k][c] * d;
-  float* x = g.out[k] + (size_t)c * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) x[j] = __bfloat162float(e[j]);
-}
 // hidden rows handed over from the previous stage -> the member's residual stream
-__global__ void copy_rows_kernel(const __grid_constant__ RowCopyGroup G, int d) {
-  pdl_wait();
-  pdl_trigger();
-  const int it = blockIdx.y, r = blockIdx.x;
-  if (r >= G.rows[it]) return;
-  const float4* s = reinterpret_cast<const float4*>(G.src[it] + (size_t)r * d);
-  float4* o = reinterpret_cast<float4*>(G.dst[it] + (size_t)r * d);
-  for (int j = threadIdx.x; j < d / 4; j += blockDim.x) o[j] = s[j];
-}
 
 struct RopeGroup {
   const int32_t* pos[kMaxBatchItems];
   float* out[kMaxBatchItems];
   int n[kMaxBatchItems];
 };
-__global__ void rope_group_kernel(const __grid_constant__ RopeGroup G, double theta) {
+
+// The prep of a forward call as ONE launch (each a separate grid before: every
+// launch in the PDL chain costs a grid-completion hop): blockIdx.y selects an
+// embedding item, a hidden-row copy item or a RoPE-table item; the per-task
+// arithmetic of each task is unchanged (bf16 -> fp32 row, float4 row copy, f64 RoPE angles).
+struct PrepGroup {
+  EmbedGroup e;
+  RowCopyGroup c;
+  RopeGroup r;
+  int ne, nc, nr;
+};
+__global__ void __launch_bounds__(256) prep_group_kernel(const __nv_bfloat16* __restrict__ E,
+                                                         const __grid_constant__ PrepGroup P, int d, double theta) {
   pdl_wait();
   pdl_trigger();
-  const int it = blockIdx.y, c = blockIdx.x, i = threadIdx.x;  // i in [0, 64)
-  if (c >= G.n[it]) return;
+  int y = blockIdx.y;
+  const int x = blockIdx.x;
+  if (y < P.ne) {
+    if (x >= P.e.n[y]) return;
+    const __nv_bfloat16* e = E + (size_t)P.e.tok[y][x] * d;
+    float* o = P.e.out[y] + (size_t)x * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) o[j] = __bfloat162float(e[j]);
+    return;
+  }
+  y -= P.ne;
+  if (y < P.nc) {
+    if (x >= P.c.rows[y]) return;
+    const float4* s = reinterpret_cast<const float4*>(P.c.src[y] + (size_t)x * d);
+    float4* o = reinterpret_cast<float4*>(P.c.dst[y] + (size_t)x * d);
+    for (int j = threadIdx.x; j < d / 4; j += blockDim.x) o[j] = s[j];
+    return;
+  }
+  y -= P.nc;
+  const int i = threadIdx.x;
+  if (x >= P.r.n[y] || i >= 64) return;
   const double inv = pow(theta, -2.0 * (double)i / 128.0);
   double sn, cs;
-  sincos((double)G.pos[it][c] * inv, &sn, &cs);
-  G.out[it][((size_t)c * 64 + i) * 2] = (float)cs;
-  G.out[it][((size_t)c * 64 + i) * 2 + 1] = (float)sn;
+  sincos((double)P.r.pos[y][x] * inv, &sn, &cs);
+  P.r.out[y][((size_t)x * 64 + i) * 2] = (float)cs;
+  P.r.out[y][((size_t)x * 64 + i) * 2 + 1] = (float)sn;
 }
 
 // ---- host ---------------------------------------------------------------------------
@@ -499,57 +499,57 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     }
     slots = std::max(slots, hi[g] - lo[g]);
   }
-  for (size_t c0 = 0; c0 < embeds.size(); c0 += kMaxBatchItems) {  // every item's token embedding, one launch
-    EmbedGroup eg;
-    int mr = 0, cnt = (int)std::min<size_t>(kMaxBatchItems, embeds.size() - c0);
-    for (int k = 0; k < cnt; ++k) {
-      eg.tok[k] = embeds[c0 + k].tok;
-      eg.out[k] = embeds[c0 + k].out;
-      eg.n[k] = embeds[c0 + k].n;
-      mr = std::max(mr, eg.n[k]);
+  {  // embeddings, hidden-row copies and RoPE tables of every item: one launch per 64 of each kind
+    struct Rope {
+      const int32_t* pos;
+      float* out;
+      int n;
+    };
+    std::vector<Rope> ropes;
+    for (int g = 0; g < count && slots > 0; ++g) {
+      if (hi[g] == lo[g]) continue;
+      for (int r = 0; r < mem[g].count; ++r) {
+        const FwdItem& it = mem[g].items[r];
+        ropes.push_back({it.lv.positions, ws[g]->rope + (size_t)offs[g][r] * 128, it.lv.n});
+      }
     }
-    ::tp::count_launch();
-    TP_CUDA(launch_pdl(embed_group_kernel, dim3(mr, cnt), dim3(256), 0, st, (const __nv_bfloat16*)m0->embed, eg, d));
-  }
-  for (size_t c0 = 0; c0 < copies.size(); c0 += kMaxBatchItems) {
-    RowCopyGroup cg;
-    int mr = 0, cnt = (int)std::min<size_t>(kMaxBatchItems, copies.size() - c0);
-    for (int k = 0; k < cnt; ++k) {
-      cg.src[k] = copies[c0 + k].src;
-      cg.dst[k] = copies[c0 + k].dst;
-      cg.rows[k] = copies[c0 + k].rows;
-      mr = std::max(mr, cg.rows[k]);
+    size_t ie = 0, ic = 0, ir = 0;
+    while (ie < embeds.size() || ic < copies.size() || ir < ropes.size()) {
+      PrepGroup P;
+      P.ne = (int)std::min<size_t>(kMaxBatchItems, embeds.size() - ie);
+      P.nc = (int)std::min<size_t>(kMaxBatchItems, copies.size() - ic);
+      P.nr = (int)std::min<size_t>(kMaxBatchItems, ropes.size() - ir);
+      int mx = 1;
+      for (int k = 0; k < P.ne; ++k) {
+        P.e.tok[k] = embeds[ie + k].tok;
+        P.e.out[k] = embeds[ie + k].out;
+        P.e.n[k] = embeds[ie + k].n;
+        mx = std::max(mx, P.e.n[k]);
+      }
+      for (int k = 0; k < P.nc; ++k) {
+        P.c.src[k] = copies[ic + k].src;
+        P.c.dst[k] = copies[ic + k].dst;
+        P.c.rows[k] = copies[ic + k].rows;
+        mx = std::max(mx, P.c.rows[k]);
+      }
+      for (int k = 0; k < P.nr; ++k) {
+        P.r.pos[k] = ropes[ir + k].pos;
+        P.r.out[k] = ropes[ir + k].out;
+        P.r.n[k] = ropes[ir + k].n;
+        mx = std::max(mx, P.r.n[k]);
+      }
+      ::tp::count_launch();
+      TP_CUDA(launch_pdl(prep_group_kernel, dim3(mx, P.ne + P.nc + P.nr), dim3(256), 0, st,
+                         (const __nv_bfloat16*)m0->embed, P, d, (double)c.rope_theta));
+      ie += P.ne;
+      ic += P.nc;
+      ir += P.nr;
     }
-    ::tp::count_launch();
-    TP_CUDA(launch_pdl(copy_rows_kernel, dim3(mr, cnt), dim3(256), 0, st, cg, d));
   }
   if (slots == 0) return TP_OK;
   // per-request KV destinations of ragged members (one small upload each)
   const QkvItem* qitems[kMaxGroup] = {nullptr};
   const int32_t* qnode[kMaxGroup] = {nullptr};
-  {  // RoPE tables of every item, one launch
-    RopeGroup rg;
-    int cnt = 0, mn = 0;
-    auto flush = [&]() -> int {
-      if (!cnt) return TP_OK;
-      ::tp::count_launch();
-      TP_CUDA(launch_pdl(rope_group_kernel, dim3(mn, cnt), dim3(64), 0, st, rg, (double)c.rope_theta));
-      cnt = mn = 0;
-      return TP_OK;
-    };
-    for (int g = 0; g < count; ++g) {
-      if (hi[g] == lo[g]) continue;
-      for (int r = 0; r < mem[g].count; ++r) {
-        const FwdItem& it = mem[g].items[r];
-        rg.pos[cnt] = it.lv.positions;
-        rg.out[cnt] = ws[g]->rope + (size_t)offs[g][r] * 128;
-        rg.n[cnt] = it.lv.n;
-        mn = std::max(mn, it.lv.n);
-        if (++cnt == kMaxBatchItems) TP_TRY(flush());
-      }
-    }
-    TP_TRY(flush());
-  }
   for (int g = 0; g < count; ++g) {
     const FwdMember& M = mem[g];
     if (hi[g] == lo[g]) continue;

@@ -89,6 +89,28 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
+// RMSNorm of one row held as v[u] = x[threadIdx.x + u * kNormThreads] (1024 threads):
+// the single definition of its arithmetic (rmsnorm_group_kernel and the fused
+// first-layer norm of prep_group_kernel), so a row's bits do not depend on which
+// kernel normalised it.
+constexpr int kNormPerRow = 8;  // d <= 8192
+__device__ __forceinline__ void norm_row(const float (&v)[kNormPerRow], int d, float eps, __nv_bfloat16* out,
+                                         float* red) {
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kNormPerRow; ++u) {
+    const int j = threadIdx.x + u * 1024;
+    if (j < d) ss += v[u] * v[u];
+  }
+  ss = block_sum(ss, red);
+  const float r = 1.0f / sqrtf(ss / (float)d + eps);
+#pragma unroll
+  for (int u = 0; u < kNormPerRow; ++u) {
+    const int j = threadIdx.x + u * 1024;
+    if (j < d) out[j] = __float2bfloat16_rn(v[u] * r);
+  }
+}
+
 // Xd[c] = bf16(x[c] * 1/sqrt(mean(x[c]^2) + eps)); one CTA per node row, the
 // same reduction shape at every call site (stage boundaries included).
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
@@ -123,12 +145,14 @@ constexpr int kMaxBatchItems = 64;
 struct RowCopyGroup {
   const float* src[kMaxBatchItems];
   float* dst[kMaxBatchItems];
+  __nv_bfloat16* xd[kMaxBatchItems];  // the first layer's RMSNorm output (nullptr: none)
   int rows[kMaxBatchItems];
 };
 // token rows of several items -> their residual-stream rows (fp32), one launch
 struct EmbedGroup {
   const int32_t* tok[kMaxBatchItems];
   float* out[kMaxBatchItems];
+  __nv_bfloat16* xd[kMaxBatchItems];  // the first layer's RMSNorm output (nullptr: none)
   int n[kMaxBatchItems];
 };
 // hidden rows handed over from the previous stage -> the member's residual stream
@@ -149,28 +173,45 @@ struct PrepGroup {
   RopeGroup r;
   int ne, nc, nr;
 };
-__global__ void __launch_bounds__(256) prep_group_kernel(const __nv_bfloat16* __restrict__ E,
-                                                         const __grid_constant__ PrepGroup P, int d, double theta) {
+__global__ void __launch_bounds__(1024) prep_group_kernel(const __nv_bfloat16* __restrict__ E,
+                                                          const __grid_constant__ PrepGroup P, int d, double theta,
+                                                          float eps) {
   pdl_wait();
   pdl_trigger();
+  __shared__ float red[33];
   int y = blockIdx.y;
   const int x = blockIdx.x;
-  if (y < P.ne) {
-    if (x >= P.e.n[y]) return;
-    const __nv_bfloat16* e = E + (size_t)P.e.tok[y][x] * d;
-    float* o = P.e.out[y] + (size_t)x * d;
-    for (int j = threadIdx.x; j < d; j += blockDim.x) o[j] = __bfloat162float(e[j]);
+  if (y < P.ne + P.nc) {  // one residual-stream row (+ its first-layer RMSNorm)
+    const bool emb = y < P.ne;
+    const int k = emb ? y : y - P.ne;
+    if (x >= (emb ? P.e.n[k] : P.c.rows[k])) return;
+    float* o = (emb ? P.e.out[k] : P.c.dst[k]) + (size_t)x * d;
+    __nv_bfloat16* xd = emb ? P.e.xd[k] : P.c.xd[k];
+    float v[kNormPerRow];
+    if (emb) {
+      const __nv_bfloat16* e = E + (size_t)P.e.tok[k][x] * d;
+#pragma unroll
+      for (int u = 0; u < kNormPerRow; ++u) {
+        const int j = threadIdx.x + u * 1024;
+        v[u] = j < d ? __bfloat162float(e[j]) : 0.f;
+      }
+    } else {
+      const float* src = P.c.src[k] + (size_t)x * d;
+#pragma unroll
+      for (int u = 0; u < kNormPerRow; ++u) {
+        const int j = threadIdx.x + u * 1024;
+        v[u] = j < d ? src[j] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kNormPerRow; ++u) {
+      const int j = threadIdx.x + u * 1024;
+      if (j < d) o[j] = v[u];
+    }
+    if (xd) norm_row(v, d, eps, xd + (size_t)x * d, red);
     return;
   }
-  y -= P.ne;
-  if (y < P.nc) {
-    if (x >= P.c.rows[y]) return;
-    const float4* s = reinterpret_cast<const float4*>(P.c.src[y] + (size_t)x * d);
-    float4* o = reinterpret_cast<float4*>(P.c.dst[y] + (size_t)x * d);
-    for (int j = threadIdx.x; j < d / 4; j += blockDim.x) o[j] = s[j];
-    return;
-  }
-  y -= P.nc;
+  y -= P.ne + P.nc;
   const int i = threadIdx.x;
   if (x >= P.r.n[y] || i >= 64) return;
   const double inv = pow(theta, -2.0 * (double)i / 128.0);
@@ -404,26 +445,13 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __gri
   if ((int)blockIdx.x >= ng.n[g]) return;
   __shared__ float red[33];
   const float* xr = ng.x[g] + (size_t)blockIdx.x * d;
-  float v[kNormPer];
-  float ss = 0.f;
+  float v[kNormPerRow];
 #pragma unroll
-  for (int u = 0; u < kNormPer; ++u) {
+  for (int u = 0; u < kNormPerRow; ++u) {
     const int j = threadIdx.x + u * kNormThreads;
     v[u] = j < d ? xr[j] : 0.f;
   }
-#pragma unroll
-  for (int u = 0; u < kNormPer; ++u) {
-    const int j = threadIdx.x + u * kNormThreads;
-    if (j < d) ss += v[u] * v[u];
-  }
-  ss = block_sum(ss, red);
-  const float r = 1.0f / sqrtf(ss / (float)d + eps);
-  __nv_bfloat16* out = ng.xd[g] + (size_t)blockIdx.x * d;
-#pragma unroll
-  for (int u = 0; u < kNormPer; ++u) {
-    const int j = threadIdx.x + u * kNormThreads;
-    if (j < d) out[j] = __float2bfloat16_rn(v[u] * r);
-  }
+  norm_row(v, d, eps, ng.xd[g] + (size_t)blockIdx.x * d, red);
 }
 
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
@@ -458,12 +486,14 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
   struct Copy {
     const float* src;
     float* dst;
+    __nv_bfloat16* xd;
     int rows;
   };
   std::vector<Copy> copies;
   struct Embed {
     const int32_t* tok;
     float* out;
+    __nv_bfloat16* xd;
     int n;
   };
   std::vector<Embed> embeds;
@@ -490,11 +520,14 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     for (int r = 0; r < M.count; ++r) {
       const FwdItem& it = M.items[r];
       float* x = M.x + (size_t)offs[g][r] * d;
+      // the first layer's RMSNorm is fused into the prep launch (rows in place are
+      // "copied" onto themselves so that every row of a member with layers gets it)
+      __nv_bfloat16* xd = hi[g] > lo[g] ? ws[g]->Xd + (size_t)offs[g][r] * d : nullptr;
       if (it.hin) {
-        if (it.hin != x) copies.push_back({(const float*)it.hin, x, it.lv.n});
+        if (it.hin != x || xd) copies.push_back({(const float*)it.hin, x, xd, it.lv.n});
       } else {
         TP_CHECK(m0->embed, TP_ECONFIG, "model has no embedding table");
-        embeds.push_back({it.lv.tokens, x, it.lv.n});
+        embeds.push_back({it.lv.tokens, x, xd, it.lv.n});
       }
     }
     slots = std::max(slots, hi[g] - lo[g]);
@@ -523,12 +556,14 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       for (int k = 0; k < P.ne; ++k) {
         P.e.tok[k] = embeds[ie + k].tok;
         P.e.out[k] = embeds[ie + k].out;
+        P.e.xd[k] = embeds[ie + k].xd;
         P.e.n[k] = embeds[ie + k].n;
         mx = std::max(mx, P.e.n[k]);
       }
       for (int k = 0; k < P.nc; ++k) {
         P.c.src[k] = copies[ic + k].src;
         P.c.dst[k] = copies[ic + k].dst;
+        P.c.xd[k] = copies[ic + k].xd;
         P.c.rows[k] = copies[ic + k].rows;
         mx = std::max(mx, P.c.rows[k]);
       }
@@ -539,8 +574,8 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
         mx = std::max(mx, P.r.n[k]);
       }
       ::tp::count_launch();
-      TP_CUDA(launch_pdl(prep_group_kernel, dim3(mx, P.ne + P.nc + P.nr), dim3(256), 0, st,
-                         (const __nv_bfloat16*)m0->embed, P, d, (double)c.rope_theta));
+      TP_CUDA(launch_pdl(prep_group_kernel, dim3(mx, P.ne + P.nc + P.nr), dim3(1024), 0, st,
+                         (const __nv_bfloat16*)m0->embed, P, d, (double)c.rope_theta, c.norm_eps));
       ie += P.ne;
       ic += P.nc;
       ir += P.nr;
@@ -660,11 +695,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       }
     }
     gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
-    if (j == 0 && !(g_dbg_skip & 2)) {
-      ::tp::count_launch();
-      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
-      TP_CUDA(cudaGetLastError());
-    }
+    // (slot 0's input RMSNorm ran inside the prep launch)
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gq, pqkv, st));
     timeline_mark("gemm_qkv", st);
     for (size_t a0 = 0; a0 < aa.size() && !(g_dbg_skip & 1); a0 += kAttnMaxGroup) {

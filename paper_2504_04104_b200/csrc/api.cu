@@ -11,6 +11,7 @@
 #include "internal.h"
 
 #include <atomic>
+#include <cstdlib>
 
 namespace tp {
 static thread_local std::string g_err;
@@ -684,8 +685,12 @@ struct CallRing {
   char* host = nullptr;
   char* dev = nullptr;
   size_t slot_bytes = 0;
-  cudaEvent_t ev[kSlots] = {nullptr};
-  int next = 0;
+  cudaEvent_t ev[kSlots] = {nullptr};    // copy of the slot complete (host buffer reusable)
+  cudaEvent_t free_[kSlots] = {nullptr}; // compute stream past the slot's readers (device buffer reusable)
+  cudaStream_t copy = nullptr;           // side copy stream (default; TP_SIDE_COPY=0 copies on the compute stream)
+  cudaStream_t last_st = nullptr;        // the compute stream of the previous call
+  int next = 0, last = -1;
+  bool side = false;
 };
 
 int call_slot(tp_model* m, size_t bytes, char** host, char** dev, int* slot) {
@@ -697,6 +702,12 @@ int call_slot(tp_model* m, size_t bytes, char** host, char** dev, int* slot) {
       TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       TP_CUDA(cudaEventRecord(e, 0));
     }
+    for (auto& e : r->free_) {
+      TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      TP_CUDA(cudaEventRecord(e, 0));
+    }
+    r->side = !(getenv("TP_SIDE_COPY") && atoi(getenv("TP_SIDE_COPY")) == 0);
+    if (r->side) TP_CUDA(cudaStreamCreateWithFlags(&r->copy, cudaStreamNonBlocking));
   }
   if (bytes > r->slot_bytes) {  // grow (rare): drain users of the old buffers first
     TP_CUDA(cudaDeviceSynchronize());
@@ -718,6 +729,23 @@ int call_slot(tp_model* m, size_t bytes, char** host, char** dev, int* slot) {
 int call_push(tp_model* m, int slot, size_t bytes, cudaStream_t st) {
   auto* r = reinterpret_cast<CallRing*>(m->call_ring);
   const size_t off = (size_t)slot * r->slot_bytes;
+  if (r->side) {
+    // Metadata copies run on a side copy stream: the compute stream only waits for
+    // this slot's copy (typically long done) instead of serialising a memcpy node
+    // behind all of its previous kernels.  The previous call's readers are all
+    // enqueued on its compute stream by now: mark that slot reusable there.
+    if (r->last >= 0) TP_CUDA(cudaEventRecord(r->free_[r->last], r->last_st));
+    r->last = slot;
+    r->last_st = st;
+    if (bytes) {
+      TP_CUDA(cudaStreamWaitEvent(r->copy, r->free_[slot], 0));  // this slot's earlier readers are done
+      TP_CUDA(cudaMemcpyAsync(r->dev + off, r->host + off, bytes, cudaMemcpyHostToDevice, r->copy));
+      count_io((long long)bytes, 0);
+    }
+    TP_CUDA(cudaEventRecord(r->ev[slot], r->copy));
+    TP_CUDA(cudaStreamWaitEvent(st, r->ev[slot], 0));
+    return TP_OK;
+  }
   if (bytes) {
     TP_CUDA(cudaMemcpyAsync(r->dev + off, r->host + off, bytes, cudaMemcpyHostToDevice, st));
     count_io((long long)bytes, 0);
@@ -733,6 +761,9 @@ void call_ring_free(tp_model* m) {
   if (r->dev) cudaFree(r->dev);
   for (auto e : r->ev)
     if (e) cudaEventDestroy(e);
+  for (auto e : r->free_)
+    if (e) cudaEventDestroy(e);
+  if (r->copy) cudaStreamDestroy(r->copy);
   delete r;
   m->call_ring = nullptr;
 }

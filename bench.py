@@ -199,12 +199,13 @@ def cpu_step_estimate(cfg, node_layers_per_step, head_per_token, prompt_len, sam
 def run_reference(args):
     cfg = model_cfg(args.model)
     # node-layers per step and steps per token of this workload as measured on the
-    # GPU arm (same synthetic draft, same tree process): 650 node-layers/step and
-    # 2.0 steps/token at 7B / 8 stages / w=64 (SURVEY §8 probe: ~169 resident nodes
-    # per step summed over stages); override with TP_NODE_LAYERS_PER_STEP /
-    # TP_STEPS_PER_TOKEN for other configs
-    nl = float(os.environ.get("TP_NODE_LAYERS_PER_STEP", 169.3 * cfg.layers / args.stages))
-    spt = float(os.environ.get("TP_STEPS_PER_TOKEN", 2.0))
+    # GPU arm over its default 512-step steady-state window (same synthetic draft,
+    # same tree process — the path is lossless, so the reference walks the same
+    # tree): 661 node-layers/step (165.3 resident nodes summed over stages) and
+    # 2.32 steps/token at 7B / 8 stages / w=64; override with
+    # TP_NODE_LAYERS_PER_STEP / TP_STEPS_PER_TOKEN for other configs
+    nl = float(os.environ.get("TP_NODE_LAYERS_PER_STEP", 165.3 * cfg.layers / args.stages))
+    spt = float(os.environ.get("TP_STEPS_PER_TOKEN", 2.32))
     cores = os.cpu_count()
     samples = []
     for _ in range(max(1, min(args.steps, 3))):

@@ -6,9 +6,9 @@ mkdir -p gpurun_out
 out=gpurun_out/config_sweep.jsonl
 : > $out
 run() { timeout 900 python bench.py --db-batches "" --no-cpu-baseline --no-comparators --no-perfect "$@" 2>>gpurun_out/config_sweep.err | tail -1 >> $out; echo "done $*: rc=$?"; }
-for st in 2 4 8; do run --model 13b --stages $st --w 64 --k 16 --steps 32 --warmup 8; done
-for w in 16 128; do run --model 13b --stages 8 --w $w --k 16 --steps 32 --warmup 8; done
-run --model 70b --stages 8 --w 64 --k 16 --prompt-len 4096 --steps 16 --warmup 4 --profile-steps 8
+for st in 2 4 8; do run --model 13b --stages $st --w 64 --k 16 --steps 256 --warmup 8; done
+for w in 16 128; do run --model 13b --stages 8 --w $w --k 16 --steps 256 --warmup 8; done
+run --model 70b --stages 8 --w 64 --k 16 --prompt-len 4096 --steps 96 --warmup 4 --profile-steps 8
 python - <<'PY'
 import json
 for line in open("gpurun_out/config_sweep.jsonl"):

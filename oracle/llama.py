@@ -19,12 +19,79 @@ over 64-slot chunks), so comparisons use a stated tolerance.
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from .lcg import uniform_stream
 from .toy import OracleKv
 
 F32 = np.float32
+
+
+class DenseKv(OracleKv):
+    """``OracleKv`` semantics (reference KvCache, `model.py:105-204`) with the
+    per-layer K/V rows held in growable dense arrays, so the batched oracle
+    forwards below can gather thousands of rows per node cheaply."""
+
+    def __init__(self, layers: int, width: int, capacity: int = 256):
+        super().__init__(layers, width)
+        self.k = [np.zeros((capacity, width), F32) for _ in range(layers)]
+        self.v = [np.zeros((capacity, width), F32) for _ in range(layers)]
+        self.filled = [0] * layers
+
+    def _grow(self, layer, rows):
+        cap = self.k[layer].shape[0]
+        if rows <= cap:
+            return
+        while cap < rows:
+            cap *= 2
+        for store in (self.k, self.v):
+            new = np.zeros((cap, self.hidden), F32)
+            new[: self.filled[layer]] = store[layer][: self.filled[layer]]
+            store[layer] = new
+
+    def put_many(self, layer, k, v):
+        n0 = self.filled[layer]
+        self._grow(layer, n0 + len(k))
+        self.k[layer][n0 : n0 + len(k)] = k
+        self.v[layer][n0 : n0 + len(v)] = v
+        self.filled[layer] = n0 + len(k)
+
+    def put(self, layer, k, v):
+        self.put_many(layer, k[None, :], v[None, :])
+
+    def _rows(self, store, rows):  # store is a dense array here
+        return store[np.asarray(rows, dtype=np.int64)] if len(rows) else np.empty((0, self.hidden), F32)
+
+    def k_rows(self, layer, rows):
+        return self._rows(self.k[layer], rows)
+
+    def v_rows(self, layer, rows):
+        return self._rows(self.v[layer], rows)
+
+    def keys(self, layer):
+        return self.k[layer][: self.filled[layer]]
+
+    def values(self, layer):
+        return self.v[layer][: self.filled[layer]]
+
+    def allowed(self, ancestors):
+        anc = np.fromiter((int(a) for a in ancestors), dtype=np.int64)
+        u = np.asarray(self.uids, dtype=np.int64)
+        return np.flatnonzero(np.asarray(self.prefix, dtype=bool) | np.isin(u, anc)).tolist()
+
+    def restrict(self, keep):
+        keep = np.asarray(keep, dtype=np.int64)
+        for layer in range(len(self.k)):
+            if self.filled[layer]:
+                self.k[layer][: keep.size] = self.k[layer][keep]
+                self.v[layer][: keep.size] = self.v[layer][keep]
+                self.filled[layer] = keep.size
+        self.uids = [self.uids[i] for i in keep]
+        self.positions = [self.positions[i] for i in keep]
+        self.prefix = [self.prefix[i] for i in keep]
 
 
 def bf16(x) -> np.ndarray:
@@ -46,12 +113,22 @@ class LlamaOracle:
         lo, hi = layer_range if layer_range is not None else (0, layers)
         self.layer_range = (lo, hi)
 
-        def mat(start, rows, cols, fan_in):
-            u = uniform_stream(seed, rows * cols, start).reshape(rows, cols)
-            scale = np.sqrt(3.0 / fan_in) / 0.1 if weight_scale else 1.0
-            return bf16((u * scale).astype(F32))
+        def mat(start, rows, cols, fan_in, scaled=True):
+            # chunked over host threads (numpy ufuncs release the GIL); every
+            # chunk is the exact stream slice [start+off, start+off+len)
+            scale = np.sqrt(3.0 / fan_in) / 0.1 if (weight_scale and scaled) else 1.0
+            out = np.empty(rows * cols, dtype=F32)
+            step = 1 << 22
 
-        self.embedding = bf16(uniform_stream(seed, vocab * d, 0).astype(F32)).reshape(vocab, d)
+            def work(off):
+                u = uniform_stream(seed, min(step, out.size - off), start + off)
+                out[off : off + u.size] = bf16((u * scale).astype(F32) if scale != 1.0 else u.astype(F32))
+
+            with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+                list(ex.map(work, range(0, out.size, step)))
+            return out.reshape(rows, cols)
+
+        self.embedding = mat(0, vocab, d, d, scaled=False)
         self.blocks = {}
         for layer in range(lo, hi):
             off = vocab * d + layer * per_layer
@@ -126,3 +203,123 @@ class LlamaOracle:
 
     def new_kv(self) -> OracleKv:
         return OracleKv(self.layers, self.kv_heads * 128)
+
+    def new_dense_kv(self, capacity: int = 256) -> DenseKv:
+        return DenseKv(self.layers, self.kv_heads * 128, capacity)
+
+    # -- batched restatement (same per-node semantics, GEMMs over a level) ----
+    def norm_rows(self, x):
+        x = x.astype(F32)
+        r = F32(1.0) / np.sqrt(np.mean(x * x, axis=1, dtype=F32) + F32(self.eps), dtype=F32)
+        return bf16(x * r[:, None])
+
+    def rope_rows(self, y, pos):
+        ang = np.asarray(pos, dtype=np.float64)[:, None] * self._inv[None, :]
+        c, s = np.cos(ang).astype(F32)[:, None, :], np.sin(ang).astype(F32)[:, None, :]
+        n = y.shape[0]
+        y = y.reshape(n, -1, 128)
+        y1, y2 = y[..., :64], y[..., 64:]
+        return np.concatenate([y1 * c - y2 * s, y2 * c + y1 * s], axis=2).reshape(n, -1)
+
+    def block_many(self, layer, x, kv: DenseKv, row_lists, append, pos):
+        """``block`` for n nodes at once.  Node i attends the stored rows
+        ``row_lists[i]`` (in that order) then its own K/V (self last), exactly
+        the per-node rule of `model.py:265-271`; with ``append`` the n new K/V
+        rows are stored first (rows len(kv)-n .. in node order)."""
+        w = self.blocks[layer]
+        n = x.shape[0]
+        h = self.norm_rows(x)
+        qb = bf16(self.rope_rows(h @ w["wq"], pos))
+        kb = bf16(self.rope_rows(h @ w["wk"], pos))
+        vb = bf16(h @ w["wv"])
+        if append:
+            kv.put_many(layer, kb, vb)
+        g = self.heads // self.kv_heads
+        scale = F32(1.0 / np.sqrt(128.0))
+        out = np.empty((n, self.heads * 128), dtype=F32)
+        for i in range(n):
+            rows = row_lists[i]
+            ks = np.concatenate([kv.k_rows(layer, rows), kb[i : i + 1]]).reshape(-1, self.kv_heads, 128)
+            vs = np.concatenate([kv.v_rows(layer, rows), vb[i : i + 1]]).reshape(-1, self.kv_heads, 128)
+            q = qb[i].reshape(self.kv_heads, g, 128)
+            sc = np.einsum("kgd,rkd->kgr", q, ks) * scale
+            p = np.exp(sc - sc.max(axis=2, keepdims=True)).astype(F32)
+            o = np.einsum("kgr,rkd->kgd", bf16(p), vs) / p.sum(axis=2, dtype=F32)[..., None]
+            out[i] = o.reshape(-1)
+        x = x + bf16(out) @ w["wo"]
+        h2 = self.norm_rows(x)
+        gg = h2 @ w["wg"]
+        u = h2 @ w["wu"]
+        a = bf16((gg / (F32(1.0) + np.exp(-gg))) * u)
+        return (x + a @ w["wd"]).astype(F32)
+
+    def causal_block(self, layer, x, kv: DenseKv, pos):
+        """Prompt block: row r0+i attends rows [0, r0+i) then self (prefill,
+        `pipeline.py:247-254`), computed as one masked attention per KV head."""
+        w = self.blocks[layer]
+        n = x.shape[0]
+        h = self.norm_rows(x)
+        qb = bf16(self.rope_rows(h @ w["wq"], pos))
+        kb = bf16(self.rope_rows(h @ w["wk"], pos))
+        vb = bf16(h @ w["wv"])
+        kv.put_many(layer, kb, vb)
+        tot = kv.filled[layer]
+        r0 = tot - n
+        K = kv.keys(layer).reshape(tot, self.kv_heads, 128)
+        V = kv.values(layer).reshape(tot, self.kv_heads, 128)
+        g = self.heads // self.kv_heads
+        scale = F32(1.0 / np.sqrt(128.0))
+        mask = np.arange(tot)[None, :] > (r0 + np.arange(n))[:, None]
+        out = np.empty((n, self.heads, 128), dtype=F32)
+        q = qb.reshape(n, self.heads, 128)
+        for hh in range(self.heads):
+            kh = hh // g
+            sc = (q[:, hh] @ K[:, kh].T) * scale
+            sc[mask] = -np.inf
+            p = np.exp(sc - sc.max(axis=1, keepdims=True)).astype(F32)
+            out[:, hh] = (bf16(p) @ V[:, kh]) / p.sum(axis=1, dtype=F32)[:, None]
+        x = x + bf16(out.reshape(n, -1)) @ w["wo"]
+        h2 = self.norm_rows(x)
+        gg = h2 @ w["wg"]
+        u = h2 @ w["wu"]
+        a = bf16((gg / (F32(1.0) + np.exp(-gg))) * u)
+        return (x + a @ w["wd"]).astype(F32)
+
+    def prefill_block(self, tokens, kv: DenseKv, start_pos=0, layer_range=None, x_in=None, chunk=512):
+        """Causal prompt forward of ``tokens`` (or rows ``x_in``) in chunks."""
+        lo, hi = layer_range if layer_range is not None else self.layer_range
+        n = len(tokens) if x_in is None else len(x_in)
+        outs = []
+        for s0 in range(0, n, chunk):
+            s1 = min(n, s0 + chunk)
+            x = (self.embedding[np.asarray(tokens[s0:s1])].astype(F32) if x_in is None
+                 else np.asarray(x_in[s0:s1], dtype=F32))
+            pos = np.arange(start_pos + s0, start_pos + s1)
+            for p in pos:
+                kv.open_row(-1, int(p), True)
+            for layer in range(lo, hi):
+                x = self.causal_block(layer, x, kv, pos)
+            outs.append(x)
+        return np.concatenate(outs)
+
+    def forward_level(self, kv: DenseKv, nodes, embeddings=None, layer_range=None, append=True):
+        """``forward_tree`` (`model.py:312-349`) for a batch of
+        (uid, token, position, ancestors) nodes, none of which is an
+        ancestor of another (a tree level): rows = prefix ∪ ancestors, in
+        cache order, then self; recompute mode drops same-position rows."""
+        lo, hi = layer_range if layer_range is not None else self.layer_range
+        rows = []
+        for uid, _tok, pos, anc in nodes:
+            r = kv.allowed(anc)
+            if not append:
+                r = [i for i in r if kv.positions[i] != pos]
+            rows.append(r)
+        x = (self.embedding[np.asarray([nd[1] for nd in nodes])].astype(F32) if embeddings is None
+             else np.asarray(embeddings, dtype=F32))
+        pos = np.asarray([nd[2] for nd in nodes])
+        if append:
+            for uid, _tok, p, _anc in nodes:
+                kv.open_row(uid, int(p), False)
+        for layer in range(lo, hi):
+            x = self.block_many(layer, x, kv, rows, append, pos)
+        return x

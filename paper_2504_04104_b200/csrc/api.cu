@@ -425,6 +425,7 @@ int tp_model_read_tensor(const tp_model* m, int32_t which, int32_t layer, void* 
 }
 
 static void stage_release(tp_stage* s);
+static constexpr size_t kStagePoolMax = 64;
 
 int tp_stage_create(tp_model* m, int32_t layer_lo, int32_t layer_hi, int32_t capacity_rows, tp_stage** out) {
   TP_CHECK(m && out, TP_ECONFIG, "null argument");
@@ -497,13 +498,23 @@ int tp_stage_destroy(tp_stage* s) {
   if (!s) return TP_OK;
   tp_model* m = s->m;
   bool release, free_model = false;
+  tp_stage* evict = nullptr;
   {
     std::lock_guard<std::mutex> lk(m->pool_mu);
     --m->live_stages;
     release = m->destroy_pending;
-    if (!release) m->stage_pool.push_back(s);  // parked: reused, or freed with the model
+    if (!release) {
+      m->stage_pool.push_back(s);  // parked: reused, or freed with the model
+      // bounded: past kStagePoolMax parked stages the oldest is really freed
+      // (one device sync, instead of memory growing with every finished request)
+      if (m->stage_pool.size() > kStagePoolMax) {
+        evict = m->stage_pool.front();
+        m->stage_pool.erase(m->stage_pool.begin());
+      }
+    }
     free_model = release && m->live_stages == 0;
   }
+  if (evict) stage_release(evict);
   if (release) stage_release(s);
   if (free_model) model_free_now(m);
   return TP_OK;

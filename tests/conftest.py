@@ -22,6 +22,18 @@ def golden():
         return json.load(fh)
 
 
+def pipeline_case(golden, idx):
+    """Recorded reference pipeline run: an index into golden.json's list, or
+    the name of a separately stored case (pipe_<name>.json)."""
+    if isinstance(idx, int):
+        return golden["pipelines"][idx]
+    with open(os.path.join(GOLDEN, f"pipe_{idx}.json")) as fh:
+        return json.load(fh)
+
+
+PIPE_CASES = [0, 1, 2, "c1_paper"]
+
+
 def golden_npz(name):
     return np.load(os.path.join(GOLDEN, name))
 

@@ -230,8 +230,20 @@ def main():
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump({"sequential": seqs, "trees": tree_fixture(), "expand": expand_fixture(),
                    "draft": draft_fixture(), "perf": perf_fixture(), "pipelines": pipes}, fh)
+    c1_paper()
+
+
+def c1_paper():
+    """C1 with the paper beam: ToyModel V=64, d=256, L=4, 2 stages,
+    w=64 / k=16, a 128-token prompt, the paper-calibrated synthetic draft."""
+    prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, 64, 128)]
+    meta, arr = pipeline_case("c1_paper", dict(vocab=64, hidden=256, layers=4, seed=0), 2, 64, 16,
+                              dict(top1_hit=0.62, rank_decay=0.6, miss_prob=0.01, seed=0), prompt, 32, 4)
+    np.savez_compressed(os.path.join(HERE, "pipe_c1_paper.npz"), **arr)
+    with open(os.path.join(HERE, "pipe_c1_paper.json"), "w") as fh:
+        json.dump(meta, fh)
     print("golden fixtures written to", HERE)
 
 
 if __name__ == "__main__":
-    main()
+    c1_paper() if "c1_paper" in sys.argv else main()

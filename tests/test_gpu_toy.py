@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import ListReplay, golden_npz
+from conftest import PIPE_CASES, ListReplay, golden_npz, pipeline_case
 from oracle.lcg import uniform_stream
 from oracle.pipeline import OracleRunner
 from oracle.toy import OracleKv, ToyOracle, forward_nodes, greedy_continuation
@@ -66,10 +66,10 @@ def test_forward_tree_vs_reference_fixture(golden):
         assert tp.sequential_decode(m, eval(prompt), 24) == want
 
 
-@pytest.mark.parametrize("idx", [0, 1, 2])
+@pytest.mark.parametrize("idx", PIPE_CASES)
 def test_pipeline_matches_reference_dump(golden, idx):
     """Tokens, hit/miss, KV keep lists and tree bytes bit-exact; stage outputs ≤1e-12."""
-    case = golden["pipelines"][idx]
+    case = pipeline_case(golden, idx)
     mc = case["model"]
     model = tp.init_model(tp.ToyModelConfig(**mc))
     runner = PipelineRunner(model, tp.PipelineConfig(num_stages=case["stages"]),

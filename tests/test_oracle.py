@@ -3,7 +3,7 @@
 import numpy as np
 import pytest
 
-from conftest import ListReplay, golden_npz
+from conftest import PIPE_CASES, ListReplay, golden_npz, pipeline_case
 from oracle.lcg import uniform_stream
 from oracle.pipeline import OracleRunner
 from oracle.toy import OracleKv, ToyOracle, forward_nodes, greedy_continuation
@@ -37,9 +37,9 @@ def test_toy_model_bit_exact(golden):
     assert np.array_equal(m.embed(5, 3), g["embed_5_3"])
 
 
-@pytest.mark.parametrize("idx", [0, 1, 2])
+@pytest.mark.parametrize("idx", PIPE_CASES)
 def test_pipeline_oracle_matches_reference_dump(golden, idx):
-    case = golden["pipelines"][idx]
+    case = pipeline_case(golden, idx)
     mc = case["model"]
     model = ToyOracle(mc["vocab"], mc["hidden"], mc["layers"], mc["seed"])
     runner = OracleRunner(model, case["stages"], case["w"], case["k"], ListReplay(case["trace"]))

@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 leg vs the unmodified reference")
     ap.add_argument("--no-comparators", action="store_true", help="skip the vanilla-PP / cuBLAS comparators")
     ap.add_argument("--no-perfect", action="store_true", help="skip the perfect-draft TBT field")
     ap.add_argument("--profile-steps", type=int, default=24)
@@ -196,30 +197,132 @@ def cpu_step_estimate(cfg, node_layers_per_step, head_per_token, prompt_len, sam
                           f"1 LM-head row, scaled to {node_layers_per_step:.0f} node-layers/step"}
 
 
+class _ControlOnlyModel:
+    """Stand-in model for a control-only run of the step machine: no compute, the
+    verified token is read from a bound continuation.  The SyntheticDraft's hit
+    pattern depends on whether its candidates contain the true next token, not on
+    the token values, so a random continuation gives the workload's schedule
+    (steps/token, resident nodes per stage) without the model's arithmetic."""
+
+    def __init__(self, layers, truth, runner_ref):
+        self.layers, self.hidden, self.truth, self._runner = layers, 1, truth, runner_ref
+
+    def embed(self, token, pos):
+        return np.zeros(1, np.float32)
+
+    def run_position(self, x, kv, rows, layer_range=None, append=True, uid=-1, pos=0, prefix=False):
+        if append:
+            kv.open_row(uid, pos, prefix)
+        return x
+
+    def greedy(self, x):
+        return int(self.truth[len(self._runner[0].verified)])
+
+
 def run_reference(args):
+    """The reference algorithm on the box's host cores (kind "port"): the step
+    machine restated in oracle/pipeline.py (`pipeline.py:272-490`) over the float32
+    Llama restatement with the reference's per-node forward_tree (one matvec chain
+    per node and layer, `model.py:250-349`), at the full 7B shape, all 32 layers.
+
+    Setup (untimed): weights from the LCG stream, a batched causal prompt prefill,
+    the greedy continuation the SyntheticDraft binds to (`pipeline.py:599-602`),
+    and the m-step pipeline fill.  Timed: min(K, 2) whole steady-state steps
+    (10-30 s of CPU work; "steps" reports what ran).  ms/token = the measured time
+    per node-layer x the node-layers per step x the steps per token, the last two
+    measured in this process by a 512-step control-only run of the same step
+    machine and draft (no constants)."""
+    import copy
+
+    import paper_2504_04104_b200 as tp
+    from oracle.llama import LlamaOracle
+    from oracle.pipeline import OracleRunner
+
     cfg = model_cfg(args.model)
-    # node-layers per step and steps per token of this workload as measured on the
-    # GPU arm over its default 512-step steady-state window (same synthetic draft,
-    # same tree process — the path is lossless, so the reference walks the same
-    # tree): 661 node-layers/step (165.3 resident nodes summed over stages) and
-    # 2.32 steps/token at 7B / 8 stages / w=64; override with
-    # TP_NODE_LAYERS_PER_STEP / TP_STEPS_PER_TOKEN for other configs
-    nl = float(os.environ.get("TP_NODE_LAYERS_PER_STEP", 165.3 * cfg.layers / args.stages))
-    spt = float(os.environ.get("TP_STEPS_PER_TOKEN", 2.32))
     cores = os.cpu_count()
-    samples = []
-    for _ in range(max(1, min(args.steps, 3))):
-        ms, info = cpu_step_estimate(cfg, nl, 1.0, args.prompt_len)
-        samples.append(ms)
-    step_ms = float(np.median(samples))
-    value = step_ms * spt
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args), "impl": "reference",
-            "steps_per_token": spt,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": info["sample"] + f"; x {spt} steps/token"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    t_setup = time.perf_counter()
+    # schedule of this workload: control-only run of the same step machine + draft
+    rng = np.random.default_rng(1)
+    sched_steps = 512
+    truth = [int(t) for t in rng.integers(0, cfg.vocab, args.prompt_len + sched_steps + 4 * args.stages)]
+    ref_box = [None]
+    stub = _ControlOnlyModel(cfg.layers, truth, ref_box)
+    sdraft = tp.SyntheticDraft(draft_cfg(args.draft), cfg.vocab)
+    sdraft.bind_reference(tuple(truth))
+    sr = OracleRunner(stub, args.stages, args.w, args.k, sdraft)
+    ref_box[0] = sr
+    sr.prefill(truth[: args.prompt_len])
+    for _ in range(args.stages):
+        sr.decode_step()
+    t0, nl_sched = len(sr.emitted), 0
+    for _ in range(sched_steps):
+        nl_sched += sum(len(st["res"]["uids"]) * (st["range"][1] - st["range"][0])
+                        for st in sr.stages if st["res"] is not None)
+        sr.decode_step()
+    spt = sched_steps / max(1, len(sr.emitted) - t0)
+    nl_per_step = nl_sched / sched_steps
+
+    # the real port at the workload shape
+    o = LlamaOracle(cfg.vocab, cfg.hidden, cfg.layers, cfg.heads, cfg.kv_heads, cfg.ffn, seed=cfg.seed)
+    prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, args.prompt_len)]
+    timed = max(1, min(args.steps, 2))
+    warm = min(args.warmup, 1)
+    runner = OracleRunner(o, args.stages, args.w, args.k, None,
+                          new_kv=lambda: o.new_dense_kv(args.prompt_len + 64 * (args.stages + 4)))
+    runner.prefill(prompt, batched=True)
+    # greedy continuation (sequential_decode) on copies of the prefilled caches
+    n_truth = args.stages + warm + timed + args.stages + 2
+    caches = [copy.deepcopy(st["kv"]) for st in runner.stages]
+    cont = []
+    pos = len(prompt)
+    # the prefill already holds every prompt row: the last position's output is
+    # recomputed (append=False, same-position rows excluded) as the pipeline's root
+    # level does (`pipeline.py:264-266`, `model.py:335-338`)
+    xl = o.embed(prompt[-1], pos - 1)
+    for st, kv in zip(runner.stages, caches):
+        rows = [i for i in range(len(kv)) if kv.positions[i] != pos - 1]
+        xl = o.run_position(xl, kv, rows, st["range"], False, -1, pos - 1, True)
+    for _ in range(n_truth):
+        tok = o.greedy(xl)
+        cont.append(tok)
+        xl = o.embed(tok, pos)
+        for st, kv in zip(runner.stages, caches):
+            xl = o.run_position(xl, kv, list(range(len(kv))), st["range"], True, -1, pos, True)
+        pos += 1
+    del caches
+    draft = tp.SyntheticDraft(draft_cfg(args.draft), cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(cont))
+    runner.draft = draft
+    for _ in range(args.stages + warm):  # pipeline fill + warm-up
+        runner.decode_step()
+    setup_s = time.perf_counter() - t_setup
+    step_ms, nls = [], []
+    for _ in range(timed):
+        nls.append(sum(len(st["res"]["uids"]) * (st["range"][1] - st["range"][0])
+                       for st in runner.stages if st["res"] is not None))
+        ts = time.perf_counter()
+        runner.decode_step()
+        step_ms.append((time.perf_counter() - ts) * 1e3)
+    assert runner.emitted == cont[: len(runner.emitted)], "CPU port diverged from its own greedy decode"
+    t_head = time.perf_counter()
+    o.greedy(xl)
+    head_ms = (time.perf_counter() - t_head) * 1e3
+    per_nl = (sum(step_ms) - head_ms * timed) / max(1, sum(nls))
+    ms_step = per_nl * nl_per_step + head_ms
+    value = ms_step * spt
+    sample = (f"{timed} whole steady-state steps of the port ({sum(nls)} node-layers, "
+              f"{sum(step_ms) / 1e3:.1f} s), per-node float32 matvecs, {args.model} shape, all {cfg.layers} layers; "
+              f"scaled by {nl_per_step:.0f} node-layers/step and {spt:.3f} steps/token from a "
+              f"{sched_steps}-step control-only run in this process")
+    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": args.gpus, "steps": timed,
+            "warmup": warm, "ms_per_step": round(float(np.mean(step_ms)), 2), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args),
+            "impl": "reference", "steps_per_token": round(spt, 4), "node_layers_per_step": round(nl_per_step, 1),
+            "measured_steps_ms": [round(x, 1) for x in step_ms], "measured_node_layers": nls,
+            "ms_per_node_layer": round(per_nl, 3), "head_ms": round(head_ms, 2), "setup_s": round(setup_s, 1),
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -482,7 +585,61 @@ def run_ours(args, rank, world):
         line["comparators"] = comparators(args, cfg, model_arg, splits, prompt, sync_all)
     if rank == 0 and ngpu == 1 and args.db_batches:
         line["specpipe_db"] = run_db(args)
+    if rank == 0 and ngpu == 1 and not args.no_c1:
+        line["c1_vs_reference"] = c1_leg()
     print(json.dumps(line), flush=True)
+
+
+def c1_leg(tokens=32):
+    """BASELINE config 1 (the reference's own CPU demo shape): ToyModel V=64, d=256,
+    L=4 (float64), 2 stages, paper beam w=64/k=16 and CLI beam w=4/k=4, 128-token
+    prompt, SyntheticDraft paper defaults.  The UNMODIFIED reference (baseline/_ref,
+    its own PipelineRunner, numpy on this box's host cores) and this package's B200
+    path decode the same request; the decode loop (decode_step until `tokens` are
+    emitted) is timed on both, after the untimed draft binding and prefill."""
+    import importlib
+
+    import torch
+
+    import paper_2504_04104_b200 as tp
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "treepipe")):
+        return {"unavailable": "reference not installed under baseline/_ref"}
+    sys.path.insert(0, ref_dir)
+    try:
+        ref = importlib.import_module("treepipe")
+        refp = importlib.import_module("treepipe.pipeline")
+    finally:
+        sys.path.remove(ref_dir)
+    prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, 64, 128)]
+    out = {"config": "C1: ToyModel V64 d256 L4 f64, 2 stages, prompt 128", "tokens": tokens,
+           "reference_cores": os.cpu_count(), "results": []}
+    rmodel = ref.init_model(ref.ToyModelConfig(vocab=64, hidden=256, layers=4, seed=0))
+    gmodel = tp.init_model(tp.ToyModelConfig(vocab=64, hidden=256, layers=4, seed=0))
+    truth = ref.sequential_decode(rmodel, prompt, tokens + 8)
+    for w, k in ((64, 16), (4, 4)):
+        row = {"w": w, "k": k}
+        for impl, mod, model, Runner in (("reference", ref, rmodel, refp.PipelineRunner),
+                                         ("b200", tp, gmodel, tp.PipelineRunner)):
+            draft = mod.SyntheticDraft(mod.SyntheticDraftConfig(seed=0), 64)
+            draft.bind_reference(tuple(prompt) + tuple(truth))
+            r = Runner(model, mod.PipelineConfig(num_stages=2), mod.BeamConfig(w=w, k=k), draft,
+                       collect_trace=False)
+            r.prefill(prompt)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            while len(r.emitted) < tokens:
+                r.decode_step()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            row[impl] = {"ms_per_token": round(dt * 1e3 / len(r.emitted), 4), "steps": r.step_no,
+                         "steps_per_token": round(r.metrics().steps_per_token, 4)}
+            row[impl + "_tokens"] = list(r.emitted)
+        row["tokens_identical"] = row.pop("reference_tokens") == row.pop("b200_tokens")
+        row["speedup"] = round(row["reference"]["ms_per_token"] / row["b200"]["ms_per_token"], 2)
+        out["results"].append(row)
+    return out
 
 
 def comparators(args, cfg, model_arg, splits, prompt, sync_all):

@@ -225,6 +225,12 @@ int tp_debug_attn_tile(int32_t on);
  * 2 = shared-prefix tail for uniform levels on/off, 3 = diagnostic skip mask for the
  * Llama layer loop (bit 1 attention, 2 RMSNorm, 4 GEMMs; results WRONG while set). */
 int tp_debug_attn_knob(int32_t knob, int32_t value);
+/* Diagnostics: the next Llama forward call copies member 0's first-layer
+ * intermediates into dev_buf (input RMSNorm bf16 [n][d], RoPE'd queries bf16
+ * [n][q], attention out bf16 [n][q], x after the
+ * o-projection f32 [n][d], RMSNorm out bf16 [n][d], SwiGLU product bf16 [n][f],
+ * x after the down projection f32 [n][d]); one-shot.                          */
+int tp_debug_dump(void* dev_buf);
 /* GPU timeline (diagnostics): while enabled, CUDA events between kernel groups;
  * _read returns "tag=ms;..." (GPU time since the previous mark on the stream,
  * summed per tag) and resets.                                                 */

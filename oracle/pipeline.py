@@ -102,11 +102,11 @@ def split_even(layers: int, stages: int):
 
 
 class OracleRunner:
-    def __init__(self, model, num_stages, w, k, draft=None, splits=None):
+    def __init__(self, model, num_stages, w, k, draft=None, splits=None, new_kv=None):
         self.model, self.w, self.k, self.draft = model, w, k, draft
         self.splits = splits or split_even(model.layers, num_stages)
-        self.stages = [{"kv": OracleKv(model.layers, model.hidden), "res": None, "out": None,
-                        "range": r} for r in self.splits]
+        new_kv = new_kv or (lambda: OracleKv(model.layers, model.hidden))
+        self.stages = [{"kv": new_kv(), "res": None, "out": None, "range": r} for r in self.splits]
         self.tree = None
         self.verified, self.emitted = [], []
         self.pos, self.verified_uids = {}, set()
@@ -122,12 +122,21 @@ class OracleRunner:
                 "anc": [frozenset(t.uids[int(j)] for j in np.flatnonzero(t.mask[i])) for i in range(lo, hi)],
                 "emb": None, "cached": cached}
 
-    def prefill(self, prompt):
-        for p, tok in enumerate(prompt):
-            x = self.model.embed(tok, p)
+    def prefill(self, prompt, batched=False):
+        """Prompt through every stage (`pipeline.py:239-268`): one position at a
+        time as the reference, or — ``batched`` (Llama oracle, DenseKv caches) —
+        as one causal block per stage (same semantics, GEMMs; used to set up the
+        CPU timing arm, whose timed region is the decode steps)."""
+        if batched:
+            x = None
             for st in self.stages:
-                x = self.model.run_position(x, st["kv"], list(range(len(st["kv"]))), st["range"],
-                                            True, -1, p, True)
+                x = self.model.prefill_block(prompt, st["kv"], 0, st["range"], x_in=x)
+        else:
+            for p, tok in enumerate(prompt):
+                x = self.model.embed(tok, p)
+                for st in self.stages:
+                    x = self.model.run_position(x, st["kv"], list(range(len(st["kv"]))), st["range"],
+                                                True, -1, p, True)
         self.verified = list(prompt)
         self.tree = OTree.root(prompt[-1])
         self.pos[self.tree.uids[0]] = len(prompt) - 1

@@ -47,11 +47,17 @@ void timeline_mark(const char* tag, cudaStream_t st) {
 
 namespace tp {
 extern int g_dbg_skip;
+extern void* g_dbg_dump;
 }
 
 extern "C" int tp_debug_attn_tile(int32_t on) {
   // the experimental 16-node tile path was removed (measured slower); only "off" remains valid
   return on ? TP_ECONFIG : TP_OK;
+}
+
+extern "C" int tp_debug_dump(void* dev_buf) {
+  tp::g_dbg_dump = dev_buf;
+  return TP_OK;
 }
 
 extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {

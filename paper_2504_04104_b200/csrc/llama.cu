@@ -471,6 +471,12 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
 // to measure each one's marginal cost inside the PDL chain — results are WRONG
 // while set.  Bits: 1 attention, 2 RMSNorm, 4 GEMMs.
 int g_dbg_skip = 0;
+// Diagnostics only (tp_debug_dump): device buffer receiving member 0's slot-0
+// intermediates of the next forward call: Xd (input RMSNorm, bf16 n x d), Xq
+// (RoPE'd queries, bf16 n x q), Xo (attention out, bf16 n x q), x after
+// the o-projection (f32 n x d), Xd (post-attention RMSNorm, bf16 n x d),
+// Xf (SwiGLU product, bf16 n x f), x after the down projection (f32 n x d).
+void* g_dbg_dump = nullptr;
 
 int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int ws_base) {
   TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "member group size outside [1, 8]");
@@ -696,24 +702,40 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     }
     gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
     // (slot 0's input RMSNorm ran inside the prep launch)
+    char* dump = (j == 0 && g_dbg_dump) ? static_cast<char*>(g_dbg_dump) : nullptr;
+    const size_t dn = (size_t)ntot[idx[0]];
+    auto dump_cp = [&](const void* src, size_t bytes) -> int {
+      if (!dump) return TP_OK;
+      TP_CUDA(cudaMemcpyAsync(dump, src, bytes, cudaMemcpyDeviceToDevice, st));
+      dump += bytes;
+      return TP_OK;
+    };
+    TP_TRY(dump_cp(ws[idx[0]]->Xd, dn * d * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gq, pqkv, st));
     timeline_mark("gemm_qkv", st);
+    TP_TRY(dump_cp(ws[idx[0]]->Xq, dn * q * 2));
     for (size_t a0 = 0; a0 < aa.size() && !(g_dbg_skip & 1); a0 += kAttnMaxGroup) {
       const int cnt = (int)std::min<size_t>(kAttnMaxGroup, aa.size() - a0);
       TP_TRY(attn_tree_group(aa.data() + a0, al.data() + a0, cnt, st));
     }
+    TP_TRY(dump_cp(ws[idx[0]]->Xo, dn * q * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(go, po, st));
     timeline_mark("gemm_o", st);
+    TP_TRY(dump_cp(ng.x[0], dn * d * 4));
     if (!(g_dbg_skip & 2)) {
       ::tp::count_launch();
       TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
       TP_CUDA(cudaGetLastError());
     }
     timeline_mark("rmsnorm", st);
+    TP_TRY(dump_cp(ws[idx[0]]->Xd, dn * d * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(ggu, pgu, st));
     timeline_mark("gemm_gate_up", st);
+    TP_TRY(dump_cp(ws[idx[0]]->Xf, dn * f * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gdn, pdn, st));
     timeline_mark("gemm_down", st);
+    TP_TRY(dump_cp(ng.x[0], dn * d * 4));
+    if (dump) g_dbg_dump = nullptr;
     // input norm of the next slot, for the members that continue
     int nc = 0, maxc = 0;
     NormGroup nn;

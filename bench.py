@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--no-perfect", action="store_true", help="skip the perfect-draft TBT field")
     ap.add_argument("--profile-steps", type=int, default=24)
     ap.add_argument("--db-model", default="13b", choices=["7b", "13b", "70b", "tiny"])
-    ap.add_argument("--db-batches", default="1,16", help="SpecPipe-DB batch sizes (empty: skip)")
+    ap.add_argument("--db-batches", default="1,2,4,8,16,32,64", help="SpecPipe-DB batch sizes (empty: skip)")
     ap.add_argument("--db-new", type=int, default=24)
     return ap.parse_args()
 
@@ -165,7 +165,7 @@ def peaks():
 # ----------------------------------------------------------------------------- CPU arm
 
 
-def cpu_step_estimate(cfg, node_layers_per_step, head_per_token, prompt_len, sample_nodes=4):
+def cpu_step_estimate(cfg, node_layers_per_step, head_per_token, prompt_len, sample_nodes=8):
     """Time the numpy restatement on a bounded sample: `sample_nodes` tree-node
     forwards through one Llama layer (ctx = prompt_len) plus one LM-head row,
     then scale to the measured node-layer count of a step."""
@@ -715,13 +715,14 @@ def run_db(args):
 
     gc.collect()
     torch.cuda.empty_cache()
-    model = LlamaModel(model_cfg(args.db_model), max_nodes=64)
+    # max_nodes 256: admission prefill of several requests in combined 256-row forwards
+    model = LlamaModel(model_cfg(args.db_model), max_nodes=256)
     out = {"metric": "SpecPipe-DB tokens/s", "model": f"llama2-{args.db_model}-shape", "stages": 8,
            "total_width": 64, "k": 16, "prompt_len": args.prompt_len, "new_tokens": args.db_new, "results": []}
     batches = [int(x) for x in args.db_batches.split(",") if x]
     # untimed warm-up at the largest batch: workspace / stage-pool growth and first-use
     # costs otherwise land in the first measured session's steady-state ticks
-    measure_db(model, max(batches), args.prompt_len, 8)
+    measure_db(model, min(16, max(batches)), args.prompt_len, 8)
     for b in batches:
         out["results"].append(measure_db(model, b, args.prompt_len, args.db_new))
     del model

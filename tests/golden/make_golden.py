@@ -231,6 +231,34 @@ def main():
         json.dump({"sequential": seqs, "trees": tree_fixture(), "expand": expand_fixture(),
                    "draft": draft_fixture(), "perf": perf_fixture(), "pipelines": pipes}, fh)
     c1_paper()
+    artefacts()
+
+
+def artefacts():
+    """Reference-written on-disk artefacts: the checkpoint file
+    (`model.py:388-435`), the StepTrace CSV (`pipeline.py:123-152`) and the
+    RunMetrics JSON of a replayed run, plus the draft-trace JSONL
+    (`token_source.py:178-226`)."""
+    import io
+
+    model = tp.init_model(tp.ToyModelConfig(vocab=32, hidden=8, layers=2, seed=11))
+    tp_model.save_checkpoint(model, os.path.join(HERE, "ref_ckpt_v32_d8_l2_s11.bin"))
+    cfg = dict(vocab=48, hidden=8, layers=4, seed=3)
+    model = tp.init_model(tp.ToyModelConfig(**cfg))
+    prompt = [2, 4]
+    reference = tp.sequential_decode(model, prompt, 24)
+    rec = tp.RecordingDraft(tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.7, rank_decay=0.5,
+                                                                       miss_prob=0.1, seed=9), 48))
+    rec.bind_reference(tuple(prompt) + tuple(reference))
+    res = tp.run(model, tp.PipelineConfig(num_stages=3), tp.BeamConfig(w=3, k=3), rec, prompt, 24)
+    buf = io.StringIO()
+    tp.write_trace_csv(res.trace, buf)
+    with open(os.path.join(HERE, "ref_trace_m3.csv"), "w", newline="") as fh:
+        fh.write(buf.getvalue())
+    with open(os.path.join(HERE, "ref_metrics_m3.json"), "w") as fh:
+        json.dump({"model": cfg, "prompt": prompt, "stages": 3, "w": 3, "k": 3, "tokens": res.tokens,
+                   "metrics": res.metrics.to_json()}, fh)
+    tp.write_trace(rec.records, os.path.join(HERE, "ref_draft_m3.jsonl"))
 
 
 def c1_paper():
@@ -246,4 +274,9 @@ def c1_paper():
 
 
 if __name__ == "__main__":
-    c1_paper() if "c1_paper" in sys.argv else main()
+    if "c1_paper" in sys.argv:
+        c1_paper()
+    elif "artefacts" in sys.argv:
+        artefacts()
+    else:
+        main()

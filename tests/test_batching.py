@@ -93,3 +93,32 @@ def test_llama_combined_tick_equals_solo(stages, max_batch):
         for s in slots:
             assert s.runner.emitted[:10] == tp.sequential_decode(m, list(s.request.prompt), 10)
     assert out[True] == out[False]
+
+
+@pytest.mark.gpu
+def test_prefill_requests_bitwise_equal_solo_prefill():
+    """Batched admission (prefill_requests: ragged combined forwards, rows shared
+    between requests up to max_nodes per call) leaves every stage cache and the
+    root output bit-identical to each request's own PipelineRunner.prefill."""
+    import torch
+
+    from paper_2504_04104_b200.batching import prefill_requests
+    from paper_2504_04104_b200.pipeline import PipelineRunner
+
+    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=4, heads=2, kv_heads=1, ffn=512)
+    model = tp.LlamaModel(cfg, max_nodes=96)
+    rng = np.random.default_rng(6)
+    prompts = [[int(t) for t in rng.integers(0, 512, n)] for n in (7, 130, 64, 1, 201)]
+    pcfg = tp.PipelineConfig(num_stages=4)
+    beam = tp.BeamConfig(w=4, k=2)
+    together = [PipelineRunner(model, pcfg, beam, None, collect_trace=False) for _ in prompts]
+    prefill_requests(together, prompts)
+    for r, p in zip(together, prompts):
+        solo = PipelineRunner(model, pcfg, beam, None, collect_trace=False)
+        solo.prefill(p)
+        assert r.verified == solo.verified and r.tree.tokens.tolist() == solo.tree.tokens.tolist()
+        for a, b in zip(r.stages, solo.stages):
+            assert a.kv.uids == b.kv.uids and a.kv.positions == b.kv.positions
+            lo = a.layer_range[0]
+            assert np.array_equal(a.kv.keys[lo], b.kv.keys[lo]) and np.array_equal(a.kv.values[lo], b.kv.values[lo])
+    torch.cuda.synchronize()

@@ -168,6 +168,33 @@ int tp_stages_compact(int32_t count, tp_stage* const* stages, const int32_t* fir
 /* Copy K (kind 0) or V (kind 1) of one layer, rows [lo,hi), as [rows][kv_heads][head_dim]. */
 int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo, int32_t hi, void* host);
 
+/* ---- K3 driven by the device-resident verification (pipeline.py:333-400) ---
+ * Enqueued right after tp_model_verify_async, before the host knows tau: the
+ * device reads tau from the verify stage's result, finds the first level-1 child
+ * carrying it (level-1 tokens given here, BFS order), and for every stage
+ *   - compacts the K/V rows: rows < prefix_rows stay; speculative row r (tree node
+ *     tree_off + r, invariant I2) is kept iff it is an ancestor-or-self or a
+ *     descendant-or-self of the child (row | col of the tree mask); on a miss
+ *     only the root row (tree node 0, promoted) is kept;
+ *   - gathers the surviving hidden rows of its resident level (tree nodes
+ *     level_lo .. +level_n, kept iff descendant-or-self of the child) from
+ *     hidden_src to hidden_dst (hidden_src may live on a peer GPU).
+ * The stages' host row counts are then set with tp_stage_truncate once the
+ * caller has tau (the K/V data is final when the stream reaches the kernels).
+ * keep_out (optional, device int32 [2 + spec_rows + level_n]) receives the kept
+ * counts and row lists — the reference's _restrict keep lists (tests).       */
+typedef struct tp_prune_stage {
+  tp_stage* stage;
+  int32_t prefix_rows, spec_rows, tree_off;
+  int32_t level_lo, level_n;
+  const void* hidden_src;
+  void* hidden_dst;
+  int32_t* keep_out;
+} tp_prune_stage;
+int tp_prune_device(int32_t count, const tp_prune_stage* stages, const tp_stage* verify_ws,
+                    const uint64_t* tree_bits, int32_t tree_n, int32_t words, const int32_t* level1_tokens,
+                    int32_t n_level1, int64_t hidden_row_bytes, void* stream);
+
 /* ---- transmit: in-flight embedding filter (pipeline.py:379-400) ---------- */
 /* dst[j] = src[i_j] for the set bits i_0 < i_1 < ... of keep_bits (n_src rows of row_bytes). */
 int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t row_bytes, int32_t n_src,

@@ -52,9 +52,16 @@ class Item(C.Structure):
     _fields_ = [("stage", C.c_void_p), ("level", Level), ("hidden_in", C.c_void_p), ("member", C.c_int32)]
 
 
+class PruneStage(C.Structure):
+    _fields_ = [("stage", C.c_void_p), ("prefix_rows", C.c_int32), ("spec_rows", C.c_int32),
+                ("tree_off", C.c_int32), ("level_lo", C.c_int32), ("level_n", C.c_int32),
+                ("hidden_src", C.c_void_p), ("hidden_dst", C.c_void_p), ("keep_out", C.c_void_p)]
+
+
 _P = C.c_void_p
 _I = C.c_int32
 _SIGS = {
+    "tp_prune_device": (C.c_int, [_I, _P, _P, _P, _I, _I, _P, _I, C.c_int64, _P]),
     "tp_last_error": (C.c_char_p, []),
     "tp_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "tp_model_create": (C.c_int, [C.POINTER(ModelConfig), C.POINTER(_P)]),

@@ -353,6 +353,7 @@ static void model_free_now(tp_model* m) {
       if (p) cudaFree(p);
   if (!is_toy(m)) llama_model_free(m);
   call_ring_free(m);
+  if (m->prune_plan) cudaFree(m->prune_plan);
   delete m;
 }
 

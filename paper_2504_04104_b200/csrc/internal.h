@@ -1,6 +1,8 @@
 // Internal object layout shared by the C-ABI (api.cu) and the kernel files.
 #pragma once
 
+#include <algorithm>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -23,6 +25,8 @@ struct tp_model {
   // llama: tensor maps for TMA live beside the weights (filled lazily)
   void* tma_cache = nullptr;
   void* call_ring = nullptr;  // staging ring for multi-level / multi-stage calls (api.cu)
+  int32_t* prune_plan = nullptr;  // device keep lists of tp_prune_device (prune.cu)
+  size_t prune_plan_ints = 0;
   // Destroyed stages are parked here and reused by tp_stage_create (same layer
   // range, enough capacity): cudaFree / cudaFreeHost synchronise the device, and
   // a request finishing mid-stream (SpecPipe-DB) must not stall every other one.

@@ -24,17 +24,14 @@ def measure_db(model, batch, prompt_len, new_tokens, total_width=64, k=16, stage
                        new_tokens) for i in range(batch)]
     # same-kernel batched greedy decode (one token per request per forward): the
     # references the drafts bind to, and the steady-state greedy comparator
-    # (difference of a 4-token and a new_tokens decode: the prefill cancels)
-    ts = []
-    for n_new in (4, new_tokens):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        out = tp.sequential_decode_batch(model, [list(r.prompt) for r in reqs], n_new)
-        torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
-    refs = dict(enumerate(out))
-    ref_s = ts[1]
-    greedy_tps = batch * (new_tokens - 4) / max(1e-9, ts[1] - ts[0])
+    # (tokens/s of its decode loop, prefill excluded)
+    timing = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    refs = dict(enumerate(tp.sequential_decode_batch(model, [list(r.prompt) for r in reqs], new_tokens, timing)))
+    torch.cuda.synchronize()
+    ref_s = time.perf_counter() - t0
+    greedy_tps = batch * new_tokens / timing["decode_s"]
     bcfg = tp.BatchConfig(max_batch=batch, total_width=total_width, k=k, draft=tp.SyntheticDraftConfig(seed=seed),
                           check_isolation_every_tick=False)
     sched = tp.BatchScheduler(model, tp.PipelineConfig(num_stages=stages), bcfg, references=refs, combined=combined)

@@ -614,8 +614,9 @@ static int level_validate(tp_stage* s, const tp_level* L, const void* hidden_in,
     for (int w = 0; w < L->words; ++w) pc += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
     if (uniform_a == -2) uniform_a = pc;
     else if (uniform_a != pc || L->prefix_rows[i] != L->prefix_rows[0]) uniform_a = -1;
-    TP_CHECK(is_toy(m) || pc <= 64, TP_ESHAPE, "more than 64 speculative ancestors per node");
-    a_max = std::max(a_max, std::min(pc, 64));
+    // Llama attention: the node-specific ancestors live in the last 16-slot window (attn.cu)
+    TP_CHECK(is_toy(m) || pc <= 15, TP_ESHAPE, "more than 15 speculative ancestors per node");
+    (void)a_max;
     max_t = std::max(max_t, L->prefix_rows[i] + pc + 1);
     TP_CHECK(L->prefix_rows[i] >= 0 && L->prefix_rows[i] <= visible, TP_ECONTRACT, "prefix rows beyond cache");
     if (L->tokens && !hidden_in)
@@ -661,18 +662,12 @@ static void level_write(const tp_level* L, LevelDev* lv, char* h, const char* dm
   std::memcpy(h + off_pos, L->positions, 4 * (size_t)n);
   std::memcpy(h + off_pre, L->prefix_rows, 4 * (size_t)n);
   if (L->words) std::memcpy(h + off_anc, L->anc_bits, 8 * (size_t)n * L->words);
+  // per-node ancestor counts; the rows themselves are decoded from the bit-rows on
+  // the device (attn.cu ancestor_row)
   int32_t* cnt = reinterpret_cast<int32_t*>(h + off_cnt);
-  int32_t* rows = reinterpret_cast<int32_t*>(h + off_rows);
-  // ancestor rows decoded once here (the kernels would otherwise redo it per head)
   for (int i = 0; i < n; ++i) {
     int k = 0;
-    for (int w = 0; w < L->words && k < a_max; ++w) {
-      uint64_t bits = L->anc_bits[(int64_t)i * L->words + w];
-      while (bits && k < a_max) {
-        rows[(size_t)i * a_max + k++] = L->bits_base + w * 64 + __builtin_ctzll(bits);
-        bits &= bits - 1;
-      }
-    }
+    for (int w = 0; w < L->words; ++w) k += __builtin_popcountll(L->anc_bits[(int64_t)i * L->words + w]);
     cnt[i] = k;
   }
   lv->tokens = (const int32_t*)(dm + off_tok);

@@ -6,6 +6,7 @@
 namespace tp {
 
 constexpr int kAttnChunk = 64;     // logical key slots per canonical chunk
+constexpr int kAttnSuffix = 16;    // node-specific window at the end of the key sequence (> ancestors)
 constexpr int kAttnMaxExtra = 64;  // speculative ancestor rows per node
 constexpr int kAttnHeadDim = 128;
 constexpr int kAttnMaxGroup = 64;  // (request, stage) items per grouped launch (large kernel params)
@@ -32,7 +33,8 @@ struct AttnArgs {
 struct AttnMember {
   AttnArgs a;
   LevelDev lv;
-  int c_shared;    // chunks inside every node's verified prefix
+  int c_shared;    // chunks of the member's longest chunked part (slots [0, T - kAttnSuffix))
+  int max_c;       // slots of that part
   int zt;          // row blocks of the shared launch (64 rows; 16-row tiles when `small`)
   int small;       // few rows: the run's chunks in parallel across warps
   int cta_shared;  // first CTA of this member in the shared launch

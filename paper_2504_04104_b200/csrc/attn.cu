@@ -279,22 +279,30 @@ __device__ __forceinline__ void merge_scale_live(float& M, float& L, float mc, f
   }
 }
 
-// Stage K and V rows [j0, j0 + nrows) of one kv-head plane pair into a (K, V)
-// tile pair by bulk copies issued by the calling warp; rows beyond nrows of V
-// are zeroed (their P is 0, and 0 x stale bits must not be NaN).
+// Stage rows [j0, j0 + nrows) of one kv-head plane into a tile by bulk copies
+// issued by the calling warp (completion counted on `bar`); with zero_tail the
+// rows beyond nrows are zeroed (V of a partial chunk: their P is 0, and
+// 0 x stale bits must not be NaN).
+__device__ __forceinline__ void stage_rows(const __nv_bfloat16* plane, const AttnArgs& a, int kh, int j0, int nrows,
+                                           __nv_bfloat16* tile, uint64_t* bar, bool zero_tail, int lane) {
+  const __nv_bfloat16* src = plane + ((size_t)kh * a.cap + (size_t)j0) * kAttnHeadDim;
+  // the tile's previous generic-proxy reads / zero stores are ordered before these async-proxy writes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  for (int r = lane; r < nrows; r += 32) bulk_row(tile + r * kPad, src + (size_t)r * kAttnHeadDim, bar);
+  if (zero_tail) {
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (int e = nrows * 16 + lane; e < kAttnChunk * 16; e += 32)
+      *reinterpret_cast<uint4*>(tile + (e >> 4) * kPad + (e & 15) * 8) = z;
+  }
+}
+
+// K and V of one chunk into a (K, V) tile pair, one mbarrier phase.
 __device__ __forceinline__ void stage_chunk(const AttnArgs& a, int kh, int j0, int nrows, __nv_bfloat16* sK,
                                             __nv_bfloat16* sV, uint64_t* bar, int lane) {
   if (lane == 0) sm100::mbar_expect_tx(bar, (uint32_t)(2 * nrows * kRowBytes));
   __syncwarp();
-  const __nv_bfloat16* Kh = a.k + ((size_t)kh * a.cap + (size_t)j0) * kAttnHeadDim;
-  const __nv_bfloat16* Vh = a.v + ((size_t)kh * a.cap + (size_t)j0) * kAttnHeadDim;
-  for (int r = lane; r < nrows; r += 32) {
-    bulk_row(sK + r * kPad, Kh + (size_t)r * kAttnHeadDim, bar);
-    bulk_row(sV + r * kPad, Vh + (size_t)r * kAttnHeadDim, bar);
-  }
-  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-  for (int e = nrows * 16 + lane; e < kAttnChunk * 16; e += 32)
-    *reinterpret_cast<uint4*>(sV + (e >> 4) * kPad + (e & 15) * 8) = z;
+  stage_rows(a.k, a, kh, j0, nrows, sK, bar, false, lane);
+  stage_rows(a.v, a, kh, j0, nrows, sV, bar, true, lane);
 }
 
 // Few rows (<= kSmallRows (query head, node) pairs, e.g. the lone verification
@@ -315,10 +323,9 @@ __device__ __forceinline__ void chunks_small(const AttnGroup& G, int gi, int loc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
   const int nw = min(R, c_hi - r * R);
-  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)warp * 2 * kTileElems;
-  __nv_bfloat16* sV = sK + kTileElems;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)kWarps * 2 * kTileElems);
-  float* xs = reinterpret_cast<float*>(sK);  // [16][kXsLd] partial, then 16 max + 16 sum + 16 live
+  __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)warp * kTileElems;  // K, then V
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)kWarps * kTileElems);
+  float* xs = reinterpret_cast<float*>(buf);  // [16][kXsLd] partial, then 16 max + 16 sum + 16 live
   const int c = r * R + warp;
   const int ra = 16 * t + g, rb = ra + 8;
   const bool va = ra < rows, vb = rb < rows;
@@ -331,7 +338,9 @@ __device__ __forceinline__ void chunks_small(const AttnGroup& G, int gi, int loc
   if (warp < nw) {
     const int j0 = c * kAttnChunk;
     const int nrows = min(kAttnChunk, max(0, G.m[gi].max_c - j0));
-    stage_chunk(a, kh, j0, nrows, sK, sV, bars + warp, lane);
+    if (lane == 0) sm100::mbar_expect_tx(bars + warp, (uint32_t)(nrows * kRowBytes));
+    __syncwarp();
+    stage_rows(a.k, a, kh, j0, nrows, buf, bars + warp, false, lane);
     uint32_t qa[8][4];
     const __nv_bfloat16* qra = a.q + (size_t)ia * a.q_stride + ha * kAttnHeadDim;
     const __nv_bfloat16* qrb = a.q + (size_t)ib * a.q_stride + hb * kAttnHeadDim;
@@ -346,11 +355,17 @@ __device__ __forceinline__ void chunks_small(const AttnGroup& G, int gi, int loc
     sm100::mbar_wait(bars + warp, 0);
     float m[2], l[2];
     uint32_t pa[4][4];
-    chunk_scores(qa, sK, lim, a.scale, m, l, pa, lane);
+    chunk_scores(qa, buf, lim, a.scale, m, l, pa, lane);
+    __syncwarp();  // every lane is done reading K: the tile takes V
+    if (lane == 0) sm100::mbar_expect_tx(bars + warp, (uint32_t)(nrows * kRowBytes));
+    __syncwarp();
+    stage_rows(a.v, a, kh, j0, nrows, buf, bars + warp, true, lane);
+    __syncwarp();
+    sm100::mbar_wait(bars + warp, 1);
     float o0[8][4], o1[8][4];
-    chunk_pv_half<0>(pa, sV, o0, lane);
-    chunk_pv_half<1>(pa, sV, o1, lane);
-    __syncwarp();  // the K tile becomes the hand-over buffer
+    chunk_pv_half<0>(pa, buf, o0, lane);
+    chunk_pv_half<1>(pa, buf, o1, lane);
+    __syncwarp();  // the tile becomes the hand-over buffer
 #pragma unroll
     for (int nd = 0; nd < 8; ++nd) {
       *reinterpret_cast<float2*>(xs + g * kXsLd + nd * 8 + 2 * tig) = make_float2(o0[nd][0], o0[nd][1]);
@@ -376,7 +391,7 @@ __device__ __forceinline__ void chunks_small(const AttnGroup& G, int gi, int loc
   for (int d = 0; d < 16; ++d) O[d] = 0.f;
   for (int w = 0; w < nw; ++w) {
     const float* xw = reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(dsm) +
-                                                     (size_t)w * 2 * kTileElems);
+                                                     (size_t)w * kTileElems);
     float sa, sb;
     merge_scale_live(M, L, xw[16 * kXsLd + row], xw[16 * kXsLd + 16 + row], xw[16 * kXsLd + 32 + row] != 0.f, sa,
                      sb);

@@ -40,6 +40,7 @@
 // rounded ops).  A node computed inside a 64-node tree level is therefore
 // bit-identical to the same position decoded alone (GPU pipeline == GPU greedy
 // decode), whatever its launch-mates.
+#include <cstdlib>
 #include <type_traits>
 
 #include "attn.h"
@@ -478,11 +479,18 @@ __global__ void __launch_bounds__(kWarps * 32, 3) attn_chunks_kernel(const __gri
   for (int c = c0; c < c1; ++c) {
     const int buf = (c - c0) & 1;
     if (c + 1 < c1) stage(c + 1, buf ^ 1);
+#ifdef TP_ATTN_PRINTF
+    if (threadIdx.x == 0) printf("blk %d c %d c0 %d c1 %d max_c %d rows %d\n", blockIdx.x, c, c0, c1, max_c, rows);
+#endif
     sm100::mbar_wait(bars + buf, ((c - c0) >> 1) & 1);
+#ifdef TP_ATTN_PRINTF
+    if (threadIdx.x == 0) printf("blk %d c %d waited\n", blockIdx.x, c);
+#endif
     __syncthreads();  // the zero-filled V rows of a partial chunk are visible too
     const int j0 = c * kAttnChunk;
     const int lim[2] = {min(kAttnChunk, max(0, Ca - j0)), min(kAttnChunk, max(0, Cb - j0))};
-    if (busy && (lim[0] > 0 || lim[1] > 0)) {
+    // warp-uniform: the MMAs and shuffles below need every lane of the warp
+    if (busy && __any_sync(0xffffffffu, lim[0] > 0 || lim[1] > 0)) {
       const __nv_bfloat16* sK = smt + (size_t)buf * 2 * kTileElems;
       float m[2], l[2], sa[2], sb[2];
       uint32_t pa[4][4];
@@ -681,6 +689,9 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     TP_CUDA(cudaFuncSetAttribute(attn_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunksSmem));
     attr_set[dev & 63] = true;
   }
+  static const int dbg = getenv("TP_ATTN_DEBUG") ? atoi(getenv("TP_ATTN_DEBUG")) : 0;  // diagnostics: 1 skip tail, 2 skip chunks
+  if (dbg & 2) cs = 0;
+  if (dbg & 1) ct = 0;
   if (cs > 0) {
     ::tp::count_launch();
     TP_CUDA(launch_pdl(attn_chunks_kernel, dim3(cs), dim3(kWarps * 32), kChunksSmem, st, G));

@@ -252,6 +252,8 @@ int tp_debug_attn_tile(int32_t on);
  * 2 = shared-prefix tail for uniform levels on/off, 3 = diagnostic skip mask for the
  * Llama layer loop (bit 1 attention, 2 RMSNorm, 4 GEMMs; results WRONG while set). */
 int tp_debug_attn_knob(int32_t knob, int32_t value);
+/* Diagnostics: K1 run-kernel event trace buffer ([grid][8][1024] u64; only -DTP_ATTN_TRACE builds write). */
+int tp_debug_attn_trace(void* dev_buf);
 /* Diagnostics: the next Llama forward call copies member 0's first-layer
  * intermediates into dev_buf (input RMSNorm bf16 [n][d], RoPE'd queries bf16
  * [n][q], attention out bf16 [n][q], x after the

@@ -103,6 +103,7 @@ _SIGS = {
                                             _I, _I, _P, _P]),
     "tp_debug_attn_tile": (C.c_int, [_I]),
     "tp_debug_attn_knob": (C.c_int, [_I, _I]),
+    "tp_debug_attn_trace": (C.c_int, [C.c_void_p]),
     "tp_debug_dump": (C.c_int, [_P]),
     "tp_timeline_enable": (C.c_int, [_I]),
     "tp_timeline_read": (C.c_int, [C.c_char_p, _I]),

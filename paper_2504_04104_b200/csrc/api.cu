@@ -60,6 +60,8 @@ extern "C" int tp_debug_dump(void* dev_buf) {
   return TP_OK;
 }
 
+extern "C" int tp_debug_attn_trace(void* dev_buf) { return tp::attn_set_trace(dev_buf); }
+
 extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
   if (knob == 3) {
     tp::g_dbg_skip = value;
@@ -203,38 +205,94 @@ size_t meta_capacity(const tp_model* m, int cap, int* words) {
   return (bytes + 255) & ~(size_t)255;
 }
 
+// Llama pages from the model's pool (kvpage.cuh): slabs of >= 64 MB, zeroed once
+// (stale rows of recycled pages are finite; the attention kernel multiplies the
+// rows past a chunk's end by exact zeros).
+int page_take(tp_model* m, size_t count, char** out) {
+  std::lock_guard<std::mutex> lk(m->pool_mu);
+  if (m->page_free.size() < count) {
+    const int64_t pb = page_bytes(m->cfg.kv_heads);
+    const size_t want = std::max<size_t>(count - m->page_free.size(), (size_t)std::max<int64_t>(1, (64LL << 20) / pb));
+    void* slab = nullptr;
+    TP_CUDA(cudaMalloc(&slab, want * pb));
+    TP_CUDA(cudaMemset(slab, 0, want * pb));
+    m->page_slabs.push_back(slab);
+    for (size_t i = 0; i < want; ++i) m->page_free.push_back(static_cast<char*>(slab) + i * pb);
+  }
+  for (size_t i = 0; i < count; ++i) {
+    out[i] = m->page_free.back();
+    m->page_free.pop_back();
+  }
+  return TP_OK;
+}
+
+// Grow a Llama stage to >= cap rows by appending pages to every hosted layer.
+int alloc_pages(tp_stage* s, int cap) {
+  const int nl = s->hi - s->lo;
+  const int have = s->cap / kPageRows, need = (cap + kPageRows - 1) / kPageRows;
+  if (need > have && nl > 0) {
+    if (need > s->max_pages) {  // the table itself grows (rare): in-flight kernels may read the old one
+      const int mp = std::max(need, std::max(16, 2 * s->max_pages));
+      std::vector<char*> t((size_t)nl * mp, nullptr);
+      for (int l = 0; l < nl; ++l)
+        for (int p = 0; p < have; ++p) t[(size_t)l * mp + p] = s->ptab[(size_t)l * s->max_pages + p];
+      s->ptab.swap(t);
+      if (s->d_ptab) {
+        TP_CUDA(cudaDeviceSynchronize());
+        cudaFree(s->d_ptab);
+      }
+      TP_CUDA(cudaMalloc((void**)&s->d_ptab, sizeof(char*) * (size_t)nl * mp));
+      s->max_pages = mp;
+    }
+    std::vector<char*> fresh((size_t)nl * (need - have));
+    TP_TRY(page_take(s->m, fresh.size(), fresh.data()));
+    size_t k = 0;
+    for (int l = 0; l < nl; ++l)
+      for (int p = have; p < need; ++p) s->ptab[(size_t)l * s->max_pages + p] = fresh[k++];
+    // entries below `have` are unchanged, so kernels still reading them are unaffected
+    TP_CUDA(cudaMemcpy(s->d_ptab, s->ptab.data(), sizeof(char*) * s->ptab.size(), cudaMemcpyHostToDevice));
+  }
+  s->cap = std::max(have, need) * kPageRows;
+  return TP_OK;
+}
+
 int alloc_kv(tp_stage* s, int cap) {
   int nl = s->hi - s->lo;
-  size_t plane = (size_t)s->kv_heads * cap * s->head_dim * s->esize;
-  std::vector<void*> k(nl), v(nl);
-  for (int l = 0; l < nl; ++l) {
-    TP_CUDA(cudaMalloc(&k[l], plane));
-    TP_CUDA(cudaMalloc(&v[l], plane));
-    TP_CUDA(cudaMemset(k[l], 0, plane));
-    TP_CUDA(cudaMemset(v[l], 0, plane));
-    if (!s->k.empty()) {  // reserve(): carry rows over, head plane by head plane
-      size_t row = (size_t)s->head_dim * s->esize;
-      for (int h = 0; h < s->kv_heads; ++h) {
-        TP_CUDA(cudaMemcpy((char*)k[l] + h * cap * row, (char*)s->k[l] + h * (size_t)s->cap * row,
-                           (size_t)s->rows * row, cudaMemcpyDeviceToDevice));
-        TP_CUDA(cudaMemcpy((char*)v[l] + h * cap * row, (char*)s->v[l] + h * (size_t)s->cap * row,
-                           (size_t)s->rows * row, cudaMemcpyDeviceToDevice));
+  if (s->m->cfg.arch != TP_ARCH_TOY) {
+    TP_TRY(alloc_pages(s, cap));
+    cap = s->cap;
+  } else {
+    size_t plane = (size_t)s->kv_heads * cap * s->head_dim * s->esize;
+    std::vector<void*> k(nl), v(nl);
+    for (int l = 0; l < nl; ++l) {
+      TP_CUDA(cudaMalloc(&k[l], plane));
+      TP_CUDA(cudaMalloc(&v[l], plane));
+      TP_CUDA(cudaMemset(k[l], 0, plane));
+      TP_CUDA(cudaMemset(v[l], 0, plane));
+      if (!s->k.empty()) {  // reserve(): carry rows over, head plane by head plane
+        size_t row = (size_t)s->head_dim * s->esize;
+        for (int h = 0; h < s->kv_heads; ++h) {
+          TP_CUDA(cudaMemcpy((char*)k[l] + h * cap * row, (char*)s->k[l] + h * (size_t)s->cap * row,
+                             (size_t)s->rows * row, cudaMemcpyDeviceToDevice));
+          TP_CUDA(cudaMemcpy((char*)v[l] + h * cap * row, (char*)s->v[l] + h * (size_t)s->cap * row,
+                             (size_t)s->rows * row, cudaMemcpyDeviceToDevice));
+        }
+        cudaFree(s->k[l]);
+        cudaFree(s->v[l]);
       }
-      cudaFree(s->k[l]);
-      cudaFree(s->v[l]);
     }
+    s->k = k;
+    s->v = v;
+    s->cap = cap;
+    std::vector<void*> planes(2 * nl);
+    for (int l = 0; l < nl; ++l) {
+      planes[2 * l] = k[l];
+      planes[2 * l + 1] = v[l];
+    }
+    if (s->d_planes) cudaFree(s->d_planes);
+    TP_CUDA(cudaMalloc(&s->d_planes, sizeof(void*) * std::max(1, 2 * nl)));
+    if (nl) TP_CUDA(cudaMemcpy(s->d_planes, planes.data(), sizeof(void*) * 2 * nl, cudaMemcpyHostToDevice));
   }
-  s->k = k;
-  s->v = v;
-  s->cap = cap;
-  std::vector<void*> planes(2 * nl);
-  for (int l = 0; l < nl; ++l) {
-    planes[2 * l] = k[l];
-    planes[2 * l + 1] = v[l];
-  }
-  if (s->d_planes) cudaFree(s->d_planes);
-  TP_CUDA(cudaMalloc(&s->d_planes, sizeof(void*) * std::max(1, 2 * nl)));
-  if (nl) TP_CUDA(cudaMemcpy(s->d_planes, planes.data(), sizeof(void*) * 2 * nl, cudaMemcpyHostToDevice));
   // metadata staging follows capacity
   if (s->meta) cudaFree(s->meta);
   if (s->host_meta) cudaFreeHost(s->host_meta);
@@ -247,6 +305,24 @@ int alloc_kv(tp_stage* s, int cap) {
 bool is_toy(const tp_model* m) { return m->cfg.arch == TP_ARCH_TOY; }
 
 }  // namespace
+
+namespace tp {
+KvView kv_view(const tp_stage* s) {
+  KvView v{};
+  v.heads = s->kv_heads;
+  v.row_bytes = s->head_dim * s->esize;
+  if (is_toy(s->m)) {
+    v.tab = reinterpret_cast<char* const*>(s->d_planes);
+    v.paged = 0;
+    v.plane_stride = (int64_t)s->cap * v.row_bytes;
+  } else {
+    v.tab = s->d_ptab;
+    v.paged = 1;
+    v.max_pages = s->max_pages;
+  }
+  return v;
+}
+}  // namespace tp
 
 extern "C" {
 
@@ -354,6 +430,7 @@ static void model_free_now(tp_model* m) {
   if (!is_toy(m)) llama_model_free(m);
   call_ring_free(m);
   if (m->prune_plan) cudaFree(m->prune_plan);
+  for (void* p : m->page_slabs) cudaFree(p);
   delete m;
 }
 
@@ -531,6 +608,12 @@ static void stage_release(tp_stage* s) {
   cudaSetDevice(s->m->cfg.device);
   for (void* p : s->k) cudaFree(p);
   for (void* p : s->v) cudaFree(p);
+  {  // pages go back to the model's pool
+    std::lock_guard<std::mutex> lk(s->m->pool_mu);
+    for (char* p : s->ptab)
+      if (p) s->m->page_free.push_back(p);
+  }
+  if (s->d_ptab) cudaFree(s->d_ptab);
   if (s->ws) cudaFree(s->ws);
   if (s->meta) cudaFree(s->meta);
   if (s->host_meta) cudaFreeHost(s->host_meta);
@@ -553,7 +636,7 @@ int tp_stage_rows(const tp_stage* s, int32_t* rows) {
 int tp_stage_reserve(tp_stage* s, int32_t capacity_rows) {
   if (capacity_rows <= s->cap) return TP_OK;
   TP_CUDA(cudaSetDevice(s->m->cfg.device));
-  TP_CUDA(cudaDeviceSynchronize());
+  TP_CUDA(cudaDeviceSynchronize());  // the metadata ring follows the capacity (re-allocated)
   TP_TRY(alloc_kv(s, capacity_rows));
   return is_toy(s->m) ? TP_OK : llama_stage_init(s);
 }
@@ -902,7 +985,7 @@ int tp_stage_compact(tp_stage* s, int32_t first_row, int32_t count, const uint64
     cudaStream_t st = (cudaStream_t)stream;
     const char* d;
     TP_TRY(upload(s, src.data(), src.size() * 4, st, &d));
-    TP_TRY(kv_compact(s, (const int32_t*)d, (int)src.size(), first_row, s->d_planes, st));
+    TP_TRY(kv_compact(s, (const int32_t*)d, (int)src.size(), first_row, st));
     timeline_mark("kv_compact", st);
   }
   s->rows = first_row + (int)src.size();
@@ -942,17 +1025,14 @@ int tp_stages_compact(int32_t count, tp_stage* const* stages, const int32_t* fir
     for (int i = c0; i < c1; ++i) {
       tp_stage* s = stages[i];
       const std::vector<int32_t>& v = src[i - c0];
-      const int nl = s->hi - s->lo, rb = s->head_dim * s->esize;
+      const int nl = s->hi - s->lo;
       std::memcpy(h + off, v.data(), 4 * v.size());
       if (!v.empty() && nl > 0) {
         MoveItem& it = g.m[g.count++];
-        it.planes = s->d_planes;
-        it.plane_stride = (int64_t)s->cap * rb;
+        it.kv = kv_view(s);
         it.src = reinterpret_cast<const int32_t*>(dm + off);
-        it.row_bytes = rb;
         it.n_keep = (int)v.size();
         it.first = first_rows[i];
-        it.heads = s->kv_heads;
         it.cta0 = ctas;
         ctas += 2 * nl * s->kv_heads;
       }
@@ -1014,9 +1094,18 @@ int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo,
   TP_CHECK(layer >= s->lo && layer < s->hi, TP_ESHAPE, "layer not hosted by stage");
   TP_CHECK(0 <= lo && lo <= hi && hi <= s->cap, TP_ESHAPE, "row range outside capacity");
   if (hi == lo) return TP_OK;
-  const char* plane = (const char*)(kind == 0 ? s->k : s->v)[layer - s->lo];
   size_t row = (size_t)s->head_dim * s->esize;
   TP_CUDA(cudaDeviceSynchronize());
+  if (!is_toy(s->m)) {  // paged: gather on the device, one copy out
+    void* d = nullptr;
+    const size_t bytes = (size_t)(hi - lo) * s->kv_heads * row;
+    TP_CUDA(cudaMalloc(&d, bytes));
+    int rc = kv_read_rows(s, layer, kind, lo, hi, d, 0);
+    if (rc == TP_OK) TP_CUDA(cudaMemcpy(host, d, bytes, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return rc;
+  }
+  const char* plane = (const char*)(kind == 0 ? s->k : s->v)[layer - s->lo];
   for (int h = 0; h < s->kv_heads; ++h)
     TP_CUDA(cudaMemcpy2D((char*)host + h * row, row * s->kv_heads, plane + (h * (size_t)s->cap + lo) * row, row,
                          row, hi - lo, cudaMemcpyDeviceToHost));

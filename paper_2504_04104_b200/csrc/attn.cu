@@ -1,5 +1,5 @@
-// K1: tree-masked attention of a level's nodes against one stage's KV cache
-// (Llama path; replaces the gather + softmax + PV of the reference
+// K1: tree-masked attention of a level's nodes against one stage's paged KV
+// cache (Llama path; replaces the gather + softmax + PV of the reference
 // layer_step, `/root/reference/pkg/src/treepipe/model.py:157-167,265-276`).
 //
 // Node i attends its *logical* key sequence of T_i = P_i + A_i + 1 slots: cache
@@ -7,41 +7,48 @@
 // (the set bits of its packed ancestor row), then itself (self last).  The
 // sequence is split at a fixed distance from its end:
 //
-//   * chunked part, slots [0, T_i - W) (W = kSuffix = 16): with A_i < W these
-//     are prefix rows only — cache row = slot — so every node of a tree level
-//     shares them.  Cut into canonical 64-slot chunks (chunk c = slots
-//     [64c, 64c + 64), the last one partial) and runs of kRun chunks.  A chunk
-//     yields a partial (max, sum, unnormalised P.V) from one m16n8k16 bf16
-//     tensor-core pass over a padded shared-memory tile; a run's state is the
-//     in-order merge of its chunks from the empty state.
-//       attn_chunks_kernel  one CTA per (member, KV head, run, block of 64
-//                           (query head, node) rows): the run's K/V chunks are
-//                           staged ONCE for all rows by bulk TMA copies
-//                           (cp.async.bulk, one per 256-byte row, mbarrier
-//                           completion, double buffered) and the run states
-//                           written; members with few rows take the run's
-//                           chunks in parallel across warps instead.
+//   * chunked part, slots [0, C_i), C_i = max(0, T_i - W) (W = kAttnSuffix = 16):
+//     with A_i < W these are prefix rows only — cache row = slot — so every
+//     node of a tree level shares them.  Canonical 64-slot chunks (chunk c =
+//     slots [64c, 64c + 64) = KV page c) are grouped into canonical runs of R
+//     chunks.  A run's state is the online softmax over its chunks on the 5th-
+//     generation tensor cores:
+//       attn_run_kernel  one CTA per (member, KV head, run, block of 128
+//                        (node, query head) rows).  A producer thread stages
+//                        each chunk's K and V page blocks with ONE 16 KB bulk
+//                        copy each (the pages are stored in the SW128 operand
+//                        layout, kvpage.cuh; two stages, mbarrier completion);
+//                        an MMA thread issues S = Q K^T (M=128, N=64, K=128)
+//                        into TMEM and O += P V (M=128, N=128, K=64; V is the
+//                        MN-major operand) accumulating in TMEM; four softmax
+//                        warps own one row each per thread: they read the
+//                        row's 64 scores from TMEM, apply the row's chunk
+//                        limit, take the max, rescale the row's O in TMEM only
+//                        when the max grew, write bf16 P to shared memory in
+//                        the SW128 layout and keep the row sum.  S of chunk
+//                        c+1 is computed while the softmax of chunk c runs.
 //   * suffix, the last W slots (prefix tail, ancestors, self): node-specific.
-//       attn_tail_kernel    one warp per (node, query head): decodes the
-//                           node's ancestor rows from its packed bit-row in
-//                           registers (word popcounts + a warp scan, then
-//                           the rank-th set bit), computes the suffix partial
-//                           on the FMA pipes in a fixed order (lane l owns
-//                           dims 4l..4l+3, dot products by a butterfly sum),
-//                           merges the run states in order and the suffix
-//                           last, and writes the bf16 output row.  The suffix
-//                           is computed before griddepcontrol.wait, while the
-//                           chunk kernel still runs.
+//       attn_tail_kernel one CTA per (member, node, 8 query heads): warp 0
+//                        decodes the node's suffix rows (the ancestor bit-row
+//                        walked in registers: word popcounts, then the
+//                        rank-th set bit) into shared memory; warp w computes
+//                        head w's suffix partial on the FMA pipes in a fixed
+//                        order (lane l owns dims 4l..4l+3, dot products by a
+//                        butterfly sum) before griddepcontrol.wait — while
+//                        the run kernel still runs — then merges the run
+//                        states in order and the suffix last, and writes the
+//                        bf16 output row.
 //
 // Batch invariance: every boundary above depends only on T_i, which is the
-// node's position + 1 whether it sits in a tree level or is decoded alone, and
-// a chunk partial depends only on the node's query and the chunk's key rows
-// (tensor-core rows and columns are independent; merges use explicitly
-// rounded ops).  A node computed inside a 64-node tree level is therefore
-// bit-identical to the same position decoded alone (GPU pipeline == GPU greedy
-// decode), whatever its launch-mates.
+// node's position + 1 whether it sits in a tree level or is decoded alone.  A
+// row's run state depends only on its own query and the chunk rows: tensor-
+// core rows are independent, the same MMA shapes run for any number of valid
+// rows, the rescale decision and factor are the row's own, masked slots
+// contribute exact zeros, and merges use explicitly rounded ops.  A node
+// computed inside a 64-node tree level is therefore bit-identical to the same
+// position decoded alone (GPU pipeline == GPU greedy decode), whatever its
+// launch-mates.
 #include <cstdlib>
-#include <type_traits>
 
 #include "attn.h"
 #include "gemm_tc.h"
@@ -49,196 +56,46 @@
 
 namespace tp {
 
-constexpr int kPad = 136;  // bf16 per staged row: 128 + 8 pad (conflict-free ldmatrix)
-constexpr int kWarps = 4;
-constexpr int kTileElems = kAttnChunk * kPad;
-constexpr int kRowBytes = kAttnHeadDim * 2;
+using namespace sm100;
 
-__device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) {
-  return *reinterpret_cast<const uint32_t*>(p);
-}
+constexpr int kRowsPerCta = 128;  // tcgen05 M: (node, query head) rows of a run task
+constexpr int kRunThreads = 320;  // warps 0-7 softmax (column half = warp / 4), 8 K/V producer, 9 MMA issuer + Q loader
+constexpr int kKvStages = 2;
+constexpr int kQBytes = kRowsPerCta * kAttnHeadDim * 2;  // 32 KB: 2 dim-blocks of [128 rows][128 B]
+constexpr int kChunkBytes = 2 * kPageBlockBytes;           // K + V blocks of one chunk
+constexpr int kRunSmem = kQBytes + kKvStages * kChunkBytes;  // 96 KB: two CTAs per SM
+constexpr int kTmemCols = 256;  // S[b] (64 fp32 columns; P[b] packed bf16 pairs over its first 32) | O (128)
+constexpr int kTmemO = 128;
+constexpr int kTailWarps = 8;
+
 __device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
   return (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
 }
 __device__ __forceinline__ uint32_t pack_f32(float lo, float hi) {
   return pack_bf16(__float2bfloat16_rn(lo), __float2bfloat16_rn(hi));
 }
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-// exp(x) as one MUFU op: 2^(x*log2 e) with ex2.approx (flush-to-zero; every
-// attention path — shared chunks, per-node tail, tile, merges — uses this same
-// function, so batch invariance is unaffected).
-__device__ __forceinline__ float fast_exp(float x) {
+// 2^x as one MUFU op (ex2.approx, flush-to-zero).  K1 keeps scores, maxima
+// and run states in the base-2 domain (scores pre-multiplied by
+// scale * log2 e); every path uses this same function, so batch invariance is
+// unaffected.
+__device__ __forceinline__ float ex2f(float x) {
   float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(x, 1.4426950408889634f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-// 16-byte async copy global -> shared; src_bytes = 0 writes zeros.
-__device__ __forceinline__ void cp16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// wait until at most `ahead` (0..3) committed groups are still pending
-__device__ __forceinline__ void cp_wait_ahead(int ahead) {
-  switch (ahead) {
-    case 0: cp_wait_group<0>(); break;
-    case 1: cp_wait_group<1>(); break;
-    case 2: cp_wait_group<2>(); break;
-    default: cp_wait_group<3>(); break;
-  }
-}
+__device__ __forceinline__ float score_scale(float scale) { return __fmul_rn(scale, 1.4426950408889634f); }
 
-__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t (&r)[4]) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-
-// Scores + chunk softmax of one canonical 64-slot chunk for the 16-row tile
-// this warp holds, K staged in sK[slot][kPad]:
-//   qa   : Q A-fragments (8 k-steps over head_dim)
-//   lim  : rows g / g+8 see slots [0, lim) of this chunk
-// Returns the chunk max m, sum l and the bf16 P A-fragments.
-// Raw scores s = Q.K^T of one 64-slot chunk for the warp's 16-row tile, K
-// staged in sK[slot][kPad].
-__device__ __forceinline__ void tile_qk(const uint32_t (&qa)[8][4], const __nv_bfloat16* sK, float (&s)[8][4],
-                                        int lane) {
-  const int mi = lane >> 3, mr = lane & 7;
-#pragma unroll
-  for (int nt = 0; nt < 8; ++nt) {
-    s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-#pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) {
-      uint32_t b[4];  // b0/b1 of k-steps 2*k2 and 2*k2+1
-      ldsm4(su32(sK + (nt * 8 + mr) * kPad + 32 * k2 + 8 * mi), b);
-      mma16816(s[nt], qa[2 * k2], b[0], b[1]);
-      mma16816(s[nt], qa[2 * k2 + 1], b[2], b[3]);
-    }
-  }
-}
-
-// Chunk softmax of the raw scores: rows g / g+8 see slots [0, lim); returns the
-// chunk max m, sum l and the bf16 P A-fragments.
-__device__ __forceinline__ void chunk_softmax(float (&s)[8][4], const int (&lim)[2], float scale, float (&m)[2],
-                                              float (&l)[2], uint32_t (&pa)[4][4], int lane) {
-  const int tig = lane & 3;
-  float mc[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-  for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int slot = nt * 8 + 2 * tig + (e & 1);
-      const float v = slot < lim[e >> 1] ? __fmul_rn(s[nt][e], scale) : -INFINITY;
-      s[nt][e] = v;
-      mc[e >> 1] = fmaxf(mc[e >> 1], v);
-    }
-  float rs[2] = {0.f, 0.f};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    mc[h] = fmaxf(mc[h], __shfl_xor_sync(0xffffffffu, mc[h], 1));
-    mc[h] = fmaxf(mc[h], __shfl_xor_sync(0xffffffffu, mc[h], 2));
-  }
-#pragma unroll
-  for (int nt = 0; nt < 8; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int h = e >> 1;
-      const float p = s[nt][e] == -INFINITY ? 0.f : fast_exp(__fsub_rn(s[nt][e], mc[h]));
-      s[nt][e] = p;
-      rs[h] = __fadd_rn(rs[h], p);
-    }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    rs[h] = __fadd_rn(rs[h], __shfl_xor_sync(0xffffffffu, rs[h], 1));
-    rs[h] = __fadd_rn(rs[h], __shfl_xor_sync(0xffffffffu, rs[h], 2));
-    l[h] = rs[h];
-    m[h] = mc[h];
-  }
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
-    pa[kk][0] = pack_f32(s[2 * kk][0], s[2 * kk][1]);
-    pa[kk][1] = pack_f32(s[2 * kk][2], s[2 * kk][3]);
-    pa[kk][2] = pack_f32(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-    pa[kk][3] = pack_f32(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-  }
-}
-
-__device__ __forceinline__ void chunk_scores(const uint32_t (&qa)[8][4], const __nv_bfloat16* sK,
-                                             const int (&lim)[2], float scale, float (&m)[2], float (&l)[2],
-                                             uint32_t (&pa)[4][4], int lane) {
-  float s[8][4];
-  tile_qk(qa, sK, s, lane);
-  chunk_softmax(s, lim, scale, m, l, pa, lane);
-}
-
-// Online merge of a chunk partial (mc, lc, oc) into the running (M, L, O).
+// Online merge of a partial (mc, lc, oc) into the running (M, L, O).
 __device__ __forceinline__ void merge_scale(float& M, float& L, float mc, float lc, float& sa, float& sb) {
   const float mn = fmaxf(M, mc);
-  sa = M == -INFINITY ? 0.f : fast_exp(__fsub_rn(M, mn));
-  sb = fast_exp(__fsub_rn(mc, mn));
+  sa = M == -INFINITY ? 0.f : ex2f(__fsub_rn(M, mn));
+  sb = ex2f(__fsub_rn(mc, mn));
   L = __fmaf_rn(L, sa, __fmul_rn(lc, sb));
   M = mn;
 }
 __device__ __forceinline__ float merge_val(float O, float oc, float sa, float sb) {
   return __fmaf_rn(O, sa, __fmul_rn(oc, sb));
 }
-
-__device__ __forceinline__ size_t part_idx(const AttnArgs& a, int node, int h, int c) {
-  return ((size_t)node * a.H + h) * a.max_chunks + c;
-}
-
-// kind: 0 shared, 1 per-node tail, 2 GQA tail
-__device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
-  auto start = [&](int g) { return kind == 0 ? G.m[g].cta_shared : kind == 1 ? G.m[g].cta_tail : G.m[g].cta_gqa; };
-  int gi = 0;
-  while (gi + 1 < G.count && b >= start(gi + 1)) ++gi;
-  return gi;
-}
-
-// o = P . V over the dims [128 / NP * PART, 128 / NP * (PART + 1)) — n-tiles of
-// the full P . V in the same k order (the same MMAs per output element), with
-// 1/NP of the accumulators live.
-template <int PART, int NP>
-__device__ __forceinline__ void chunk_pv_part(const uint32_t (&pa)[4][4], const __nv_bfloat16* sV,
-                                              float (&o)[16 / NP][4], int lane) {
-  const int mi = lane >> 3, mr = lane & 7;
-#pragma unroll
-  for (int nd = 0; nd < 16 / NP; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
-#pragma unroll
-  for (int n2l = 0; n2l < 8 / NP; ++n2l)
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int n2 = (8 / NP) * PART + n2l;
-      uint32_t b[4];
-      ldsm4t(su32(sV + (16 * kk + 8 * (mi & 1) + mr) * kPad + 16 * n2 + 8 * (mi >> 1)), b);
-      mma16816(o[2 * n2l], pa[kk], b[0], b[1]);
-      mma16816(o[2 * n2l + 1], pa[kk], b[2], b[3]);
-    }
-}
-template <int HALF>
-__device__ __forceinline__ void chunk_pv_half(const uint32_t (&pa)[4][4], const __nv_bfloat16* sV, float (&o)[8][4],
-                                              int lane) {
-  chunk_pv_part<HALF, 2>(pa, sV, o, lane);
-}
-
-// Merge a partial (mc, lc, oc) into a lane-layout state (M, L, O).
 __device__ __forceinline__ void merge_lane(float& M, float& L, float4& O, float mc, float lc, float4 oc) {
   float sa, sb;
   merge_scale(M, L, mc, lc, sa, sb);
@@ -248,20 +105,15 @@ __device__ __forceinline__ void merge_lane(float& M, float& L, float4& O, float 
   O.w = merge_val(O.w, oc.w, sa, sb);
 }
 
+__device__ __forceinline__ size_t part_idx(const AttnArgs& a, int node, int h, int r) {
+  return ((size_t)node * a.H + h) * a.max_chunks + r;
+}
 
-// Canonical chunks per run: a fixed property of the numerics (every launch of a
-// process must use the same value for batch invariance); knob 1 for tuning.
-static int g_attn_run = 4;
-constexpr int kCtaRows = 64;  // (query head, node) rows per chunk CTA: one 16-row MMA tile per warp
-constexpr int kSmallRows = 32;
-constexpr int kXsLd = 132;  // floats per hand-over row
-constexpr size_t kChunksSmem = (size_t)4 * kTileElems * 2 + 64;  // 2 x (K, V) chunk tiles + mbarriers
-
-__device__ __forceinline__ void bulk_row(void* smem_dst, const void* gsrc, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(smem_dst)),
-               "l"(gsrc), "r"(kRowBytes), "r"(su32(bar))
-               : "memory");
+// kind 0: run launch, 1: tail launch
+__device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
+  int gi = 0;
+  while (gi + 1 < G.count && b >= (kind == 0 ? G.m[gi + 1].cta_run : G.m[gi + 1].cta_tail)) ++gi;
+  return gi;
 }
 
 // Slots of node i's chunked part (T_i - W, >= 0).
@@ -269,367 +121,533 @@ __device__ __forceinline__ int chunked_slots(const LevelDev& lv, int i) {
   return max(0, __ldg(lv.prefix_rows + i) + __ldg(lv.anc_cnt + i) + 1 - kAttnSuffix);
 }
 
-// Empty-partial guard of a merge: a row with no slot in the chunk keeps its state.
-__device__ __forceinline__ void merge_scale_live(float& M, float& L, float mc, float lc, bool live, float& sa,
-                                                 float& sb) {
-  if (live) {
-    merge_scale(M, L, mc, lc, sa, sb);
-  } else {
-    sa = 1.f;
-    sb = 0.f;
-  }
+// ---- tcgen05 helpers local to K1 ----------------------------------------------
+// 32 lanes x 32 columns of 32-bit (no wait: pair with tmem_wait_ld).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// MN-major operand in the 128-byte-swizzled layout: 64-element (128 B) rows
+// along MN, one row per K index; 8-row atoms of 1024 B along K (SBO), the next
+// 64 MN elements LBO bytes further.
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(const void* smem_tile, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(smem_tile) >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;  // LBO: next 64 MN elements
+  d |= (uint64_t)(1024 >> 4) << 32;                  // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
 }
 
-// Stage rows [j0, j0 + nrows) of one kv-head plane into a tile by bulk copies
-// issued by the calling warp (completion counted on `bar`); with zero_tail the
-// rows beyond nrows are zeroed (V of a partial chunk: their P is 0, and
-// 0 x stale bits must not be NaN).
-__device__ __forceinline__ void stage_rows(const __nv_bfloat16* plane, const AttnArgs& a, int kh, int j0, int nrows,
-                                           __nv_bfloat16* tile, uint64_t* bar, bool zero_tail, int lane) {
-  const __nv_bfloat16* src = plane + ((size_t)kh * a.cap + (size_t)j0) * kAttnHeadDim;
-  // the tile's previous generic-proxy reads / zero stores are ordered before these async-proxy writes
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  for (int r = lane; r < nrows; r += 32) bulk_row(tile + r * kPad, src + (size_t)r * kAttnHeadDim, bar);
-  if (zero_tail) {
-    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-    for (int e = nrows * 16 + lane; e < kAttnChunk * 16; e += 32)
-      *reinterpret_cast<uint4*>(tile + (e >> 4) * kPad + (e & 15) * 8) = z;
-  }
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-// K and V of one chunk into a (K, V) tile pair, one mbarrier phase.
-__device__ __forceinline__ void stage_chunk(const AttnArgs& a, int kh, int j0, int nrows, __nv_bfloat16* sK,
-                                            __nv_bfloat16* sV, uint64_t* bar, int lane) {
-  if (lane == 0) sm100::mbar_expect_tx(bar, (uint32_t)(2 * nrows * kRowBytes));
-  __syncwarp();
-  stage_rows(a.k, a, kh, j0, nrows, sK, bar, false, lane);
-  stage_rows(a.v, a, kh, j0, nrows, sV, bar, true, lane);
+// D (TMEM) += A (TMEM, M rows on lanes, K packed 2 x bf16 per column) x B (shared).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 
-// Few rows (<= kSmallRows (query head, node) pairs, e.g. the lone verification
-// node): one CTA per (member, KV head, run, 16-row tile), warp w computing chunk
-// w of the run (run <= kWarps) on its own tile, partials handed over through
-// smem and merged in chunk order — the same chunk arithmetic and merge sequence
-// as the row-parallel path, the run's chunks in parallel.
-__device__ __forceinline__ void chunks_small(const AttnGroup& G, int gi, int local, uint8_t* dsm) {
-  const AttnArgs& a = G.m[gi].a;
-  const LevelDev& lv = G.m[gi].lv;
-  const int c_hi = G.m[gi].c_shared, R = G.run;
-  const int runs = (c_hi + R - 1) / R;
-  const int kh = local % a.KV;
+// Canonical chunks per run: a fixed property of the numerics (every launch of a
+// process must use the same value for batch invariance); knob 1 for tuning.
+static int g_attn_run = 4;
+
+// A run task: (member, KV head, run, block of 128 (node, query head) rows).
+struct RunTask {
+  int gi, kh, r, base, rows, c0, nch;
+};
+__device__ __forceinline__ RunTask run_task(const AttnGroup& G, int t) {
+  RunTask k;
+  k.gi = member_of(G, t, 0);
+  const AttnMember& M = G.m[k.gi];
+  const AttnArgs& a = M.a;
+  int local = t - M.cta_run;
+  k.kh = local % a.KV;
   local /= a.KV;
-  const int r = local % runs, t = local / runs;
-  const int grp = a.H / a.KV;
-  const int n = lv.n, rows = n * grp;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, tig = lane & 3;
-  const int nw = min(R, c_hi - r * R);
-  __nv_bfloat16* buf = reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)warp * kTileElems;  // K, then V
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<__nv_bfloat16*>(dsm) + (size_t)kWarps * kTileElems);
-  float* xs = reinterpret_cast<float*>(buf);  // [16][kXsLd] partial, then 16 max + 16 sum + 16 live
-  const int c = r * R + warp;
-  const int ra = 16 * t + g, rb = ra + 8;
-  const bool va = ra < rows, vb = rb < rows;
-  const int ia = va ? ra % n : 0, ib = vb ? rb % n : 0;
-  const int ha = kh * grp + (va ? ra / n : 0), hb = kh * grp + (vb ? rb / n : 0);
-  const int Ca = va ? chunked_slots(lv, ia) : 0, Cb = vb ? chunked_slots(lv, ib) : 0;
-  if (threadIdx.x < kWarps) sm100::mbar_init(bars + threadIdx.x, 1);
-  sm100::fence_barrier_init();
-  __syncthreads();
-  if (warp < nw) {
-    const int j0 = c * kAttnChunk;
-    const int nrows = min(kAttnChunk, max(0, G.m[gi].max_c - j0));
-    if (lane == 0) sm100::mbar_expect_tx(bars + warp, (uint32_t)(nrows * kRowBytes));
-    __syncwarp();
-    stage_rows(a.k, a, kh, j0, nrows, buf, bars + warp, false, lane);
-    uint32_t qa[8][4];
-    const __nv_bfloat16* qra = a.q + (size_t)ia * a.q_stride + ha * kAttnHeadDim;
-    const __nv_bfloat16* qrb = a.q + (size_t)ib * a.q_stride + hb * kAttnHeadDim;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      qa[kk][0] = va ? ld_b32(qra + 16 * kk + 2 * tig) : 0u;
-      qa[kk][1] = vb ? ld_b32(qrb + 16 * kk + 2 * tig) : 0u;
-      qa[kk][2] = va ? ld_b32(qra + 16 * kk + 8 + 2 * tig) : 0u;
-      qa[kk][3] = vb ? ld_b32(qrb + 16 * kk + 8 + 2 * tig) : 0u;
-    }
-    const int lim[2] = {min(kAttnChunk, max(0, Ca - j0)), min(kAttnChunk, max(0, Cb - j0))};
-    sm100::mbar_wait(bars + warp, 0);
-    float m[2], l[2];
-    uint32_t pa[4][4];
-    chunk_scores(qa, buf, lim, a.scale, m, l, pa, lane);
-    __syncwarp();  // every lane is done reading K: the tile takes V
-    if (lane == 0) sm100::mbar_expect_tx(bars + warp, (uint32_t)(nrows * kRowBytes));
-    __syncwarp();
-    stage_rows(a.v, a, kh, j0, nrows, buf, bars + warp, true, lane);
-    __syncwarp();
-    sm100::mbar_wait(bars + warp, 1);
-    float o0[8][4], o1[8][4];
-    chunk_pv_half<0>(pa, buf, o0, lane);
-    chunk_pv_half<1>(pa, buf, o1, lane);
-    __syncwarp();  // the tile becomes the hand-over buffer
-#pragma unroll
-    for (int nd = 0; nd < 8; ++nd) {
-      *reinterpret_cast<float2*>(xs + g * kXsLd + nd * 8 + 2 * tig) = make_float2(o0[nd][0], o0[nd][1]);
-      *reinterpret_cast<float2*>(xs + (g + 8) * kXsLd + nd * 8 + 2 * tig) = make_float2(o0[nd][2], o0[nd][3]);
-      *reinterpret_cast<float2*>(xs + g * kXsLd + 64 + nd * 8 + 2 * tig) = make_float2(o1[nd][0], o1[nd][1]);
-      *reinterpret_cast<float2*>(xs + (g + 8) * kXsLd + 64 + nd * 8 + 2 * tig) = make_float2(o1[nd][2], o1[nd][3]);
-    }
-    if (tig == 0) {
-      xs[16 * kXsLd + g] = m[0];
-      xs[16 * kXsLd + g + 8] = m[1];
-      xs[16 * kXsLd + 16 + g] = l[0];
-      xs[16 * kXsLd + 16 + g + 8] = l[1];
-      xs[16 * kXsLd + 32 + g] = lim[0] > 0 ? 1.f : 0.f;
-      xs[16 * kXsLd + 32 + g + 8] = lim[1] > 0 ? 1.f : 0.f;
-    }
-  }
-  __syncthreads();
-  const int row = threadIdx.x >> 3, d0 = (threadIdx.x & 7) * 16;  // 8 threads per row, 16 dims each
-  const int rr = 16 * t + row;
-  if (rr >= rows) return;
-  float M = -INFINITY, L = 0.f, O[16];
-#pragma unroll
-  for (int d = 0; d < 16; ++d) O[d] = 0.f;
-  for (int w = 0; w < nw; ++w) {
-    const float* xw = reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(dsm) +
-                                                     (size_t)w * kTileElems);
-    float sa, sb;
-    merge_scale_live(M, L, xw[16 * kXsLd + row], xw[16 * kXsLd + 16 + row], xw[16 * kXsLd + 32 + row] != 0.f, sa,
-                     sb);
-#pragma unroll
-    for (int d = 0; d < 16; ++d) O[d] = merge_val(O[d], xw[row * kXsLd + d0 + d], sa, sb);
-  }
-  const size_t idx = part_idx(a, rr % n, kh * grp + rr / n, r);
-  float* po = a.po + idx * kAttnHeadDim + d0;
-#pragma unroll
-  for (int d = 0; d < 16; d += 4) *reinterpret_cast<float4*>(po + d) = make_float4(O[d], O[d + 1], O[d + 2], O[d + 3]);
-  if ((threadIdx.x & 7) == 0) {
-    a.pm[idx] = M;
-    a.pl[idx] = L;
-  }
+  const int runs = (M.c_hi + G.run - 1) / G.run;
+  k.r = local % runs;
+  const int blk = local / runs;
+  const int grp = a.H / a.KV, npc = kRowsPerCta / grp;
+  k.base = blk * npc;
+  k.rows = min(npc, M.lv.n - k.base) * grp;
+  k.c0 = k.r * G.run;
+  k.nch = min(M.c_hi, k.c0 + G.run) - k.c0;
+  return k;
 }
 
-// One CTA per (member, KV head, run, block of kCtaRows (query head, node) rows):
-// streams the run's chunks (chunk c + 1 in flight by bulk TMA while chunk c
-// computes), each K/V chunk staged once for every row, merges them in order
-// into the rows' run states (fragment layout, the same scalar merge ops as
-// merge_lane) and writes the states.
-__global__ void __launch_bounds__(kWarps * 32, 3) attn_chunks_kernel(const __grid_constant__ AttnGroup G) {
-  pdl_wait();
+// Diagnostics (built with -DTP_ATTN_TRACE): per-CTA, per-role globaltimer
+// events of the run kernel into a device buffer set by tp_debug_attn_trace.
+__device__ unsigned long long* g_attn_trace = nullptr;
+#ifdef TP_ATTN_TRACE
+__device__ __forceinline__ void trace_ev(int role, int& idx, int tag, int arg) {
+  unsigned long long* b = g_attn_trace;
+  if (!b || idx >= 1024) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  b[((size_t)blockIdx.x * 8 + role) * 1024 + idx++] = ((unsigned long long)tag << 56) |
+                                                       ((unsigned long long)(arg & 0xffff) << 40) |
+                                                       (t & 0xffffffffffull);
+}
+#define TRACE(role, idx, tag, arg) trace_ev(role, idx, tag, arg)
+#else
+#define TRACE(role, idx, tag, arg) ((void)0)
+#endif
+
+// Persistent, two CTAs per SM: CTA b takes tasks b, b + grid, ...  Every role
+// walks the same chunk sequence (global chunk counter g), so K/V staging runs
+// ahead across task boundaries:
+//   warp 8      K/V producer: one 16 KB bulk copy per K / V page block, 2 stages
+//   warp 8      also stages each task's Q tile with a 3D TMA box (node x head x dim)
+//   warp 9      MMA issuer (lane 0):
+//               S[g&1] = Q K^T (SS), then O += P[g&1] V (TS: P from TMEM over
+//               the S buffer it came from, V the MN-major shared operand); S of
+//               chunk g+1 is issued before waiting for P of chunk g
+//   warps 0-7   softmax; warp w owns TMEM lanes 32 (w % 4) .. +31 (rows) and
+//               column half w / 4: S half-row from TMEM, the row max shared with
+//               the partner warp through shared memory, lazy rescale of O in
+//               TMEM, bf16 P back to TMEM, half-row sum; at a task's end the O
+//               row (its 64 columns) and the state are stored.
+__global__ void __launch_bounds__(kRunThreads, 2) attn_run_kernel(const __grid_constant__ AttnGroup G, int ntasks) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  __shared__ uint64_t bars[2 * kKvStages + 8];  // (q_full: producer TMA, expect-tx)
+  __shared__ uint32_t tmem_holder;
+  __shared__ float xchg[2][2][kRowsPerCta];  // [chunk parity][column half] partial row maxima
+  __shared__ float xl[2][kRowsPerCta];       // [column half] a task's final row sums
+  uint64_t* kv_full = bars;                 // [2] producer -> MMA
+  uint64_t* kv_empty = bars + kKvStages;    // [2] MMA (PV done) -> producer
+  uint64_t* s_full = bars + 2 * kKvStages;  // [2] MMA -> softmax
+  uint64_t* p_full = s_full + 2;            // [2] softmax (8 warps) -> MMA
+  uint64_t* pv_done = s_full + 4;           // [2] MMA -> softmax, MMA (S/P buffer reuse)
+  uint64_t* q_free = s_full + 6;            // MMA: the task's last S is complete (Q tile reusable)
+  uint64_t* q_full = s_full + 7;            // producer (TMA) -> MMA: the task's Q tile is staged
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sQ = dsm;
+  uint8_t* sKV = dsm + kQBytes;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(kv_full + b, 1);
+      mbar_init(kv_empty + b, 1);
+      mbar_init(s_full + b, 1);
+      mbar_init(p_full + b, 8);
+      mbar_init(pv_done + b, 1);
+    }
+    mbar_init(q_free, 1);
+    mbar_init(q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tmem_holder, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_holder;
+  pdl_wait();  // Q and the new K/V rows come from the QKV GEMM
   pdl_trigger();
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int gi = member_of(G, blockIdx.x, 0);
-  if (G.m[gi].small) {
-    chunks_small(G, gi, blockIdx.x - G.m[gi].cta_shared, dsm);
-    return;
-  }
-  const AttnArgs& a = G.m[gi].a;
-  const LevelDev& lv = G.m[gi].lv;
-  const int c_hi = G.m[gi].c_shared;
-  const int kRun = G.run;
-  const int runs = (c_hi + kRun - 1) / kRun;
-  int local = blockIdx.x - G.m[gi].cta_shared;
-  const int kh = local % a.KV;
-  local /= a.KV;
-  const int r = local % runs, blk = local / runs;
-  const int grp = a.H / a.KV;
-  const int npc = kCtaRows / grp;  // nodes per CTA
-  const int base = blk * npc;
-  const int c0 = r * kRun, c1 = min(c_hi, c0 + kRun);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, tig = lane & 3;
-  const int nreal = min(npc, lv.n - base);
-  const int rows = nreal * grp;  // (query head, node) pairs, head-major
-  __nv_bfloat16* smt = reinterpret_cast<__nv_bfloat16*>(dsm);  // [2][K | V][kTileElems]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smt + 4 * kTileElems);
-  if (threadIdx.x < 2) sm100::mbar_init(bars + threadIdx.x, 1);
-  sm100::fence_barrier_init();
-  __syncthreads();
-  const int max_c = G.m[gi].max_c;
-  auto stage = [&](int c, int buf) {  // warp 0 issues; everyone waits on the buffer's mbarrier
-    if (warp == 0) {
-      __nv_bfloat16* sK = smt + (size_t)buf * 2 * kTileElems;
-      stage_chunk(a, kh, c * kAttnChunk, min(kAttnChunk, max(0, max_c - c * kAttnChunk)), sK, sK + kTileElems,
-                  bars + buf, lane);
+  int tix = 0;
+  (void)tix;
+  if (threadIdx.x == 0) TRACE(0, tix, 0, 0);
+  if (warp < 8) {
+    // ---- softmax warps ----
+    const int t = threadIdx.x & 127, half = warp >> 2;
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    int g = 0;
+    for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+      const RunTask k = run_task(G, task);
+      const AttnArgs& a = G.m[k.gi].a;
+      const LevelDev& lv = G.m[k.gi].lv;
+      const float c2 = score_scale(a.scale);
+      const int grp = a.H / a.KV;
+      const bool valid = t < k.rows;
+      const bool warp_live = (t & ~31) < k.rows;  // any valid row in this warp
+      const int node = k.base + (valid ? t / grp : 0), h = k.kh * grp + (valid ? t % grp : 0);
+      const int Crow = valid ? chunked_slots(lv, node) : 0;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < k.nch; ++j, ++g) {
+        const int b = g & 1;
+        mbar_wait(s_full + b, (g >> 1) & 1);
+        if (threadIdx.x == 0) TRACE(0, tix, 1, g);
+        tc_fence_after();
+        uint32_t sv[32];
+        if (warp_live) {
+          tmem_ld32(tl + b * 64 + half * 32, sv);
+          tmem_wait_ld();
+        }
+        if (threadIdx.x == 0) TRACE(0, tix, 8, g);
+        const int lim = min(32, max(0, Crow - (k.c0 + j) * kAttnChunk - half * 32));
+        const bool full = __all_sync(0xffffffffu, lim == 32);  // warp-uniform unmasked fast path
+        // partial row max over this half (4 independent chains, combined in a fixed order)
+        float c4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (warp_live) {
+          if (full) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) c4[q & 3] = fmaxf(c4[q & 3], __uint_as_float(sv[q]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q < lim) c4[q & 3] = fmaxf(c4[q & 3], __uint_as_float(sv[q]));
+          }
+        }
+        xchg[b][half][t] = fmaxf(fmaxf(c4[0], c4[1]), fmaxf(c4[2], c4[3]));
+        // the pair of warps sharing these rows: both have read S[b] past this point,
+        // so P may overwrite it
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp & 3)) : "memory");
+        const float cmax = fmaxf(xchg[b][0][t], xchg[b][1][t]);
+        if (threadIdx.x == 0) TRACE(0, tix, 9, g);
+        // Lazy rescale: the row keeps its reference max m until a chunk's max
+        // exceeds it by more than 8 (p <= 2^8 meanwhile), so O is rescaled —
+        // and the previous PV waited for — only on such jumps.  The decision
+        // depends on the row's own scores only.
+        const float cand = cmax == -INFINITY ? -INFINITY : __fmul_rn(cmax, c2);
+        const bool grow = m != -INFINITY && cand > __fadd_rn(m, 8.f);
+        const float mn = (m == -INFINITY || grow) ? cand : m;
+        const float alpha = grow ? ex2f(__fsub_rn(m, mn)) : 1.f;
+        uint32_t pk[16];
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};  // fp32 sum of the unrounded p (4 chains, fixed combine order)
+        if (warp_live) {
+          if (full) {
+#pragma unroll
+            for (int q = 0; q < 32; q += 2) {
+              const float p0 = ex2f(__fmaf_rn(__uint_as_float(sv[q]), c2, -mn));
+              const float p1 = ex2f(__fmaf_rn(__uint_as_float(sv[q + 1]), c2, -mn));
+              const __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
+              pk[q >> 1] = *reinterpret_cast<const uint32_t*>(&pp);
+              s4[q & 3] = __fadd_rn(s4[q & 3], p0);
+              s4[(q + 1) & 3] = __fadd_rn(s4[(q + 1) & 3], p1);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q += 2) {
+              const float p0 = q < lim ? ex2f(__fmaf_rn(__uint_as_float(sv[q]), c2, -mn)) : 0.f;
+              const float p1 = q + 1 < lim ? ex2f(__fmaf_rn(__uint_as_float(sv[q + 1]), c2, -mn)) : 0.f;
+              const __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
+              pk[q >> 1] = *reinterpret_cast<const uint32_t*>(&pp);
+              s4[q & 3] = __fadd_rn(s4[q & 3], p0);
+              s4[(q + 1) & 3] = __fadd_rn(s4[(q + 1) & 3], p1);
+            }
+          }
+        }
+        const float ls = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
+        if (threadIdx.x == 0) TRACE(0, tix, 10, g);
+        if (j > 0 && warp_live && __any_sync(0xffffffffu, grow)) {  // O must be stable: the previous PV is complete
+          mbar_wait(pv_done + ((g - 1) & 1), ((g - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int q2 = 0; q2 < 2; ++q2) {
+            uint32_t o[32];
+            const uint32_t col = tl + kTmemO + half * 64 + q2 * 32;
+            tmem_ld32(col, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__fmul_rn(__uint_as_float(o[e]), alpha));
+            tmem_st32(col, o);
+          }
+        }
+        if (threadIdx.x == 0) TRACE(0, tix, 11, g);
+        if (warp_live) tmem_st16(tl + b * 64 + half * 16, pk);  // P[b] over the S[b] columns both halves read
+        tmem_wait_st();
+        l = __fmaf_rn(l, alpha, ls);  // this half's running sum (the halves are added at the end)
+        m = mn;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full + b);
+        if (threadIdx.x == 0) TRACE(0, tix, 2, g);
+      }
+      mbar_wait(pv_done + ((g - 1) & 1), ((g - 1) >> 1) & 1);  // the task's last PV
+      if (threadIdx.x == 0) TRACE(0, tix, 3, g);
+      tc_fence_after();
+      float* po = valid ? a.po + part_idx(a, node, h, k.r) * kAttnHeadDim + half * 64 : nullptr;
+      if (warp_live) {
+#pragma unroll 1
+        for (int q2 = 0; q2 < 2; ++q2) {
+          uint32_t o[32];
+          tmem_ld32(tl + kTmemO + half * 64 + q2 * 32, o);
+          tmem_wait_ld();
+          if (valid)
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(po + q2 * 32 + e) =
+                  make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]), __uint_as_float(o[e + 2]),
+                              __uint_as_float(o[e + 3]));
+        }
+      }
+      if (threadIdx.x == 0) TRACE(0, tix, 12, g);
+      tc_fence_before();  // the next task's first PV (accumulate = 0) overwrites O after our p_full arrival
+      xl[half][t] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp & 3)) : "memory");
+      if (valid && half == 0) {
+        a.pm[part_idx(a, node, h, k.r)] = m;
+        a.pl[part_idx(a, node, h, k.r)] = __fadd_rn(xl[0][t], xl[1][t]);
+      }
+      if (threadIdx.x == 0) TRACE(0, tix, 13, g);
     }
-  };
-  stage(c0, 0);
-  const int ra = 16 * warp + g, rb = ra + 8;
-  const bool busy = 16 * warp < rows;
-  const bool va = ra < rows, vb = rb < rows;
-  const int ia = base + (va ? ra % nreal : 0), ib = base + (vb ? rb % nreal : 0);
-  const int ha = kh * grp + (va ? ra / nreal : 0), hb = kh * grp + (vb ? rb / nreal : 0);
-  const int Ca = va ? chunked_slots(lv, ia) : 0, Cb = vb ? chunked_slots(lv, ib) : 0;
-  uint32_t qa[8][4];
-  {
-    const __nv_bfloat16* qra = a.q + (size_t)ia * a.q_stride + ha * kAttnHeadDim;
-    const __nv_bfloat16* qrb = a.q + (size_t)ib * a.q_stride + hb * kAttnHeadDim;
+  } else if (warp == 8) {
+    // ---- K/V producer ----
+    if (lane == 0) {
+      int g = 0, it = 0;
+      for (int task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
+        const RunTask k = run_task(G, task);
+        const AttnArgs& a = G.m[k.gi].a;
+        // the task's query rows: two TMA boxes (dims 0-63, 64-127) of 128 (node, head) rows
+        if (it > 0) mbar_wait(q_free, (it - 1) & 1);  // every S of the previous task has read the tile
+        mbar_expect_tx(q_full, kQBytes);
+        const int grp = a.H / a.KV;
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      qa[kk][0] = va ? ld_b32(qra + 16 * kk + 2 * tig) : 0u;
-      qa[kk][1] = vb ? ld_b32(qrb + 16 * kk + 2 * tig) : 0u;
-      qa[kk][2] = va ? ld_b32(qra + 16 * kk + 8 + 2 * tig) : 0u;
-      qa[kk][3] = vb ? ld_b32(qrb + 16 * kk + 8 + 2 * tig) : 0u;
+        for (int kb = 0; kb < 2; ++kb)
+          tma_load_3d(sQ + kb * (kQBytes / 2), &a.qmap, kb * 64, k.kh * grp, a.q_row0 + k.base, q_full);
+        TRACE(2, tix, 7, it);
+        for (int j = 0; j < k.nch; ++j, ++g) {
+          const int s = g & 1;
+          if (g >= kKvStages) mbar_wait(kv_empty + s, ((g >> 1) - 1) & 1);
+          TRACE(1, tix, 4, g);
+          const int row = (k.c0 + j) * kAttnChunk;
+          uint8_t* dst = sKV + s * kChunkBytes;
+          mbar_expect_tx(kv_full + s, kChunkBytes);
+          bulk_g2s(dst, kv_block(a.ptab, a.KV, 0, k.kh, row), kPageBlockBytes, kv_full + s);
+          bulk_g2s(dst + kPageBlockBytes, kv_block(a.ptab, a.KV, 1, k.kh, row), kPageBlockBytes, kv_full + s);
+        }
+      }
     }
-  }
-  float M[2] = {-INFINITY, -INFINITY}, L[2] = {0.f, 0.f};
-  float O[16][4];
+    __syncwarp();
+  } else {
+    // ---- MMA issuer (lane 0) ----
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc_bf16_f32(kRowsPerCta, kAttnChunk);
+      constexpr uint32_t idPV = idesc_bf16_f32(kRowsPerCta, kAttnHeadDim) | (1u << 16);  // B (V) MN-major
+      int gs = 0, it = 0;  // S issued (global chunk index), task iteration
+      auto issue_s = [&](bool last) {
+        const int b = gs & 1;
+        mbar_wait(kv_full + b, (gs >> 1) & 1);
+        if (gs >= 2) mbar_wait(pv_done + b, ((gs >> 1) - 1) & 1);  // P of chunk gs - 2 consumed: S[b] free
+        TRACE(3, tix, 5, gs);
+        tc_fence_after();
+        const uint8_t* sK = sKV + b * kChunkBytes;
 #pragma unroll
-  for (int nd = 0; nd < 16; ++nd) O[nd][0] = O[nd][1] = O[nd][2] = O[nd][3] = 0.f;
-  for (int c = c0; c < c1; ++c) {
-    const int buf = (c - c0) & 1;
-    if (c + 1 < c1) stage(c + 1, buf ^ 1);
-#ifdef TP_ATTN_PRINTF
-    if (threadIdx.x == 0) printf("blk %d c %d c0 %d c1 %d max_c %d rows %d\n", blockIdx.x, c, c0, c1, max_c, rows);
-#endif
-    sm100::mbar_wait(bars + buf, ((c - c0) >> 1) & 1);
-#ifdef TP_ATTN_PRINTF
-    if (threadIdx.x == 0) printf("blk %d c %d waited\n", blockIdx.x, c);
-#endif
-    __syncthreads();  // the zero-filled V rows of a partial chunk are visible too
-    const int j0 = c * kAttnChunk;
-    const int lim[2] = {min(kAttnChunk, max(0, Ca - j0)), min(kAttnChunk, max(0, Cb - j0))};
-    // warp-uniform: the MMAs and shuffles below need every lane of the warp
-    if (busy && __any_sync(0xffffffffu, lim[0] > 0 || lim[1] > 0)) {
-      const __nv_bfloat16* sK = smt + (size_t)buf * 2 * kTileElems;
-      float m[2], l[2], sa[2], sb[2];
-      uint32_t pa[4][4];
-      chunk_scores(qa, sK, lim, a.scale, m, l, pa, lane);
-      merge_scale_live(M[0], L[0], m[0], l[0], lim[0] > 0, sa[0], sb[0]);
-      merge_scale_live(M[1], L[1], m[1], l[1], lim[1] > 0, sa[1], sb[1]);
-      auto merge_part = [&](auto part_tag) {  // PV a quarter of the dims at a time, merged at once
-        constexpr int PT = decltype(part_tag)::value;
-        float o[4][4];
-        chunk_pv_part<PT, 4>(pa, sK + kTileElems, o, lane);
+        for (int kb = 0; kb < 2; ++kb) {
+          const uint64_t ad = desc_kmajor_sw128(sQ + kb * (kQBytes / 2));
+          const uint64_t bd = desc_kmajor_sw128(sK + kb * (kPageBlockBytes / 2));
 #pragma unroll
-        for (int nd = 0; nd < 4; ++nd)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            O[4 * PT + nd][e] = merge_val(O[4 * PT + nd][e], o[nd][e], sa[e >> 1], sb[e >> 1]);
+          for (int q = 0; q < 4; ++q) mma_bf16(tmem + b * 64, ad + 2 * q, bd + 2 * q, idS, (kb | q) ? 1u : 0u);
+        }
+        mma_commit(s_full + b);
+        if (last) mma_commit(q_free);  // the Q loader may refill the tile once these MMAs complete
+        ++gs;
       };
-      merge_part(std::integral_constant<int, 0>{});
-      merge_part(std::integral_constant<int, 1>{});
-      merge_part(std::integral_constant<int, 2>{});
-      merge_part(std::integral_constant<int, 3>{});
+      for (int task = blockIdx.x; task < ntasks; task += gridDim.x, ++it) {
+        const RunTask k = run_task(G, task);
+        mbar_wait(q_full, it & 1);
+        issue_s(k.nch == 1);
+        for (int j = 0; j < k.nch; ++j) {
+          if (j + 1 < k.nch) issue_s(j + 2 == k.nch);
+          const int gc = gs - (j + 1 < k.nch ? 2 : 1);  // chunk whose PV is next
+          const int b = gc & 1;
+          mbar_wait(p_full + b, (gc >> 1) & 1);
+          TRACE(3, tix, 6, gc);
+          tc_fence_after();
+          const uint8_t* sV = sKV + b * kChunkBytes + kPageBlockBytes;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)  // 16 slots per MMA: 8 packed P columns, 2 8-row atoms of V
+            mma_bf16_ts(tmem + kTmemO, tmem + b * 64 + 8 * q, desc_mnmajor_sw128(sV + q * 2048, kPageBlockBytes / 2),
+                        idPV, (j > 0 || q > 0) ? 1u : 0u);
+          mma_commit(pv_done + b);
+          mma_commit(kv_empty + b);
+        }
+      }
     }
-    __syncthreads();  // buffer `buf` is restaged for chunk c + 2
+    __syncwarp();
   }
-  if (!busy) return;
-#pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    if (!(hh ? vb : va)) continue;
-    const size_t idx = part_idx(a, hh ? ib : ia, hh ? hb : ha, r);
-    float* po = a.po + idx * kAttnHeadDim;
-#pragma unroll
-    for (int nd = 0; nd < 16; ++nd)
-      *reinterpret_cast<float2*>(po + nd * 8 + 2 * tig) = make_float2(O[nd][2 * hh], O[nd][2 * hh + 1]);
-    if (tig == 0) {
-      a.pm[idx] = M[hh];
-      a.pl[idx] = L[hh];
-    }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
   }
 }
 
-// The cache row of the rank-th (0-based) speculative ancestor of a node: its
-// packed ancestor bit-row is walked word by word in registers (popcount to skip
-// whole words, __fns for the bit inside the word) — no host-side decode.
-__device__ __forceinline__ int ancestor_row(const uint64_t* __restrict__ bits, int rank, int bits_base) {
-  for (int w = 0;; ++w) {
-    const uint64_t x = __ldg(bits + w);
-    const int pc = __popcll(x);
-    if (rank < pc) {
-      const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-      const int plo = __popc(lo);
-      const int bit = rank < plo ? (int)__fns(lo, 0, rank + 1) : 32 + (int)__fns(hi, 0, rank - plo + 1);
-      return bits_base + 64 * w + bit;
-    }
-    rank -= pc;
-  }
-}
+// ---- per-node suffix + ordered merge --------------------------------------------
 
-// One warp per (node, query head): suffix partial of the last kSuffix slots on the
-// FMA pipes (before griddepcontrol.wait when `early`), then the ordered merge of
-// the chunk kernel's run states, the suffix last, and the bf16 output row.
-__global__ void __launch_bounds__(kWarps * 32) attn_tail_kernel(const __grid_constant__ AttnGroup G, int early) {
+// One CTA per (member, node, 8 query heads).  Warp 0 resolves the node's suffix
+// slots (prefix tail rows, ancestors decoded from the packed bit-row, self) to
+// (page, row-in-page) pairs in shared memory.  Warp w then takes query head
+// 8*hb + w: lanes j and j + 16 compute slot j's score over dims [0, 64) and
+// [64, 128) (sequential FMAs, halves added), the softmax runs over the 16 slot
+// lanes, and P.V runs with lane l owning dims 4l..4l+3 (slots in order) — all
+// before griddepcontrol.wait when `early`; then the run states are merged in
+// order, the suffix last, and the bf16 output row is written.
+__global__ void __launch_bounds__(kTailWarps * 32) attn_tail_kernel(const __grid_constant__ AttnGroup G, int early) {
   if (!early) pdl_wait();
   pdl_trigger();  // the O-projection GEMM may start streaming its weights
+  __shared__ const char* spg[kAttnSuffix];  // page base of the slot's row (nullptr: a self buffer row)
+  __shared__ int sr[kAttnSuffix];           // row within the page
+  __shared__ __align__(16) float sq[kTailWarps][kAttnHeadDim];
   const int gi = member_of(G, blockIdx.x, 1);
   const AttnArgs& a = G.m[gi].a;
   const LevelDev& lv = G.m[gi].lv;
+  const int hbs = (a.H + kTailWarps - 1) / kTailWarps;
   const int local = blockIdx.x - G.m[gi].cta_tail;
-  const int h = local % a.H;
+  const int i = local / hbs, hb = local % hbs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = (local / a.H) * kWarps + warp;
-  if (i >= lv.n) {
-    if (early) pdl_wait();
-    return;
-  }
-  const int kh = h / (a.H / a.KV);
-  const __nv_bfloat16* Kh = a.k + (size_t)kh * a.cap * kAttnHeadDim;
-  const __nv_bfloat16* Vh = a.v + (size_t)kh * a.cap * kAttnHeadDim;
   const int P = __ldg(lv.prefix_rows + i);
   const int A = __ldg(lv.anc_cnt + i);
   const int T = P + A + 1;
   const int s0 = max(0, T - kAttnSuffix), ns = T - s0;
-  // lane j < ns: the cache row of suffix slot s0 + j (-1 = self)
-  int my_row = -1;
-  if (lane < ns) {
+  if (warp == 0) {
     const int slot = s0 + lane;
-    if (slot < P)
-      my_row = slot;
-    else if (slot < P + A)
-      my_row = ancestor_row(lv.anc + (size_t)i * lv.words, slot - P, lv.bits_base);
+    int rank = slot - P;  // >= 0: an ancestor slot (< A) or self (== A)
+    int row = lane < ns && slot < P ? slot : -1;
+    const uint64_t* bits = lv.anc + (size_t)i * lv.words;
+    bool found = !(lane < ns && rank >= 0 && rank < A);
+    for (int w0 = 0; w0 < lv.words; w0 += 32) {
+      const uint64_t mine = w0 + lane < lv.words ? __ldg(bits + w0 + lane) : 0ull;
+      const int nw = min(32, lv.words - w0);
+      for (int w = 0; w < nw; ++w) {
+        const uint64_t x = __shfl_sync(0xffffffffu, mine, w);
+        const int pc = __popcll(x);
+        if (!found) {
+          if (rank < pc) {
+            const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+            const int plo = __popc(lo);
+            const int bit = rank < plo ? (int)__fns(lo, 0, rank + 1) : 32 + (int)__fns(hi, 0, rank - plo + 1);
+            row = lv.bits_base + 64 * (w0 + w) + bit;
+            found = true;
+          } else {
+            rank -= pc;
+          }
+        }
+      }
+    }
+    if (lane < kAttnSuffix) {
+      const bool self_buf = lane == ns - 1 && a.kself;  // recompute mode: self K/V in side buffers
+      if (row < 0) row = lv.row0 + i;                   // self in the cache (append mode)
+      spg[lane] = self_buf || lane >= ns ? nullptr : a.ptab[row >> 6];
+      sr[lane] = row & 63;
+    }
   }
-  const __nv_bfloat16* kself = a.kself ? a.kself + ((size_t)i * a.KV + kh) * kAttnHeadDim
-                                       : Kh + (size_t)(lv.row0 + i) * kAttnHeadDim;
-  const __nv_bfloat16* vself = a.vself ? a.vself + ((size_t)i * a.KV + kh) * kAttnHeadDim
-                                       : Vh + (size_t)(lv.row0 + i) * kAttnHeadDim;
-  const uint2 qv = *reinterpret_cast<const uint2*>(a.q + (size_t)i * a.q_stride + h * kAttnHeadDim + 4 * lane);
-  const float q0 = __uint_as_float(qv.x << 16), q1 = __uint_as_float(qv.x & 0xffff0000u);
-  const float q2 = __uint_as_float(qv.y << 16), q3 = __uint_as_float(qv.y & 0xffff0000u);
-  // scores of the suffix slots (all loads first)
-  uint2 kr[kAttnSuffix];
-#pragma unroll
-  for (int j = 0; j < kAttnSuffix; ++j) {
-    const int row = __shfl_sync(0xffffffffu, my_row, j);
-    const __nv_bfloat16* kp = row >= 0 ? Kh + (size_t)row * kAttnHeadDim : kself;
-    kr[j] = j < ns ? __ldcg(reinterpret_cast<const uint2*>(kp + 4 * lane)) : make_uint2(0u, 0u);
+  __syncthreads();
+  const int h = hb * kTailWarps + warp;
+  if (h >= a.H) {
+    if (early) pdl_wait();
+    return;
   }
-  float sc[kAttnSuffix];
-  float mx = -INFINITY;
+  const int kh = h / (a.H / a.KV);
+  const int64_t koff = (int64_t)kh * kPageBlockBytes, voff = (int64_t)(a.KV + kh) * kPageBlockBytes;
+  {  // this head's query as floats (broadcast reads below)
+    const uint2 qv = *reinterpret_cast<const uint2*>(a.q + (size_t)i * a.q_stride + h * kAttnHeadDim + 4 * lane);
+    *reinterpret_cast<float4*>(&sq[warp][4 * lane]) =
+        make_float4(__uint_as_float(qv.x << 16), __uint_as_float(qv.x & 0xffff0000u), __uint_as_float(qv.y << 16),
+                    __uint_as_float(qv.y & 0xffff0000u));
+  }
+  __syncwarp();
+  // ---- all K and V loads first (one memory round trip): lanes j (< 16) and
+  // j + 16 take slot j's K over dims [0, 64) / [64, 128); for P.V lane l owns
+  // dims 4l .. 4l+3 of every slot's V row (its half of 16-byte chunk l / 2)
+  const int js = lane & 15, hh = lane >> 4;
+  const int e16 = lane >> 1;
+  const int lane_off = ((e16 >> 3) << 13) + (lane & 1) * 8;
+  uint4 kc[8];
+  {
+    const char* pg = spg[js];
+    const int r = sr[js];
+    const bool live = js < ns;
+    const char* blk = pg ? pg + koff + (hh << 13) + (r << 7) : nullptr;
+    const uint4* kp = reinterpret_cast<const uint4*>(a.kself + ((size_t)i * a.KV + kh) * kAttnHeadDim + hh * 64);
 #pragma unroll
-  for (int j = 0; j < kAttnSuffix; ++j) {
-    float d = __fmul_rn(q0, __uint_as_float(kr[j].x << 16));
-    d = __fmaf_rn(q1, __uint_as_float(kr[j].x & 0xffff0000u), d);
-    d = __fmaf_rn(q2, __uint_as_float(kr[j].y << 16), d);
-    d = __fmaf_rn(q3, __uint_as_float(kr[j].y & 0xffff0000u), d);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d = __fadd_rn(d, __shfl_xor_sync(0xffffffffu, d, o));
-    sc[j] = j < ns ? __fmul_rn(d, a.scale) : -INFINITY;
-    mx = fmaxf(mx, sc[j]);
+    for (int c = 0; c < 8; ++c)
+      kc[c] = !live ? make_uint4(0u, 0u, 0u, 0u)
+                    : pg ? __ldcg(reinterpret_cast<const uint4*>(blk + ((c ^ (r & 7)) << 4))) : __ldcg(kp + c);
   }
   uint2 vr[kAttnSuffix];
 #pragma unroll
   for (int j = 0; j < kAttnSuffix; ++j) {
-    const int row = __shfl_sync(0xffffffffu, my_row, j);
-    const __nv_bfloat16* vp = row >= 0 ? Vh + (size_t)row * kAttnHeadDim : vself;
-    vr[j] = j < ns ? __ldcg(reinterpret_cast<const uint2*>(vp + 4 * lane)) : make_uint2(0u, 0u);
+    const char* pg = spg[j];
+    const int r = sr[j];
+    vr[j] = j >= ns ? make_uint2(0u, 0u)
+            : pg   ? __ldcg(reinterpret_cast<const uint2*>(pg + voff + lane_off + (r << 7) + (((e16 & 7) ^ (r & 7)) << 4)))
+                   : __ldcg(reinterpret_cast<const uint2*>(a.vself + ((size_t)i * a.KV + kh) * kAttnHeadDim + 4 * lane));
   }
-  float ls = 0.f;
+  float sc;
+  {
+    float d = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 qa = *reinterpret_cast<const float4*>(&sq[warp][hh * 64 + 8 * c]);
+      const float4 qb = *reinterpret_cast<const float4*>(&sq[warp][hh * 64 + 8 * c + 4]);
+      d = __fmaf_rn(qa.x, __uint_as_float(kc[c].x << 16), d);
+      d = __fmaf_rn(qa.y, __uint_as_float(kc[c].x & 0xffff0000u), d);
+      d = __fmaf_rn(qa.z, __uint_as_float(kc[c].y << 16), d);
+      d = __fmaf_rn(qa.w, __uint_as_float(kc[c].y & 0xffff0000u), d);
+      d = __fmaf_rn(qb.x, __uint_as_float(kc[c].z << 16), d);
+      d = __fmaf_rn(qb.y, __uint_as_float(kc[c].z & 0xffff0000u), d);
+      d = __fmaf_rn(qb.z, __uint_as_float(kc[c].w << 16), d);
+      d = __fmaf_rn(qb.w, __uint_as_float(kc[c].w & 0xffff0000u), d);
+    }
+    const float other = __shfl_xor_sync(0xffffffffu, d, 16);
+    sc = js < ns ? __fmul_rn(hh ? __fadd_rn(other, d) : __fadd_rn(d, other), score_scale(a.scale)) : -INFINITY;
+  }
+  float mx = sc;
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float p = js < ns ? ex2f(__fsub_rn(sc, mx)) : 0.f;
+  float ls = p;
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) ls = __fadd_rn(ls, __shfl_xor_sync(0xffffffffu, ls, o));
+  const float pb = __bfloat162float(__float2bfloat16_rn(p));  // P rounded to bf16, as the run path
   float4 os = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < kAttnSuffix; ++j) {
-    if (j >= ns) break;
-    const float p = fast_exp(__fsub_rn(sc[j], mx));
-    ls = __fadd_rn(ls, p);
-    const float pb = __bfloat162float(__float2bfloat16_rn(p));  // P rounded to bf16, as the chunk path
-    os.x = __fmaf_rn(pb, __uint_as_float(vr[j].x << 16), os.x);
-    os.y = __fmaf_rn(pb, __uint_as_float(vr[j].x & 0xffff0000u), os.y);
-    os.z = __fmaf_rn(pb, __uint_as_float(vr[j].y << 16), os.z);
-    os.w = __fmaf_rn(pb, __uint_as_float(vr[j].y & 0xffff0000u), os.w);
+  for (int j = 0; j < kAttnSuffix; ++j) {  // slots in order (p = 0 past ns)
+    const float pj = __shfl_sync(0xffffffffu, pb, j);
+    os.x = __fmaf_rn(pj, __uint_as_float(vr[j].x << 16), os.x);
+    os.y = __fmaf_rn(pj, __uint_as_float(vr[j].x & 0xffff0000u), os.y);
+    os.z = __fmaf_rn(pj, __uint_as_float(vr[j].y << 16), os.z);
+    os.w = __fmaf_rn(pj, __uint_as_float(vr[j].y & 0xffff0000u), os.w);
   }
-  if (early) pdl_wait();  // the chunk kernel's run states are complete from here on
-  // ordered merge: runs of the chunked part, then the suffix
+  if (early) pdl_wait();  // the run kernel's states are complete from here on
   float M = -INFINITY, L = 0.f;
   float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
   const int C = max(0, T - kAttnSuffix);
@@ -663,44 +681,42 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
   AttnGroup G;
   G.count = count;
   G.run = g_attn_run;
-  const int kRun = G.run;
-  int cs = 0, ct = 0;
+  int cr = 0, ct = 0;
   for (int g = 0; g < count; ++g) {
     AttnMember& m = G.m[g];
     m.a = a[g];
     m.lv = lv[g];
     const int grp = a[g].H / a[g].KV;
-    TP_CHECK(grp >= 1 && kCtaRows % grp == 0, TP_ESHAPE, "query group size must divide 64");
-    m.max_c = std::max(0, lv[g].max_t - kAttnSuffix);  // longest chunked part of the member
-    m.c_shared = (m.max_c + kAttnChunk - 1) / kAttnChunk;
-    m.small = kRun <= kWarps && lv[g].n * grp <= kSmallRows;
-    m.zt = m.small ? (lv[g].n * grp + 15) / 16 : (lv[g].n + kCtaRows / grp - 1) / (kCtaRows / grp);
-    TP_CHECK(m.c_shared <= a[g].max_chunks, TP_ESHAPE, "attention chunks exceed scratch");
-    m.cta_shared = cs;
+    TP_CHECK(grp >= 1 && kRowsPerCta % grp == 0, TP_ESHAPE, "query group size must divide 128");
+    const int max_c = std::max(0, lv[g].max_t - kAttnSuffix);  // longest chunked part of the member
+    m.c_hi = (max_c + kAttnChunk - 1) / kAttnChunk;
+    m.blocks = (lv[g].n * grp + kRowsPerCta - 1) / kRowsPerCta;
+    TP_CHECK((m.c_hi + G.run - 1) / G.run <= a[g].max_chunks, TP_ESHAPE, "attention runs exceed scratch");
+    m.cta_run = cr;
     m.cta_tail = ct;
-    m.cta_gqa = 0;
-    cs += a[g].KV * ((m.c_shared + kRun - 1) / kRun) * m.zt;
-    ct += a[g].H * ((lv[g].n + kWarps - 1) / kWarps);
+    cr += a[g].KV * ((m.c_hi + G.run - 1) / G.run) * m.blocks;
+    ct += lv[g].n * ((a[g].H + kTailWarps - 1) / kTailWarps);
   }
   static bool attr_set[64] = {false};  // per device
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
   if (!attr_set[dev & 63]) {
-    TP_CUDA(cudaFuncSetAttribute(attn_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChunksSmem));
+    TP_CUDA(cudaFuncSetAttribute(attn_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRunSmem));
     attr_set[dev & 63] = true;
   }
-  static const int dbg = getenv("TP_ATTN_DEBUG") ? atoi(getenv("TP_ATTN_DEBUG")) : 0;  // diagnostics: 1 skip tail, 2 skip chunks
-  if (dbg & 2) cs = 0;
+  static const int dbg = getenv("TP_ATTN_DEBUG") ? atoi(getenv("TP_ATTN_DEBUG")) : 0;  // diagnostics: 1 skip tail, 2 skip runs
+  if (dbg & 2) cr = 0;
   if (dbg & 1) ct = 0;
-  if (cs > 0) {
+  if (cr > 0) {
     ::tp::count_launch();
-    TP_CUDA(launch_pdl(attn_chunks_kernel, dim3(cs), dim3(kWarps * 32), kChunksSmem, st, G));
+    const int grid = std::min(cr, 2 * num_sms());  // persistent: two CTAs per SM walk the tasks
+    TP_CUDA(launch_pdl(attn_run_kernel, dim3(grid), dim3(kRunThreads), (size_t)kRunSmem, st, G, cr));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_shared", st);
   }
   if (ct > 0) {
     ::tp::count_launch();
-    TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kWarps * 32), 0, st, G, cs > 0 ? 1 : 0));
+    TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kTailWarps * 32), 0, st, G, cr > 0 ? 1 : 0));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tail", st);
   }
@@ -708,6 +724,12 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
 }
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st) { return attn_tree_group(&a, &lv, 1, st); }
+
+int attn_set_trace(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  TP_CUDA(cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)));
+  return TP_OK;
+}
 
 int attn_set_run(int run) {
   TP_CHECK(run >= 1 && run <= 64, TP_ECONFIG, "attention run length outside [1, 64]");

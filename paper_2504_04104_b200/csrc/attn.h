@@ -1,27 +1,31 @@
 // K1: tree-masked attention for the Llama path (see attn.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include "internal.h"
+#include "kvpage.cuh"
 
 namespace tp {
 
-constexpr int kAttnChunk = 64;     // logical key slots per canonical chunk
-constexpr int kAttnSuffix = 16;    // node-specific window at the end of the key sequence (> ancestors)
-constexpr int kAttnMaxExtra = 64;  // speculative ancestor rows per node
+constexpr int kAttnChunk = kPageRows;  // logical key slots per canonical chunk (== one KV page)
+constexpr int kAttnSuffix = 16;        // node-specific window at the end of the key sequence (> ancestors)
+constexpr int kAttnMaxExtra = 64;      // speculative ancestor rows per node
 constexpr int kAttnHeadDim = 128;
 constexpr int kAttnMaxGroup = 64;  // (request, stage) items per grouped launch (large kernel params)
 
 struct AttnArgs {
-  const __nv_bfloat16* q;  // [n][H*128]
+  CUtensorMap qmap;        // the workspace's query rows as [nodes][H][128] (make_tmap_q3d)
+  int q_row0;              // this item's first node in qmap
+  const __nv_bfloat16* q;  // [n][H*128] (= qmap rows q_row0 ..)
   int q_stride;
-  const __nv_bfloat16* k;  // cache [KV][cap][128]
-  const __nv_bfloat16* v;
+  const char* const* ptab;  // this layer's page table row: page base per 64 cache rows
   int cap;
   const __nv_bfloat16* kself;  // self rows: [n][KV][128] (recompute) or nullptr (cache rows row0+i)
   const __nv_bfloat16* vself;
   int H, KV;
   float scale;
-  float* pm;  // [n][H][max_chunks] per-run max          (shared runs only)
+  float* pm;  // [n][H][max_chunks] per-run max
   float* pl;  // per-run sum
   float* po;  // [n][H][max_chunks][128] per-run unnormalised output
   int max_chunks;
@@ -29,17 +33,14 @@ struct AttnArgs {
   int out_stride;
 };
 
-// One grouped launch pair covers the same layer slot of several stages.
+// One grouped launch pair covers the same layer slot of several stages / requests.
 struct AttnMember {
   AttnArgs a;
   LevelDev lv;
-  int c_shared;    // chunks of the member's longest chunked part (slots [0, T - kAttnSuffix))
-  int max_c;       // slots of that part
-  int zt;          // row blocks of the shared launch (64 rows; 16-row tiles when `small`)
-  int small;       // few rows: the run's chunks in parallel across warps
-  int cta_shared;  // first CTA of this member in the shared launch
-  int cta_tail;    // first CTA of this member in the per-node tail launch (empty range for GQA)
-  int cta_gqa;     // first CTA of this member in the GQA tail launch (one CTA per node and KV head)
+  int c_hi;      // chunks of the member's longest chunked part (slots [0, T - kAttnSuffix))
+  int blocks;    // 128-row blocks of (node, query head) rows
+  int cta_run;   // first CTA of this member in the run launch
+  int cta_tail;  // first CTA of this member in the tail launch
 };
 
 struct AttnGroup {
@@ -47,10 +48,12 @@ struct AttnGroup {
   int count;
   int run;  // canonical chunks per run
 };
+static_assert(sizeof(AttnGroup) <= 32000, "AttnGroup must fit the 32 KB kernel-parameter limit");
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);
 int attn_set_run(int run);
-// members[0..count) -> two launches (shared chunks, then per-node tail + ordered combine)
+int attn_set_trace(void* dev_buf);  // diagnostics (-DTP_ATTN_TRACE builds): [grid][8 roles][1024] u64
+// members[0..count) -> two launches (run states on tcgen05, then per-node suffix + ordered merge)
 int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st);
 
 }  // namespace tp

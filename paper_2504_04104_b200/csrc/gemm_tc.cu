@@ -41,6 +41,7 @@
 #include <vector>
 
 #include "gemm_tc.h"
+#include "kvpage.cuh"
 #include "sm100.cuh"
 
 namespace tp {
@@ -99,6 +100,23 @@ int make_tmap_kmajor(CUtensorMap* map, const void* gptr, int64_t rows, int64_t k
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   TP_CHECK(r == CUDA_SUCCESS, TP_ECUDA, "cuTensorMapEncodeTiled failed");
+  return TP_OK;
+}
+
+// Query rows of the attention run kernel: Xq viewed as [nodes][heads][128] bf16,
+// box = 64 dims x grp heads x (128 / grp) nodes, 128-byte swizzle (the smem tile
+// is then the K-major SW128 A operand with row = node * grp + head).
+int make_tmap_q3d(CUtensorMap* map, const void* gptr, int64_t nodes, int heads, int grp) {
+  TP_CHECK(g_encode, TP_ECUDA, "cuTensorMapEncodeTiled unavailable (make_tmap_kmajor initialises it)");
+  TP_CHECK(grp >= 1 && 128 % grp == 0 && heads % grp == 0, TP_ESHAPE, "query group size must divide 128");
+  cuuint64_t dims[3] = {128, (cuuint64_t)heads, (cuuint64_t)nodes};
+  cuuint64_t strides[2] = {256, (cuuint64_t)heads * 256};
+  cuuint32_t box[3] = {64, (cuuint32_t)grp, (cuuint32_t)(128 / grp)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(gptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TP_CHECK(r == CUDA_SUCCESS, TP_ECUDA, "cuTensorMapEncodeTiled (3d query map) failed");
   return TP_OK;
 }
 
@@ -209,24 +227,29 @@ __device__ __forceinline__ void epi_finish(const GemmEpi& e, int mt, int lane, i
       }
       __nv_bfloat16* dst;
       if (mt < e.H) {
-        dst = e.xq + (size_t)c * e.H * kBM + mt * kBM;
+        dst = e.xq + (size_t)c * e.H * kBM + mt * kBM + f;
       } else {
         const bool is_k = mt < e.H + e.KV;
         const int kh = is_k ? mt - e.H : mt - e.H - e.KV;
+        const char* const* tab = nullptr;  // paged cache row of this layer (kvpage.cuh), or a self buffer
+        int row = 0;
         if (e.items) {
           const QkvItem& it = e.items[e.node_item[c]];
-          if (it.append)
-            dst = static_cast<__nv_bfloat16*>(it.planes[2 * (e.layer - it.lo) + (is_k ? 0 : 1)]) +
-                  ((size_t)kh * it.cap + it.row0 + (c - it.off)) * kBM;
-          else
-            dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
+          if (it.append) {
+            tab = it.ptab + (size_t)(e.layer - it.lo) * it.max_pages;
+            row = it.row0 + (c - it.off);
+          }
         } else if (e.append) {
-          dst = (is_k ? e.kc : e.vc) + ((size_t)kh * e.cap + e.row0 + c) * kBM;
-        } else {
-          dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM;
+          tab = e.ptab;
+          row = e.row0 + c;
         }
+        if (tab)  // lane's 8 bytes = half of the row's 16-byte chunk lane/2, swizzled
+          dst = reinterpret_cast<__nv_bfloat16*>(const_cast<char*>(kv_block(tab, e.KV, is_k ? 0 : 1, kh, row)) +
+                                                 page_chunk_off(row & 63, lane >> 1) + (lane & 1) * 8);
+        else
+          dst = (is_k ? e.kself : e.vself) + ((size_t)c * e.KV + kh) * kBM + f;
       }
-      st_bf16x4(dst + f, o.x, o.y, o.z, o.w);
+      st_bf16x4(dst, o.x, o.y, o.z, o.w);
     }
   }
 }

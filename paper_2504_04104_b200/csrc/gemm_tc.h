@@ -33,9 +33,10 @@ enum GemmOp : int {
 // Per-request KV destination of a ragged (multi-request) QKV member: node c of
 // item it = items[node_item[c]] writes its K/V rows to that request's cache.
 struct QkvItem {
-  void* const* planes;  // the request-stage's [2*layers] K/V plane pointers (device)
-  int lo;               // first layer hosted by that stage
-  int cap, row0, append, off;  // plane rows, first appended row, append flag, first node of the item
+  char* const* ptab;  // the request-stage's paged KV table [layers][max_pages] (device, kvpage.cuh)
+  int max_pages;
+  int lo;                 // first layer hosted by that stage
+  int row0, append, off;  // first appended row, append flag, first node of the item
 };
 
 struct GemmEpi {
@@ -43,9 +44,10 @@ struct GemmEpi {
   float* out = nullptr;
   int out_ld = 0;
   // kOpQkv
-  int H = 0, KV = 0, cap = 0, row0 = 0, append = 0;
+  int H = 0, KV = 0, row0 = 0, append = 0;
   const float* rope = nullptr;  // [n][64][2] (cos, sin) per node position
-  __nv_bfloat16 *xq = nullptr, *kc = nullptr, *vc = nullptr, *kself = nullptr, *vself = nullptr;
+  char* const* ptab = nullptr;  // single request: this layer's page table row (kvpage.cuh)
+  __nv_bfloat16 *xq = nullptr, *kself = nullptr, *vself = nullptr;
   const QkvItem* items = nullptr;      // ragged member (nullptr: single request, fields above)
   const int32_t* node_item = nullptr;  // [n]
   int layer = 0;
@@ -81,6 +83,7 @@ struct GemmGroup {
 
 int num_sms();
 int make_tmap_kmajor(CUtensorMap* map, const void* gptr, int64_t rows, int64_t k, int box_rows);
+int make_tmap_q3d(CUtensorMap* map, const void* gptr, int64_t nodes, int heads, int grp);
 SkPlan sk_plan(int n_out, int k, int n);
 inline size_t sk_part_floats(const SkPlan& p) { return (size_t)p.mtiles * p.max_contrib * p.n * 128; }
 // Launched with programmatic dependent launch: the weight prologue overlaps the

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "kvpage.cuh"
 
 // Per-layer weights.  Toy: f64 [in,out] row-major as the reference stores
 // them (model.py:72-80).  Llama: bf16 [out,in] (K-major for the swap-AB
@@ -37,6 +38,10 @@ struct tp_model {
   // live stage is destroyed.
   int live_stages = 0;
   bool destroy_pending = false;
+  // Llama KV page pool (kvpage.cuh): every stage / request of this model draws
+  // its pages here (guarded by pool_mu); slabs are freed with the model.
+  std::vector<char*> page_free;
+  std::vector<void*> page_slabs;
 };
 
 struct tp_stage {
@@ -44,7 +49,11 @@ struct tp_stage {
   int lo = 0, hi = 0;     // hosted layers
   int cap = 0, rows = 0;  // KV capacity / filled rows
   int kv_heads = 1, head_dim = 0, esize = 8;
-  std::vector<void*> k, v;  // per hosted layer [kv_heads][cap][head_dim]
+  std::vector<void*> k, v;  // toy: per hosted layer [kv_heads][cap][head_dim] (flat planes)
+  // llama: paged KV (kvpage.cuh), cap = pages * 64
+  std::vector<char*> ptab;   // host copy of the page table [layers][max_pages]
+  char** d_ptab = nullptr;   // device page table
+  int max_pages = 0;
   // device workspace
   char* ws = nullptr;
   size_t ws_bytes = 0;
@@ -62,7 +71,7 @@ struct tp_stage {
   // verify result staging
   int32_t* d_result = nullptr;
   int32_t* h_result = nullptr;
-  void** d_planes = nullptr;  // [2*layers] K/V plane bases for kv_compact
+  void** d_planes = nullptr;  // toy: [2*layers] K/V plane bases for the compaction kernels
   void* logits = nullptr;     // [logits_rows][vocab] verify scratch (f64 toy / f32 llama)
   int logits_rows = 0;
   void* ext = nullptr;        // arch-specific state (llama: tensor maps, attention partials)
@@ -146,10 +155,9 @@ int argmax_match(const void* logits, int is_f64, int vocab, const int32_t* d_chi
                  int32_t* d_result, cudaStream_t st);
 constexpr int kMaxMulti = 64;
 struct MoveItem {
-  void* const* planes;   // [2*layers] K/V plane bases of the stage
-  int64_t plane_stride;  // bytes between kv-head planes
-  const int32_t* src;    // kept rows (device), increasing
-  int row_bytes, n_keep, first, heads, cta0;
+  KvView kv;            // the stage's K/V storage
+  const int32_t* src;   // kept rows (device), increasing
+  int n_keep, first, cta0;
 };
 struct MoveGroup {
   MoveItem m[kMaxMulti];
@@ -168,8 +176,10 @@ struct RowsGroup {
 };
 int kv_compact_many(const MoveGroup& g, int ctas, cudaStream_t st);
 int rows_compact_many(const RowsGroup& g, int max_rows, cudaStream_t st);
-int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, void** d_planes,
-               cudaStream_t st);
+int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, cudaStream_t st);
+KvView kv_view(const tp_stage* s);
+// rows [lo, hi) of one layer's K (kind 0) or V plane -> device [rows][kv_heads][row bytes]
+int kv_read_rows(const tp_stage* s, int layer, int kind, int lo, int hi, void* d_out, cudaStream_t st);
 int rows_compact(const void* src, void* dst, int64_t row_bytes, const int32_t* d_idx, int n_out,
                  cudaStream_t st);
 

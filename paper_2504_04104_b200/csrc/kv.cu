@@ -19,33 +19,13 @@ namespace tp {
 constexpr int kMoveThreads = 256;
 constexpr int kMoveChunkBytes = 32 * 1024;
 
-__global__ void __launch_bounds__(kMoveThreads) kv_move_kernel(void* const* __restrict__ planes,
-                                                               int64_t plane_stride_bytes, int row_bytes,
-                                                               const int32_t* __restrict__ src_rows,
+// One stage: CTA (plane = 2 * layer + kind, kv head).
+__global__ void __launch_bounds__(kMoveThreads) kv_move_kernel(const KvView v, const int32_t* __restrict__ src_rows,
                                                                int n_keep, int first) {
   pdl_wait();
   pdl_trigger();
   __shared__ __align__(16) uint4 stage[kMoveChunkBytes / 16];
-  char* base = (char*)planes[blockIdx.x] + (int64_t)blockIdx.y * plane_stride_bytes;
-  // leading run already in place
-  int j0 = 0;
-  while (j0 < n_keep && src_rows[j0] == first + j0) ++j0;
-  const int vec_per_row = row_bytes / 16;
-  const int rows_per_chunk = max(1, kMoveChunkBytes / row_bytes);
-  for (int c = j0; c < n_keep; c += rows_per_chunk) {
-    int cnt = min(rows_per_chunk, n_keep - c);
-    int total = cnt * vec_per_row;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      int r = t / vec_per_row, e = t % vec_per_row;
-      stage[t] = reinterpret_cast<const uint4*>(base + (int64_t)src_rows[c + r] * row_bytes)[e];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      int r = t / vec_per_row, e = t % vec_per_row;
-      reinterpret_cast<uint4*>(base + (int64_t)(first + c + r) * row_bytes)[e] = stage[t];
-    }
-    __syncthreads();
-  }
+  kv_move_plane<kMoveChunkBytes>(v, blockIdx.x >> 1, blockIdx.x & 1, blockIdx.y, src_rows, n_keep, first, stage);
 }
 
 // Several stages' compactions in one launch: CTA -> (item, plane, kv-head).
@@ -57,28 +37,25 @@ __global__ void __launch_bounds__(kMoveThreads) kv_move_multi_kernel(const __gri
   while (it + 1 < G.count && (int)blockIdx.x >= G.m[it + 1].cta0) ++it;
   const MoveItem& M = G.m[it];
   const int local = blockIdx.x - M.cta0;
-  const int plane = local / M.heads, head = local % M.heads;
-  char* base = (char*)M.planes[plane] + (int64_t)head * M.plane_stride;
-  const int32_t* src_rows = M.src;
-  const int n_keep = M.n_keep, first = M.first, row_bytes = M.row_bytes;
-  int j0 = 0;
-  while (j0 < n_keep && src_rows[j0] == first + j0) ++j0;
-  const int vec_per_row = row_bytes / 16;
-  const int rows_per_chunk = max(1, kMoveChunkBytes / row_bytes);
-  for (int c = j0; c < n_keep; c += rows_per_chunk) {
-    const int cnt = min(rows_per_chunk, n_keep - c);
-    const int total = cnt * vec_per_row;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      const int r = t / vec_per_row, e = t % vec_per_row;
-      stage[t] = reinterpret_cast<const uint4*>(base + (int64_t)src_rows[c + r] * row_bytes)[e];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      const int r = t / vec_per_row, e = t % vec_per_row;
-      reinterpret_cast<uint4*>(base + (int64_t)(first + c + r) * row_bytes)[e] = stage[t];
-    }
-    __syncthreads();
-  }
+  const int plane = local / M.kv.heads, head = local % M.kv.heads;
+  kv_move_plane<kMoveChunkBytes>(M.kv, plane >> 1, plane & 1, head, M.src, M.n_keep, M.first, stage);
+}
+
+// rows [lo, hi) of one plane -> out [rows][heads][row bytes] (debug / test reads)
+__global__ void kv_read_kernel(const KvView v, int l, int kind, int lo, uint4* __restrict__ out) {
+  const int row = lo + blockIdx.x, head = blockIdx.y;
+  const int vec_per_row = v.row_bytes / 16;
+  uint4* o = out + ((size_t)blockIdx.x * v.heads + head) * vec_per_row;
+  for (int e = threadIdx.x; e < vec_per_row; e += blockDim.x)
+    o[e] = *reinterpret_cast<const uint4*>(kv_chunk(v, l, kind, head, row, e));
+}
+
+int kv_read_rows(const tp_stage* s, int layer, int kind, int lo, int hi, void* d_out, cudaStream_t st) {
+  if (hi <= lo) return TP_OK;
+  kv_read_kernel<<<dim3(hi - lo, s->kv_heads), 128, 0, st>>>(kv_view(s), layer - s->lo, kind, lo,
+                                                               static_cast<uint4*>(d_out));
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
 }
 
 int kv_compact_many(const MoveGroup& g, int ctas, cudaStream_t st) {
@@ -108,18 +85,15 @@ int rows_compact_many(const RowsGroup& g, int max_rows, cudaStream_t st) {
   return TP_OK;
 }
 
-int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, void** d_planes,
-               cudaStream_t st) {
-  int nl = s->hi - s->lo;
-  int row_bytes = s->head_dim * s->esize;
-  TP_CHECK(row_bytes % 16 == 0, TP_ESHAPE, "KV row bytes must be a multiple of 16");
-  TP_CHECK(row_bytes <= kMoveChunkBytes, TP_ESHAPE, "KV row too large for the compaction kernel");
+int kv_compact(tp_stage* s, const int32_t* d_src_rows, int n_keep, int first, cudaStream_t st) {
+  const int nl = s->hi - s->lo;
+  const KvView v = kv_view(s);
+  TP_CHECK(v.row_bytes % 16 == 0, TP_ESHAPE, "KV row bytes must be a multiple of 16");
+  TP_CHECK(v.row_bytes <= kMoveChunkBytes, TP_ESHAPE, "KV row too large for the compaction kernel");
   if (n_keep == 0 || nl == 0) return TP_OK;
-  int64_t plane = (int64_t)s->cap * row_bytes;  // one kv-head plane
-  dim3 grid(2 * nl, s->kv_heads);
   ::tp::count_launch();
-  TP_CUDA(launch_pdl(kv_move_kernel, grid, dim3(kMoveThreads), 0, st, (void* const*)d_planes, (int64_t)plane, row_bytes,
-                     d_src_rows, n_keep, first));
+  TP_CUDA(launch_pdl(kv_move_kernel, dim3(2 * nl, s->kv_heads), dim3(kMoveThreads), 0, st, v, d_src_rows, n_keep,
+                     first));
   TP_CUDA(cudaGetLastError());
   return TP_OK;
 }

@@ -43,6 +43,7 @@ struct LlamaWs {
   int ctr_stride = 0;
   float* rope = nullptr;  // [np][64][2]
   CUtensorMap mXd, mXo, mXf;
+  CUtensorMap mXq3;  // query rows for the attention run kernel (make_tmap_q3d)
   float *pm = nullptr, *pl = nullptr, *po = nullptr;
   int max_chunks = 0;
 };
@@ -341,6 +342,7 @@ static int ws_get(tp_model* m, int g, int min_chunks, LlamaWs** out) {
     TP_CUDA(cudaMemset(e->counters, 0, (size_t)kCtrKinds * e->ctr_stride * 4));
     sk_counters_forget(e->counters, (size_t)kCtrKinds * e->ctr_stride * 4);
     TP_TRY(make_tmap_kmajor(&e->mXd, e->Xd, np, d, 16));
+    TP_TRY(make_tmap_q3d(&e->mXq3, e->Xq, np, c.heads, c.heads / c.kv_heads));
     TP_TRY(make_tmap_kmajor(&e->mXo, e->Xo, np, q, 16));
     TP_TRY(make_tmap_kmajor(&e->mXf, e->Xf, np, f, 16));
   }
@@ -600,7 +602,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       int32_t* ni = reinterpret_cast<int32_t*>(blob.data() + sizeof(QkvItem) * M.count);
       for (int r = 0; r < M.count; ++r) {
         const FwdItem& it = M.items[r];
-        qi[r] = QkvItem{it.s->d_planes, it.s->lo, it.s->cap, it.lv.row0, it.lv.append, offs[g][r]};
+        qi[r] = QkvItem{it.s->d_ptab, it.s->max_pages, it.s->lo, it.lv.row0, it.lv.append, offs[g][r]};
         for (int i = 0; i < it.lv.n; ++i) ni[offs[g][r] + i] = r;
       }
       const char* dptr;
@@ -646,11 +648,9 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       eq.vself = e->vself;
       eq.layer = layer;
       if (M.count == 1) {
-        eq.cap = i0.s->cap;
         eq.row0 = i0.lv.row0;
         eq.append = i0.lv.append;
-        eq.kc = (__nv_bfloat16*)i0.s->k[layer - i0.s->lo];
-        eq.vc = (__nv_bfloat16*)i0.s->v[layer - i0.s->lo];
+        eq.ptab = i0.s->d_ptab + (size_t)(layer - i0.s->lo) * i0.s->max_pages;
       } else {
         eq.items = qitems[g];
         eq.node_item = qnode[g];
@@ -682,8 +682,9 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
         AttnArgs x;
         x.q = e->Xq + off * q;
         x.q_stride = q;
-        x.k = (const __nv_bfloat16*)it.s->k[layer - it.s->lo];
-        x.v = (const __nv_bfloat16*)it.s->v[layer - it.s->lo];
+        x.qmap = e->mXq3;
+        x.q_row0 = (int)off;
+        x.ptab = it.s->d_ptab + (size_t)(layer - it.s->lo) * it.s->max_pages;
         x.cap = it.s->cap;
         x.kself = it.lv.append ? nullptr : e->kself + off * kvd;
         x.vself = it.lv.append ? nullptr : e->vself + off * kvd;

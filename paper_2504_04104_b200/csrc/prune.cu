@@ -29,9 +29,8 @@ constexpr int kPruneMoveThreads = 256;
 constexpr int kPruneChunkBytes = 32 * 1024;
 
 struct PruneItem {
-  void* const* planes;    // [2 * layers] K/V plane bases
-  int64_t plane_stride;   // bytes between kv-head planes
-  int layers, heads, row_bytes;
+  KvView kv;              // the stage's K/V storage (paged Llama cache or flat toy planes)
+  int layers;
   int P, S, off;          // prefix rows, speculative rows = tree nodes [off, off + S)
   int lvl_lo, lvl_n;      // in-flight level
   const char* hsrc;
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(kPruneMoveThreads) prune_move_kernel(const __g
   while (it + 1 < G.count && (int)blockIdx.x >= G.m[it + 1].cta_kv) ++it;
   const PruneItem& M = G.m[it];
   const int local = blockIdx.x - M.cta_kv;
-  const int n_kv = 2 * M.layers * M.heads;
+  const int n_kv = 2 * M.layers * M.kv.heads;
   if (local >= n_kv) {  // hidden-row gather: one CTA per possible survivor
     const int r = local - n_kv;
     if (r >= M.plan[1]) return;
@@ -142,28 +141,8 @@ __global__ void __launch_bounds__(kPruneMoveThreads) prune_move_kernel(const __g
     for (int e = threadIdx.x; e < G.hrow_bytes / 16; e += blockDim.x) d[e] = s[e];
     return;
   }
-  const int plane = local / M.heads, head = local % M.heads;
-  char* base = (char*)M.planes[plane] + (int64_t)head * M.plane_stride;
-  const int32_t* src_rows = M.plan + 2;
-  const int n_keep = M.plan[0], first = M.P, row_bytes = M.row_bytes;
-  int j0 = 0;
-  while (j0 < n_keep && src_rows[j0] == first + j0) ++j0;  // leading run already in place
-  const int vec_per_row = row_bytes / 16;
-  const int rows_per_chunk = max(1, kPruneChunkBytes / row_bytes);
-  for (int c0 = j0; c0 < n_keep; c0 += rows_per_chunk) {
-    const int cnt = min(rows_per_chunk, n_keep - c0);
-    const int total = cnt * vec_per_row;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      const int r = t / vec_per_row, e = t % vec_per_row;
-      stage[t] = reinterpret_cast<const uint4*>(base + (int64_t)src_rows[c0 + r] * row_bytes)[e];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      const int r = t / vec_per_row, e = t % vec_per_row;
-      reinterpret_cast<uint4*>(base + (int64_t)(first + c0 + r) * row_bytes)[e] = stage[t];
-    }
-    __syncthreads();
-  }
+  const int plane = local / M.kv.heads, head = local % M.kv.heads;
+  kv_move_plane<kPruneChunkBytes>(M.kv, plane >> 1, plane & 1, head, M.plan + 2, M.plan[0], M.P, stage);
 }
 
 }  // namespace tp
@@ -231,12 +210,8 @@ extern "C" int tp_prune_device(int32_t count, const tp_prune_stage* stages, cons
       const tp_prune_stage& d = stages[i];
       tp_stage* s = d.stage;
       PruneItem& it = g.m[i - c0];
-      const int rb = s->head_dim * s->esize;
-      it.planes = s->d_planes;
-      it.plane_stride = (int64_t)s->cap * rb;
+      it.kv = kv_view(s);
       it.layers = s->hi - s->lo;
-      it.heads = s->kv_heads;
-      it.row_bytes = rb;
       it.P = d.prefix_rows;
       it.S = d.spec_rows;
       it.off = d.tree_off;
@@ -248,7 +223,7 @@ extern "C" int tp_prune_device(int32_t count, const tp_prune_stage* stages, cons
       it.keep_out = d.keep_out;
       plan += 2 + d.spec_rows + d.level_n;
       it.cta_kv = ctas;
-      ctas += 2 * it.layers * it.heads + d.level_n;
+      ctas += 2 * it.layers * it.kv.heads + d.level_n;
       it.cta_h = ctas - d.level_n;
     }
     ::tp::count_launch();

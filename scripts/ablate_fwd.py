@@ -32,7 +32,7 @@ args = ap.parse_args()
 cfg = model_cfg(args.model)
 m = LlamaModel(cfg, max_nodes=64)
 ns = [int(x) for x in args.n.split(",")]
-depth = 24
+depth = 12  # ancestors per node < 16 (the attention suffix window)
 prompt = [int(t) for t in np.random.default_rng(1).integers(0, cfg.vocab, args.prefix + depth)]
 r = PipelineRunner(m, PipelineConfig(num_stages=len(ns) + 1), tp.BeamConfig(w=64, k=16), None, collect_trace=False,
                    kv_capacity=2048)

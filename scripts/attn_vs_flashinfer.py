@@ -25,7 +25,7 @@ args = ap.parse_args()
 ns = [int(x) for x in args.n.split(",")]
 H = KV = 32
 D = 128
-depth = 24
+depth = 12
 rng = np.random.default_rng(2)
 
 import flashinfer  # noqa: E402

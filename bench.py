@@ -507,7 +507,7 @@ def run_ours(args, rank, world):
     peak, peak_src = peaks()
     achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
     try:  # measured DRAM traffic of the same kernel (committed ncu capture, see profiles/)
-        with open(os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")) as fh:
             cap = json.load(fh)
     except Exception:  # noqa: BLE001
         cap = None
@@ -527,8 +527,11 @@ def run_ours(args, rank, world):
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4),
                      "traffic": cap["traffic_bytes_per_launch"] if cap else None,
-                     "traffic_capture": ({k: cap[k] for k in ("launches", "algorithmic_bytes_per_launch",
-                                                              "traffic_over_algorithmic", "source")}
+                     "traffic_capture": ({**{k: cap[k] for k in ("launches", "algorithmic_bytes_per_launch",
+                                                                 "traffic_over_algorithmic", "source")},
+                                          "note": "a separate ncu capture of the same workload (profiles/); compare "
+                                                  "traffic with its own algorithmic_bytes_per_launch, not with this "
+                                                  "run's bytes_per_launch"}
                                          if cap else None),
                      "peak_source": peak_src,
                      "gemm_share_of_step": round(gemm_ms / prof_total_ms, 4) if prof_total_ms else None,
@@ -581,6 +584,9 @@ def run_ours(args, rank, world):
                                  "ideal_ms_per_step_all_stages_occupied": round(
                                      (args.stages * (cfg.layers // args.stages) * layer_w + head_w) / (peak * 1e6), 4)}
         pr.close()
+    if rank == 0 and line.get("mean_resident_nodes"):
+        line["per_stage"] = stage_profile(args, cfg, model_arg, splits, line["mean_resident_nodes"],
+                                          args.prompt_len + int(round(e2e_tokens / 2)), steps_per_token, peak)
     if not args.no_comparators:
         line["comparators"] = comparators(args, cfg, model_arg, splits, prompt, sync_all)
     if rank == 0 and ngpu == 1 and args.db_batches:
@@ -588,6 +594,77 @@ def run_ours(args, rank, world):
     if rank == 0 and ngpu == 1 and not args.no_c1:
         line["c1_vs_reference"] = c1_leg()
     print(json.dumps(line), flush=True)
+
+
+def stage_profile(args, cfg, model_arg, splits, mean_nodes, ctx, steps_per_token, peak, iters=20):
+    """Each stage's lone forward at its steady-state node count (rounded mean
+    resident nodes of the timed steps) over a `ctx`-row cache, timed with CUDA
+    events — what one stage per GPU would run every step (the last stage with K4
+    verify).  SURVEY 8d per-stage bytes (weights of its layers + prefix K/V +
+    new K/V rows + [first] embeddings + [last] LM head) over that time gives the
+    per-stage roofline fraction; max over stages x steps/token is the projected
+    stage-per-GPU TBT (a projection from one-GPU measurements, not a multi-GPU
+    run)."""
+    import torch
+
+    import paper_2504_04104_b200 as tp
+    from paper_2504_04104_b200.model import forward_members
+    from paper_2504_04104_b200.pipeline import PipelineConfig, PipelineRunner
+
+    depth = 12
+    rng = np.random.default_rng(5)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, ctx + depth)]
+    r = PipelineRunner(model_arg, PipelineConfig(num_stages=args.stages, layer_splits=tuple(splits)),
+                       tp.BeamConfig(w=args.w, k=args.k), None, collect_trace=False, kv_capacity=ctx + depth + 128,
+                       check_invariants=False)
+    r.prefill(prompt)
+    q_, kv_ = cfg.heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
+    layer_w = 2.0 * (cfg.hidden * (q_ + 2 * kv_) + q_ * cfg.hidden + 3 * cfg.hidden * cfg.ffn)
+    out = []
+    for si, stage in enumerate(r.stages):
+        n = max(1, int(round(mean_nodes[si])))
+        dev = stage.model.device
+        d = rng.integers(0, depth, n)
+        pre = np.full(n, ctx, dtype=np.int32)
+        bits = ((np.uint64(1) << d.astype(np.uint64)) - np.uint64(1)).reshape(n, 1).astype(np.uint64)
+        with torch.cuda.device(dev):
+            x = (torch.randn(n, cfg.hidden, device=f"cuda:{dev}") * 0.5).to(torch.bfloat16)
+            item = (stage.kv, stage.model, x, None, (ctx + d).tolist(), stage.layer_range, False, list(range(n)),
+                    False, (pre, ctx, 1, bits))
+            last = si == len(r.stages) - 1
+
+            def once():
+                o = forward_members([[item]])[0]
+                if last:
+                    stage.model.verify_async(o[0][0:1] if isinstance(o, list) else o[0:1])
+                    stage.model.verify_wait()
+
+            for _ in range(3):
+                once()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                once()
+            e1.record()
+            torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / iters
+        nl = stage.layer_range[1] - stage.layer_range[0]
+        b = nl * (layer_w + (ctx + depth) * 2 * kv_ * 2 + n * 2 * kv_ * 2)
+        if stage.layer_range[0] == 0:
+            b += n * cfg.hidden * 2
+        if last:
+            b += 2.0 * cfg.vocab * cfg.hidden
+        out.append({"stage": si + 1, "nodes": n, "layers": nl, "ms": round(ms, 4), "bytes": int(b),
+                    "frac": round(b / (ms * 1e-3) / 1e9 / peak, 4)})
+    r.close()
+    worst = max(x["ms"] for x in out)
+    return {"stages": out, "ctx": ctx,
+            "stage_per_gpu_projection": {"ms_per_step": worst, "tbt_ms_per_token": round(worst * steps_per_token, 4),
+                                         "note": "projection: slowest measured lone stage x measured steps/token "
+                                                 "(one stage per GPU, transfers overlapped); not a multi-GPU run"},
+            "note": "each stage's lone forward (ungrouped launch sequence, last stage + K4 verify) at its rounded "
+                    "mean resident node count, CUDA events, warm"}
 
 
 def c1_leg(tokens=32):

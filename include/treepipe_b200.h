@@ -182,7 +182,10 @@ int tp_stage_read_kv(const tp_stage* s, int32_t layer, int32_t kind, int32_t lo,
  * The stages' host row counts are then set with tp_stage_truncate once the
  * caller has tau (the K/V data is final when the stream reaches the kernels).
  * keep_out (optional, device int32 [2 + spec_rows + level_n]) receives the kept
- * counts and row lists — the reference's _restrict keep lists (tests).       */
+ * counts and row lists — the reference's _restrict keep lists (tests).
+ * stage may be NULL for a hidden-rows-only entry (prefix/spec rows 0): the
+ * receiver side of a cross-device hand-off, whose rows were sent before the
+ * verification (tp_peer_copy) and are compacted on the receiving device.     */
 typedef struct tp_prune_stage {
   tp_stage* stage;
   int32_t prefix_rows, spec_rows, tree_off;
@@ -194,6 +197,16 @@ typedef struct tp_prune_stage {
 int tp_prune_device(int32_t count, const tp_prune_stage* stages, const tp_stage* verify_ws,
                     const uint64_t* tree_bits, int32_t tree_n, int32_t words, const int32_t* level1_tokens,
                     int32_t n_level1, int64_t hidden_row_bytes, void* stream);
+
+/* ---- cross-device step (stage-per-GPU; pipeline.py:373-439) --------------
+ * tp_result_mirror: the 16-byte verification result of src_ws (K4, possibly on
+ * a peer GPU) -> dst_ws's result word, ordered on `stream` (the receiving
+ * device's stream; the caller makes it wait for the K4 launch first).  Every
+ * device then runs tp_prune_device from its own copy.
+ * tp_peer_copy: cudaMemcpyPeerAsync on `stream` (the send-before-verify
+ * hand-off of a stage's output rows to the next stage's device).            */
+int tp_result_mirror(tp_stage* dst_ws, const tp_stage* src_ws, void* stream);
+int tp_peer_copy(void* dst, int32_t dst_device, const void* src, int32_t src_device, int64_t bytes, void* stream);
 
 /* ---- transmit: in-flight embedding filter (pipeline.py:379-400) ---------- */
 /* dst[j] = src[i_j] for the set bits i_0 < i_1 < ... of keep_bits (n_src rows of row_bytes). */

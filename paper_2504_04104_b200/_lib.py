@@ -62,6 +62,8 @@ _P = C.c_void_p
 _I = C.c_int32
 _SIGS = {
     "tp_prune_device": (C.c_int, [_I, _P, _P, _P, _I, _I, _P, _I, C.c_int64, _P]),
+    "tp_result_mirror": (C.c_int, [_P, _P, _P]),
+    "tp_peer_copy": (C.c_int, [_P, _I, _P, _I, C.c_int64, _P]),
     "tp_last_error": (C.c_char_p, []),
     "tp_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "tp_model_create": (C.c_int, [C.POINTER(ModelConfig), C.POINTER(_P)]),

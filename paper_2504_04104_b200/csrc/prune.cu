@@ -157,8 +157,7 @@ extern "C" int tp_prune_device(int32_t count, const tp_prune_stage* stages, cons
   TP_CHECK(tree_n >= 1 && words >= (tree_n + 63) / 64 && tree_bits, TP_ESHAPE, "tree rows missing or too narrow");
   TP_CHECK(n_level1 >= 0 && n_level1 < tree_n && (n_level1 == 0 || level1_tokens), TP_ESHAPE, "bad level 1");
   TP_CHECK(hidden_row_bytes % 16 == 0, TP_ESHAPE, "hidden row bytes must be a multiple of 16");
-  tp_model* m0 = stages[0].stage->m;
-  TP_CHECK(verify_ws->m->cfg.device == m0->cfg.device, TP_ECONFIG, "verification result on another device");
+  tp_model* m0 = verify_ws->m;  // the device of this call (stage-less entries: hand-off receivers)
   TP_CUDA(cudaSetDevice(m0->cfg.device));
   cudaStream_t st = (cudaStream_t)stream;
   // per-model plan scratch (device), grown on demand
@@ -166,14 +165,17 @@ extern "C" int tp_prune_device(int32_t count, const tp_prune_stage* stages, cons
   size_t need = 0;
   for (int i = 0; i < count; ++i) {
     const tp_prune_stage& d = stages[i];
-    TP_CHECK(d.stage && d.stage->m->cfg.device == m0->cfg.device, TP_ECONFIG, "stages of one prune call share a device");
-    TP_CHECK(d.prefix_rows >= 0 && d.spec_rows >= 0 && d.prefix_rows + d.spec_rows == d.stage->rows, TP_ECONTRACT,
-             "prefix + speculative rows must cover the cache (invariant I1)");
+    TP_CHECK(!d.stage || d.stage->m->cfg.device == m0->cfg.device, TP_ECONFIG,
+             "stages of one prune call share the verification result's device (tp_result_mirror)");
+    TP_CHECK(d.stage || (d.prefix_rows == 0 && d.spec_rows == 0), TP_ECONTRACT, "a stage-less entry has no K/V rows");
+    TP_CHECK(!d.stage || (d.prefix_rows >= 0 && d.spec_rows >= 0 && d.prefix_rows + d.spec_rows == d.stage->rows),
+             TP_ECONTRACT, "prefix + speculative rows must cover the cache (invariant I1)");
     TP_CHECK(d.spec_rows == 0 || (d.tree_off >= 0 && d.tree_off + d.spec_rows <= tree_n), TP_ECONTRACT,
              "speculative rows outside the tree (invariant I2)");
     TP_CHECK(d.level_n == 0 || (d.level_lo >= 0 && d.level_lo + d.level_n <= tree_n && d.hidden_src && d.hidden_dst),
              TP_ECONTRACT, "in-flight level outside the tree");
-    TP_CHECK((d.stage->head_dim * d.stage->esize) % 16 == 0 && d.stage->head_dim * d.stage->esize <= kPruneChunkBytes,
+    TP_CHECK(!d.stage || ((d.stage->head_dim * d.stage->esize) % 16 == 0 &&
+                           d.stage->head_dim * d.stage->esize <= kPruneChunkBytes),
              TP_ESHAPE, "KV row size unsupported");
     need += 2 + (size_t)d.spec_rows + d.level_n;
   }
@@ -210,8 +212,9 @@ extern "C" int tp_prune_device(int32_t count, const tp_prune_stage* stages, cons
       const tp_prune_stage& d = stages[i];
       tp_stage* s = d.stage;
       PruneItem& it = g.m[i - c0];
-      it.kv = kv_view(s);
-      it.layers = s->hi - s->lo;
+      it.kv = s ? kv_view(s) : KvView{};
+      it.kv.heads = s ? it.kv.heads : 1;
+      it.layers = s ? s->hi - s->lo : 0;
       it.P = d.prefix_rows;
       it.S = d.spec_rows;
       it.off = d.tree_off;
@@ -237,5 +240,23 @@ extern "C" int tp_prune_device(int32_t count, const tp_prune_stage* stages, cons
   // host-side row bookkeeping of the stages is the caller's (it knows tau after
   // tp_model_verify_wait); the device rows are final once the move kernel ran
   timeline_mark("prune_device", st);
+  return TP_OK;
+}
+
+extern "C" int tp_result_mirror(tp_stage* dst_ws, const tp_stage* src_ws, void* stream) {
+  TP_CHECK(dst_ws && src_ws, TP_ECONFIG, "null argument");
+  TP_CUDA(cudaSetDevice(dst_ws->m->cfg.device));
+  TP_CUDA(cudaMemcpyPeerAsync(dst_ws->d_result, dst_ws->m->cfg.device, src_ws->d_result, src_ws->m->cfg.device, 16,
+                              (cudaStream_t)stream));
+  timeline_mark("verify_mirror", (cudaStream_t)stream);
+  return TP_OK;
+}
+
+extern "C" int tp_peer_copy(void* dst, int32_t dst_device, const void* src, int32_t src_device, int64_t bytes,
+                            void* stream) {
+  TP_CHECK(bytes >= 0 && (bytes == 0 || (dst && src)), TP_ECONFIG, "null argument");
+  if (bytes == 0) return TP_OK;
+  TP_CUDA(cudaSetDevice(src_device));
+  TP_CUDA(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, (size_t)bytes, (cudaStream_t)stream));
   return TP_OK;
 }

@@ -44,8 +44,10 @@ for n in ns:
     kv_indptr.append(kv_indptr[-1] + kv_len)
 dev = "cuda"
 q = (torch.randn(qo_indptr[-1], H, D, device=dev) * 0.5).to(torch.bfloat16)
-k = (torch.randn(kv_indptr[-1], KV, D, device=dev) * 0.5).to(torch.bfloat16)
-v = (torch.randn(kv_indptr[-1], KV, D, device=dev) * 0.5).to(torch.bfloat16)
+# one K/V set per layer slot of a forward (4), cycled like K1's layers (so both see the same L2 reuse)
+ks = [(torch.randn(kv_indptr[-1], KV, D, device=dev) * 0.5).to(torch.bfloat16) for _ in range(4)]
+vs = [(torch.randn(kv_indptr[-1], KV, D, device=dev) * 0.5).to(torch.bfloat16) for _ in range(4)]
+k, v = ks[0], vs[0]
 mask = torch.from_numpy(np.concatenate(masks)).to(dev)
 ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 w = flashinfer.BatchPrefillWithRaggedKVCacheWrapper(ws, "NHD")
@@ -56,8 +58,8 @@ for _ in range(5):
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(args.iters):
-    w.run(q, k, v)
+for it in range(args.iters):
+    w.run(q, ks[it % 4], vs[it % 4])
 e1.record()
 torch.cuda.synchronize()
 fi_us = e0.elapsed_time(e1) * 1e3 / args.iters
@@ -69,8 +71,15 @@ out = subprocess.run([sys.executable, os.path.join(root, "scripts", "ablate_fwd.
 full = float(out.split("full forward")[1].split("us")[0])
 noattn = float(out.split("-attention")[1].split("us")[0])
 k1_us = (full - noattn) / 4
+# K1 alone (the same forward with the GEMMs / RMSNorms skipped, minus prep only): FlashInfer's conditions
+iso = json.loads(subprocess.run([sys.executable, os.path.join(root, "scripts", "attn_bench.py"), "--prefix",
+                                 str(args.prefix), "--n", args.n], capture_output=True, text=True,
+                                check=True).stdout.strip().splitlines()[-1])
 print(json.dumps({"comparator": "K1 vs FlashInfer batched ragged prefill (custom mask)", "prefix": args.prefix,
                   "nodes_per_stage": ns, "heads": H, "head_dim": D,
+                  "k1_us_per_layer_slot_alone": iso["group_us_per_slot"],
                   "k1_us_per_layer_slot_in_situ": round(k1_us, 1),
+                  "note": "alone = back-to-back attention launches over 4 layer slots (FlashInfer: 4 K/V sets cycled); "
+                          "in situ = marginal cost inside the grouped forward (GEMM neighbours, PDL chain)",
                   "flashinfer_us_per_layer_slot": round(fi_us, 1),
                   "flashinfer_version": flashinfer.__version__}))

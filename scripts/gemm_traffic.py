@@ -1,5 +1,5 @@
 """K2 DRAM traffic vs algorithmic bytes (bench roofline.traffic): parse the ncu
-launch list of `scripts/profile_step.py` and write profiles/r01_gemm_traffic.json.
+launch list of `scripts/profile_step.py` and write profiles/r02_gemm_traffic.json.
 
     ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
         --clock-control none --cache-control none -k regex:sk_gemm --csv --log-file gpurun_out/gemm_traffic.csv \
@@ -29,5 +29,5 @@ out = {"kernel": "sk_gemm_kernel",
        "traffic_over_algorithmic": round((rd + wr) / alg, 3),
        "note": "per-launch means over the same launches; write traffic = stream-K partials + epilogue outputs"}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-json.dump(out, open(os.path.join(root, "profiles", "r01_gemm_traffic.json"), "w"), indent=1)
+json.dump(out, open(os.path.join(root, "profiles", "r02_gemm_traffic.json"), "w"), indent=1)
 print(json.dumps(out))

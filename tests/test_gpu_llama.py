@@ -381,3 +381,56 @@ def test_sharded_models_pipeline_lossless():
             r.decode_step()
         assert r.emitted[:20] == ref[:20], grouped
         r.close()
+
+
+@pytest.mark.gpu
+def test_cross_shard_protocol_on_one_gpu():
+    """The stage-per-GPU step protocol (send-before-verify hand-offs by
+    tp_peer_copy, K4's result mirrored to every shard by tp_result_mirror,
+    per-shard tp_prune_device with receiver-side compaction of the hand-offs)
+    exercised on one GPU with one stream per shard: tokens equal the greedy
+    decode, and every step's device keep lists equal the single-shard run's."""
+    from paper_2504_04104_b200.pipeline import PipelineRunner, split_layers
+
+    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=6, heads=2, kv_heads=1, ffn=512)
+    full = tp.LlamaModel(cfg, max_nodes=64)
+    stages = 6
+    splits = split_layers(cfg.layers, stages)
+    owner = [0, 0, 1, 1, 2, 2]  # three shards of two stages each
+    shards = {}
+    for o in sorted(set(owner)):
+        mine = [splits[s] for s in range(stages) if owner[s] == o]
+        lo, hi = mine[0][0], mine[-1][1]
+        shards[o] = tp.LlamaModel(cfg, max_nodes=64, layer_range=(lo, hi), with_embed=lo == 0,
+                                  with_head=hi == cfg.layers)
+    per_stage = [shards[owner[s]] for s in range(stages)]
+    prompt = [int(t) for t in np.random.default_rng(21).integers(0, cfg.vocab, 60)]
+    ref = tp.sequential_decode(full, prompt, 40)
+
+    def run(models, shard_streams):
+        draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.6, rank_decay=0.5, miss_prob=0.1, seed=5),
+                                  cfg.vocab)
+        draft.bind_reference(tuple(prompt) + tuple(ref))
+        r = PipelineRunner(models, tp.PipelineConfig(num_stages=stages, layer_splits=tuple(splits)),
+                           tp.BeamConfig(w=8, k=4), draft, collect_trace=False, shard_streams=shard_streams)
+        r.capture_device_keeps = []
+        r.prefill(prompt)
+        keeps = []
+        while len(r.emitted) < 28:
+            r.decode_step()
+            keeps.append([list(x) for x in r.last_keeps] if r.last_keeps else None)
+        import torch
+
+        torch.cuda.synchronize()
+        return r, keeps
+
+    r1, k1 = run(full, False)
+    r2, k2 = run(per_stage, True)
+    assert r2.cross and not r1.cross
+    assert r2.emitted[:28] == ref[:28] == r1.emitted[:28]
+    assert k1 == k2
+    dev1 = [[int(b[0])] + b[2:2 + int(b[0])].tolist() for b in (x.cpu() for x in r1.capture_device_keeps[-1])]
+    dev2 = [[int(b[0])] + b[2:2 + int(b[0])].tolist() for b in (x.cpu() for x in r2.capture_device_keeps[-1])]
+    assert dev1 == dev2
+    r1.close()
+    r2.close()

@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--w", type=int, default=64)
     ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--draft", default="paper", choices=["paper", "perfect"])
+    ap.add_argument("--draft-model", default="auto", choices=["auto", "none", "68m", "7b"],
+                    help="draft model whose forward runs each step (auto: 68m for 7b/13b targets, 7b for 70b)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 leg vs the unmodified reference")
     ap.add_argument("--no-comparators", action="store_true", help="skip the vanilla-PP / cuBLAS comparators")
@@ -81,10 +83,26 @@ def draft_cfg(kind, seed=0):
     return tp.SyntheticDraftConfig(seed=seed)
 
 
+def draft_model_name(args):
+    if args.draft_model != "auto":
+        return None if args.draft_model == "none" else args.draft_model
+    return {"70b": "7b", "tiny": None}.get(args.model, "68m")
+
+
+def draft_model_cfg(name):
+    from paper_2504_04104_b200.model import LlamaConfig
+
+    return {"68m": LlamaConfig.llama_68m, "7b": lambda: LlamaConfig.llama2_7b(seed=1)}[name]()
+
+
 def workload(args):
+    dm = draft_model_name(args)
     return {"workload": f"Llama-2-{args.model}-shape target, {args.stages}-stage SpecPipe, single request, dynamic tree",
             "model": f"llama2-{args.model}-shape (random LCG init, fan-in scaled)", "stages": args.stages,
             "w": args.w, "k": args.k, "prompt_len": args.prompt_len, "draft": f"SyntheticDraft({args.draft})",
+            "draft_model": (f"llama-{dm}-shape on stage 1's GPU: its tree forward over stage 1's level, LM head and "
+                            "top-k run every step (timed); the host waits for the top-k before expanding"
+                            if dm else None),
             "global_batch": 1, "parallelism": f"pp{args.stages} over {args.gpus} GPU(s)",
             "l2": "no flush: every step streams all stage weights (>>126 MB L2)",
             "untimed_before_warmup": f"a priming run of {2 * args.stages + 8} steps on a separate runner, then "
@@ -344,6 +362,51 @@ def build_shards(cfg, stages, ngpu, max_nodes):
     return [shards[dev_of[s]] for s in range(stages)], splits
 
 
+def run_single_stage(args):
+    """C3's 1-stage point: SpecPipe needs >= 2 stages (the reference's ConfigError), so
+    m = 1 is the GPU greedy decode of the whole model (`sequential_decode`, reference
+    `model.py:364-385`), steady-state ms/token as the difference of two
+    decode lengths (prefill and first-use costs cancel), wall clock, synchronised."""
+    import torch
+
+    import paper_2504_04104_b200 as tp
+    from paper_2504_04104_b200.model import LlamaModel
+
+    torch.cuda.set_device(0)
+    cfg = model_cfg(args.model)
+    m = LlamaModel(cfg, max_nodes=64)
+    prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, args.prompt_len)]
+    tp.sequential_decode(m, prompt, 8)  # untimed warm-up
+    lens = (8, 8 + args.steps)
+    ts = []
+    with ClockSampler(0) as clocks:
+        for n_tok in lens:
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            tp.sequential_decode(m, prompt, n_tok)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t)
+    ms = (ts[1] - ts[0]) * 1e3 / (lens[1] - lens[0])
+    peak, peak_src = peaks()
+    q_, kv_ = cfg.heads * cfg.head_dim, cfg.kv_heads * cfg.head_dim
+    wbytes = 2.0 * (cfg.layers * (cfg.hidden * (q_ + 2 * kv_) + q_ * cfg.hidden + 3 * cfg.hidden * cfg.ffn)
+                    + cfg.vocab * cfg.hidden)
+    line = {"metric": "TBT ms/token (single request, 1 stage = GPU greedy decode)", "value": round(ms, 4),
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": 8, "ms_per_step": round(ms, 4),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"Llama-2-{args.model}-shape, 1 stage: sequential greedy decode (SpecPipe needs "
+                                   ">= 2 stages)", "model": f"llama2-{args.model}-shape (random LCG init, fan-in scaled)",
+                       "stages": 1, "prompt_len": args.prompt_len, "global_batch": 1},
+            "tokens_per_s": round(1e3 / ms, 2),
+            "step_roofline": {"bound": "hbm", "algorithmic_bytes_per_step": round(wbytes),
+                              "ideal_ms_per_step": round(wbytes / (peak * 1e6), 4),
+                              "frac": round(wbytes / (ms * 1e-3) / 1e9 / peak, 4), "peak": peak,
+                              "note": "weights + LM head per token (KV rows omitted)"},
+            "clocks": clocks.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args, rank, world):
     import torch
 
@@ -366,11 +429,17 @@ def run_ours(args, rank, world):
     pcfg = PipelineConfig(num_stages=args.stages, layer_splits=tuple(splits))
     beam = tp.BeamConfig(w=args.w, k=args.k)
     model_arg = shards if ngpu > 1 else shards[0]
+    dm_name = draft_model_name(args)
+    dmodel = None
+    if dm_name:
+        from paper_2504_04104_b200.model import LlamaModel
 
-    def fresh(draft):
+        dmodel = LlamaModel(draft_model_cfg(dm_name), device=0, max_nodes=max(64, args.w))
+
+    def fresh(draft, with_draft_model=True):
         r = PipelineRunner(model_arg, pcfg, beam, draft, collect_trace=False,
                            kv_capacity=args.prompt_len + n_ref + args.w * (args.stages + 2) + 64,
-                           check_invariants=False)
+                           check_invariants=False, draft_model=dmodel if with_draft_model else None)
         r.prefill(prompt)
         return r
 
@@ -463,6 +532,11 @@ def run_ours(args, rank, world):
                 step_bytes += ns * cfg.hidden * 2
             if s is replay.stages[-1]:
                 step_bytes += head_w
+        if dmodel is not None and replay.stages[0].resident is not None:  # the draft's weights, per step
+            dc = dmodel.cfg
+            dq, dkv = dc.heads * dc.head_dim, dc.kv_heads * dc.head_dim
+            step_bytes += 2.0 * (dc.layers * (dc.hidden * (dq + 2 * dkv) + dq * dc.hidden + 3 * dc.hidden * dc.ffn)
+                                 + dc.vocab * dc.hidden)
         replay.step(ch)
     e1.record(streams[0])
     host_loop_s = time.perf_counter() - th
@@ -474,6 +548,26 @@ def run_ours(args, rank, world):
     value_tokens = len(replay.emitted) - tok0
     value_ms = e0.elapsed_time(e1) / max(1, value_tokens)
     assert replay.emitted == ref[: len(replay.emitted)]
+
+    no_draft_ms = None
+    if dmodel is not None:  # the same replay without the draft model's forward (its cost on this GPU)
+        nd = fresh(None, with_draft_model=False)
+        for ch in children[:pre]:
+            nd.step(ch)
+        sync_all()
+        ntok0 = len(nd.emitted)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gc.collect()
+        gc.disable()
+        d0.record(streams[0])
+        for ch in children[pre : pre + args.steps]:
+            nd.step(ch)
+        d1.record(streams[0])
+        sync_all()
+        gc.enable()
+        no_draft_ms = d0.elapsed_time(d1) / max(1, len(nd.emitted) - ntok0)
+        nd.release()
+        del nd
 
     # ---- GPU phase timeline of a few steps (diagnostic, separate from the timed run) -----
     replay.phase_events = []
@@ -542,6 +636,10 @@ def run_ours(args, rank, world):
                           "frac": round(step_bytes / (e0.elapsed_time(e1) * 1e-3) / 1e9 / peak, 4),
                           "unit": "GB/s", "note": "whole engine step (all kernels + host gaps) vs weights of the "
                                                   "occupied stages + KV rows + LM head, per SURVEY 8d"},
+        "draft_model_cost": ({"tbt_ms_per_token_without": round(no_draft_ms, 4),
+                              "share": round(1 - no_draft_ms / value_ms, 4),
+                              "note": "the same replayed steps without the draft model's forward (engine value)"}
+                             if no_draft_ms else None),
         "host_ms_per_step": host_diag,
         "e2e_host_ms_per_step": e2e_host,
         "gpu_phase_ms_per_step": phase_diag,
@@ -820,6 +918,8 @@ def main():
         if rank == 0:
             if args.impl == "reference":
                 run_reference(args)
+            elif args.stages == 1:
+                run_single_stage(args)
             else:
                 run_ours(args, rank, world)
     finally:

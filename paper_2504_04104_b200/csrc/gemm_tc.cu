@@ -277,6 +277,39 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
   const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
   const size_t slot = (size_t)n * kBM;
   const int f = lane * 4;
+  if (cnt <= 4) {
+    // The tail of the kernel: every load of a batch of kRows rows (their cnt
+    // partials and the op's operands) is issued before any arithmetic, so the
+    // reduction costs one L2 round trip per batch instead of one per row pair.
+    constexpr int kRows = 4;
+    for (int c0 = lo + ew; c0 < hi; c0 += kRows * NW) {
+      float4 v[kRows][4];
+      EpiAux x[kRows];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const int c = c0 + r * NW;
+        x[r] = EpiAux{};
+        if (c < hi) {
+          epi_aux(e, mt, f, c, x[r]);
+          const float* b = base + (size_t)c * kBM + f;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) v[r][s] = s < cnt ? ld4cg(b + s * slot) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const int c = c0 + r * NW;
+        if (c < hi) {
+          float4 acc = v[r][0];  // contributor order, as sum_partials
+#pragma unroll
+          for (int s = 1; s < 4; ++s)
+            if (s < cnt) acc = add4(acc, v[r][s]);
+          epi_finish(e, mt, lane, c, acc, x[r]);
+        }
+      }
+    }
+    return;
+  }
   for (int c = lo + ew; c < hi; c += 2 * NW) {
     const int c2 = c + NW;
     const bool two = c2 < hi;

@@ -434,3 +434,60 @@ def test_cross_shard_protocol_on_one_gpu():
     assert dev1 == dev2
     r1.close()
     r2.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cross", [False, True])
+def test_draft_model_stage(cross):
+    """The draft-model forward (BASELINE configs 2/4) inside the step: the draft's
+    cache mirrors stage 1's rows through every prune, tokens stay lossless, and
+    the draft's logits for a tree node equal a causal forward of the draft over
+    that node's path (prompt + ancestors + node), i.e. the tree masking holds."""
+    from paper_2504_04104_b200.pipeline import PipelineRunner, split_layers
+
+    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=4, heads=2, kv_heads=1, ffn=512)
+    dcfg = tp.LlamaConfig(vocab=512, hidden=256, layers=1, heads=2, kv_heads=2, ffn=512, seed=9)
+    full = tp.LlamaModel(cfg, max_nodes=64)
+    dm = tp.LlamaModel(dcfg, max_nodes=64)
+    stages = 4
+    splits = split_layers(cfg.layers, stages)
+    models = full
+    if cross:
+        models = [tp.LlamaModel(cfg, max_nodes=64, layer_range=sp, with_embed=sp[0] == 0,
+                                with_head=sp[1] == cfg.layers) for sp in splits]
+    prompt = [int(t) for t in np.random.default_rng(33).integers(0, cfg.vocab, 40)]
+    ref = tp.sequential_decode(full, prompt, 30)
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.6, rank_decay=0.5, miss_prob=0.1, seed=2), cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(ref))
+    r = PipelineRunner(models, tp.PipelineConfig(num_stages=stages, layer_splits=tuple(splits)),
+                       tp.BeamConfig(w=6, k=3), draft, collect_trace=False, shard_streams=cross, draft_model=dm)
+    r.capture_draft = []
+    r.prefill(prompt)
+    checked = 0
+    while len(r.emitted) < 20:
+        r.decode_step()
+        s1, dk = r.stages[0].kv, r.draft_stage.kv
+        assert len(s1) == len(dk) and np.array_equal(s1._uid, dk._uid) and np.array_equal(s1._pref, dk._pref)
+        if r.capture_draft and checked < 6 and r.tree is not None:
+            uids, pos, logits = r.capture_draft[-1]
+            node = len(uids) - 1  # the level's last node: its path from the tree
+            path = []
+            u = uids[node]
+            if u in r.tree._uid_index:
+                i = r.tree._uid_index[u]
+                anc = np.flatnonzero(tp.tree.mask_row(r.tree, i).bits)
+                path = [int(r.tree.tokens[j]) for j in anc]  # root .. node (root = last verified token)
+                seq = r.verified[: pos[node] - len(path) + 1] + path
+                assert len(seq) == pos[node] + 1
+                cache = tp.KvCache(dcfg.layers, dcfg.hidden)
+                rows = tp.model.prefill_rows(dm, cache, seq)
+                want = dm.logits_many(rows[-1:])[0].float().cpu()
+                got = logits[node]
+                assert float((got - want).abs().max()) <= 1e-4 * max(1.0, float(want.abs().max()))
+                checked += 1
+    import torch
+
+    torch.cuda.synchronize()
+    assert r.emitted[:20] == ref[:20]
+    assert checked >= 2
+    r.release()

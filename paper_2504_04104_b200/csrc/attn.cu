@@ -50,6 +50,8 @@
 // launch-mates.
 #include <cstdlib>
 
+#include <mutex>
+
 #include "attn.h"
 #include "gemm_tc.h"
 #include "sm100.cuh"
@@ -110,7 +112,8 @@ __device__ __forceinline__ size_t part_idx(const AttnArgs& a, int node, int h, i
 }
 
 // kind 0: run launch, 1: tail launch
-__device__ __forceinline__ int member_of(const AttnGroup& G, int b, int kind) {
+template <class Grp>
+__device__ __forceinline__ int member_of(const Grp& G, int b, int kind) {
   int gi = 0;
   while (gi + 1 < G.count && b >= (kind == 0 ? G.m[gi + 1].cta_run : G.m[gi + 1].cta_tail)) ++gi;
   return gi;
@@ -204,7 +207,8 @@ static int g_attn_run = 4;
 struct RunTask {
   int gi, kh, r, base, rows, c0, nch;
 };
-__device__ __forceinline__ RunTask run_task(const AttnGroup& G, int t) {
+template <class Grp>
+__device__ __forceinline__ RunTask run_task(const Grp& G, int t) {
   RunTask k;
   k.gi = member_of(G, t, 0);
   const AttnMember& M = G.m[k.gi];
@@ -255,7 +259,9 @@ __device__ __forceinline__ void trace_ev(int role, int& idx, int tag, int arg) {
 //               the partner warp through shared memory, lazy rescale of O in
 //               TMEM, bf16 P back to TMEM, half-row sum; at a task's end the O
 //               row (its 64 columns) and the state are stored.
-__global__ void __launch_bounds__(kRunThreads, 2) attn_run_kernel(const __grid_constant__ AttnGroup G, int ntasks) {
+template <int MG>
+__global__ void __launch_bounds__(kRunThreads, 2) attn_run_kernel(const __grid_constant__ AttnGroupT<MG> G,
+                                                                  int ntasks) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   __shared__ uint64_t bars[2 * kKvStages + 8];  // (q_full: producer TMA, expect-tx)
   __shared__ uint32_t tmem_holder;
@@ -520,7 +526,9 @@ __global__ void __launch_bounds__(kRunThreads, 2) attn_run_kernel(const __grid_c
 // lanes, and P.V runs with lane l owning dims 4l..4l+3 (slots in order) — all
 // before griddepcontrol.wait when `early`; then the run states are merged in
 // order, the suffix last, and the bf16 output row is written.
-__global__ void __launch_bounds__(kTailWarps * 32) attn_tail_kernel(const __grid_constant__ AttnGroup G, int early) {
+template <int MG>
+__global__ void __launch_bounds__(kTailWarps * 32) attn_tail_kernel(const __grid_constant__ AttnGroupT<MG> G,
+                                                                    int early) {
   if (!early) pdl_wait();
   pdl_trigger();  // the O-projection GEMM may start streaming its weights
   __shared__ const char* spg[kAttnSuffix];  // page base of the slot's row (nullptr: a self buffer row)
@@ -676,9 +684,9 @@ __global__ void __launch_bounds__(kTailWarps * 32) attn_tail_kernel(const __grid
   *reinterpret_cast<uint2*>(out) = u;
 }
 
-int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
-  TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 64]");
-  AttnGroup G;
+template <int MG>
+static int attn_group_launch(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
+  AttnGroupT<MG> G;
   G.count = count;
   G.run = g_attn_run;
   int cr = 0, ct = 0;
@@ -697,12 +705,16 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
     cr += a[g].KV * ((m.c_hi + G.run - 1) / G.run) * m.blocks;
     ct += lv[g].n * ((a[g].H + kTailWarps - 1) / kTailWarps);
   }
+  static std::mutex mu;  // per instantiation; host threads of several shards launch concurrently
   static bool attr_set[64] = {false};  // per device
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
-  if (!attr_set[dev & 63]) {
-    TP_CUDA(cudaFuncSetAttribute(attn_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRunSmem));
-    attr_set[dev & 63] = true;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr_set[dev & 63]) {
+      TP_CUDA(cudaFuncSetAttribute(attn_run_kernel<MG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRunSmem));
+      attr_set[dev & 63] = true;
+    }
   }
   static const int dbg = getenv("TP_ATTN_DEBUG") ? atoi(getenv("TP_ATTN_DEBUG")) : 0;  // diagnostics: 1 skip tail, 2 skip runs
   if (dbg & 2) cr = 0;
@@ -710,17 +722,24 @@ int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream
   if (cr > 0) {
     ::tp::count_launch();
     const int grid = std::min(cr, 2 * num_sms());  // persistent: two CTAs per SM walk the tasks
-    TP_CUDA(launch_pdl(attn_run_kernel, dim3(grid), dim3(kRunThreads), (size_t)kRunSmem, st, G, cr));
+    TP_CUDA(launch_pdl(attn_run_kernel<MG>, dim3(grid), dim3(kRunThreads), (size_t)kRunSmem, st, G, cr));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_shared", st);
   }
   if (ct > 0) {
     ::tp::count_launch();
-    TP_CUDA(launch_pdl(attn_tail_kernel, dim3(ct), dim3(kTailWarps * 32), 0, st, G, cr > 0 ? 1 : 0));
+    TP_CUDA(launch_pdl(attn_tail_kernel<MG>, dim3(ct), dim3(kTailWarps * 32), 0, st, G, cr > 0 ? 1 : 0));
     TP_CUDA(cudaGetLastError());
     timeline_mark("attn_tail", st);
   }
   return TP_OK;
+}
+
+int attn_tree_group(const AttnArgs* a, const LevelDev* lv, int count, cudaStream_t st) {
+  TP_CHECK(count >= 1 && count <= kAttnMaxGroup, TP_ECONFIG, "attention group size outside [1, 64]");
+  if (count == 1) return attn_group_launch<1>(a, lv, count, st);
+  if (count <= 8) return attn_group_launch<8>(a, lv, count, st);
+  return attn_group_launch<kAttnMaxGroup>(a, lv, count, st);
 }
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st) { return attn_tree_group(&a, &lv, 1, st); }

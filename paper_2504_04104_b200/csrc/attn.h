@@ -43,11 +43,15 @@ struct AttnMember {
   int cta_tail;  // first CTA of this member in the tail launch
 };
 
-struct AttnGroup {
-  AttnMember m[kAttnMaxGroup];
+// Kernel parameters are copied per launch, so a launch carries only as many member
+// slots as it needs: 1 (a lone stage), 8 (a device's stages) or 64 (SpecPipe-DB).
+template <int MG>
+struct AttnGroupT {
+  AttnMember m[MG];
   int count;
   int run;  // canonical chunks per run
 };
+using AttnGroup = AttnGroupT<kAttnMaxGroup>;
 static_assert(sizeof(AttnGroup) <= 32000, "AttnGroup must fit the 32 KB kernel-parameter limit");
 
 int attn_tree(const AttnArgs& a, const LevelDev& lv, cudaStream_t st);

@@ -354,12 +354,13 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // Work items are (member g, k-block t) for g = 0..count-1, t in [t0, t1):
 // the TMA producer, the MMA issuer and the epilogue warps walk the same
 // sequence, the smem ring and the TMEM double buffer continuing across members.
+template <int MG>
 #ifdef TP_GEMM_MAXNREG
 __global__ void __maxnreg__(TP_GEMM_MAXNREG)
 #else
 __global__ void __launch_bounds__(kThreads, 1)
 #endif
-    sk_gemm_kernel(const __grid_constant__ GemmGroup grp, SkPlan p, int stages, int nbuf, int fixup_mode) {
+    sk_gemm_kernel(const __grid_constant__ GemmGroupT<MG> grp, SkPlan p, int stages, int nbuf, int fixup_mode) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
@@ -636,13 +637,27 @@ int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
   const int stages = stages_for(mx);
   const size_t smem = smem_for(mx);
   const int nbuf = std::min(kMaxTmemBufs, 512 / mx);
-  static size_t smem_set[64] = {0};  // per device
   int dev = 0;
   TP_CUDA(cudaGetDevice(&dev));
-  if (smem != smem_set[dev & 63]) {
-    TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set[dev & 63] = smem;
+  const int one = grp.count == 1 ? 1 : 0;
+  {  // opt-in smem ceiling, set once per (instantiation, device): a per-launch value
+     // would race between host threads launching different node counts
+    static std::mutex mu;
+    static bool done[2][64] = {{false}};
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done[one][dev & 63]) {
+      const int need = (int)std::max(smem_for(256), smem_for(16));
+      int optin = 0;
+      TP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      const int lim = std::max(need, std::min(optin, 232448));
+      if (one)
+        TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+      else
+        TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel<kMaxGroup>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+      done[one][dev & 63] = true;
+    }
   }
+  TP_CHECK((int)smem <= 232448, TP_ECONFIG, "GEMM shared memory above the opt-in limit");
   ProfRec rec{};
   if (g_prof_on) {
     TP_CUDA(cudaEventCreate(&rec.a));
@@ -663,7 +678,15 @@ int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ::tp::count_launch();
-  TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel, grp, p, stages, nbuf, g_knob_fixup));
+  if (one) {
+    GemmGroupT<1> g1;
+    g1.m[0] = grp.m[0];
+    g1.count = 1;
+    g1.max_npad = grp.max_npad;
+    TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel<1>, g1, p, stages, nbuf, g_knob_fixup));
+  } else {
+    TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel<kMaxGroup>, grp, p, stages, nbuf, g_knob_fixup));
+  }
   if (g_prof_on) {
     TP_CUDA(cudaEventRecord(rec.b, st));
     std::lock_guard<std::mutex> g(g_prof_mu);

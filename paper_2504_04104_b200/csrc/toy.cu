@@ -14,6 +14,7 @@
 // outputs are sequential k-order FMA chains per (node, column); attention
 // walks the node's *logical* key sequence (prefix rows, then ancestor rows,
 // then self) with reductions whose shape depends only on that sequence.
+#include <mutex>
 #include <cmath>
 
 #include "internal.h"
@@ -250,10 +251,16 @@ int toy_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hi
   }
   const double sqrt_d = std::sqrt((double)d);
   size_t smem = (size_t)(d + s->cap + lv.words * 64 + 1) * 8 + (size_t)lv.words * 64 * 4 + 16;
-  static size_t smem_set = 48 * 1024;
-  if (smem > smem_set) {
-    TP_CUDA(cudaFuncSetAttribute(toy_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
+  {  // the opt-in ceiling only grows (per device; host threads may launch concurrently)
+    static std::mutex mu;
+    static size_t smem_set[64] = {0};
+    int dev = 0;
+    TP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (smem > 48 * 1024 && smem > smem_set[dev & 63]) {
+      TP_CUDA(cudaFuncSetAttribute(toy_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set[dev & 63] = smem;
+    }
   }
   for (int layer = lv.layer_lo; layer < lv.layer_hi; ++layer) {
     const tp_layer_weights& w = m->layers[layer - m->cfg.layer_lo];

@@ -210,6 +210,11 @@ int tp_peer_copy(void* dst, int32_t dst_device, const void* src, int32_t src_dev
 
 /* ---- transmit: in-flight embedding filter (pipeline.py:379-400) ---------- */
 /* dst[j] = src[i_j] for the set bits i_0 < i_1 < ... of keep_bits (n_src rows of row_bytes). */
+// Draft model proposals (BASELINE configs 2 and 4): the k (<= 32) best token ids of
+// each of n_rows fp32 logit rows, value descending, lowest id first on ties (no
+// reference counterpart: the reference's drafts are synthetic; CostModel.draft_ms).
+int tp_topk_rows(int32_t device, const void* logits_dev, int32_t vocab, int32_t n_rows, int32_t k, void* out_dev,
+                 void* stream);
 int tp_rows_compact(tp_stage* ws, const void* src_dev, void* dst_dev, int64_t row_bytes, int32_t n_src,
                     const uint64_t* keep_bits, int32_t* n_out, void* stream);
 /* tp_rows_compact for up to 64 row sets (every stage's in-flight filter of one

@@ -98,6 +98,7 @@ _SIGS = {
     "tp_debug_gemm_timed": (C.c_int, [_I, _P, _P, _I, _I, _I, _P, _I, _P, _P]),
     "tp_debug_gemm_group_timed": (C.c_int, [_I, _I, _P, _P, _P, _I, _I, _P, _I, _P, _P]),
     "tp_debug_argmax": (C.c_int, [_I, _P, _I, _I, _I, _P, _I, _P]),
+    "tp_topk_rows": (C.c_int, [_I, _P, _I, _I, _I, _P, _P]),
     "tp_debug_gemm_knob": (C.c_int, [_I, _I]),
     "tp_synthetic_draft": (C.c_int, [C.c_uint64, C.c_int64, _I, C.c_double, C.c_double, C.c_double, _I, _I,
                                       _P, _P]),
@@ -128,8 +129,27 @@ def io_bytes() -> tuple[int, int]:
     return h.value, d.value
 
 
+_PROFILE_ON = False
+
+
 def profile_enable(on: bool) -> None:
+    global _PROFILE_ON
+    _PROFILE_ON = bool(on)
     check(load().tp_profile_enable(int(on)))
+
+
+class profile_paused:
+    """Exclude a block's GEMM launches from the K2 roofline profile (the draft model's)."""
+
+    def __enter__(self):
+        self._was = _PROFILE_ON
+        if self._was:
+            check(load().tp_profile_enable(0))
+
+    def __exit__(self, *a):
+        if self._was:
+            check(load().tp_profile_enable(1))
+        return False
 
 
 def profile_read() -> tuple[float, float, int]:

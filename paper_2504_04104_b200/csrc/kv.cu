@@ -259,3 +259,108 @@ int argmax_rows(const void* logits_f32, int vocab, int n, int32_t* d_out, cudaSt
 }
 
 }  // namespace tp
+
+namespace tp {
+
+// Top-K of n rows of fp32 logits (the draft model's proposal candidates): one CTA
+// of 32 warps per row.  Each warp keeps its K best (value desc, lowest id first on
+// ties, `better`) as a sorted list spread over its lanes (lane r = rank r) and
+// scans coalesced batches of 32 logits: a batch costs one compare + ballot against
+// the list's K-th entry, and the rare candidates are inserted by a ballot rank +
+// shfl_up shift.  The warps' lists are then merged pairwise (5 levels).
+__device__ __forceinline__ void topk_insert(float& lv, int& li, float cv, int ci, int K, int lane) {
+  const unsigned ahead = __ballot_sync(0xffffffffu, lane < K && better(lv, li, cv, ci));
+  const int p = __popc(ahead);
+  const float pv = __shfl_up_sync(0xffffffffu, lv, 1);
+  const int pi = __shfl_up_sync(0xffffffffu, li, 1);
+  if (p < K) {
+    if (lane == p) {
+      lv = cv;
+      li = ci;
+    } else if (lane > p && lane < K) {
+      lv = pv;
+      li = pi;
+    }
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(1024) topk_rows_kernel(const float* __restrict__ logits, int V, int k,
+                                                         int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int W = 32, U = 8;  // warps; batches loaded per round trip
+  __shared__ float sv[W][32];
+  __shared__ int si[W][32];
+  const float* row = logits + (size_t)blockIdx.x * V;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float lv = -INFINITY;
+  int li = 0x7fffffff;
+  float tv = -INFINITY;
+  int ti = 0x7fffffff;
+  for (int base0 = w * 32; base0 < V; base0 += U * W * 32) {
+    float xs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base0 + u * W * 32 + lane;
+      xs[u] = j < V ? __ldg(row + j) : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = base0 + u * W * 32 + lane;
+      const float x = xs[u];
+      unsigned m = __ballot_sync(0xffffffffu, j < V && better(x, j, tv, ti));
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const float cv = __shfl_sync(0xffffffffu, x, src);
+        const int ci = __shfl_sync(0xffffffffu, j, src);
+        topk_insert(lv, li, cv, ci, K, lane);
+      }
+      tv = __shfl_sync(0xffffffffu, lv, K - 1);
+      ti = __shfl_sync(0xffffffffu, li, K - 1);
+    }
+  }
+  // tree merge: at each level warp w < half inserts warp w + half's list
+  for (int half = W / 2; half >= 1; half >>= 1) {
+    if (w >= half && w < 2 * half) {
+      sv[w][lane] = lv;
+      si[w][lane] = li;
+    }
+    __syncthreads();
+    if (w < half)
+      for (int r = 0; r < K; ++r) {
+        const float cv = sv[w + half][r];
+        const int ci = si[w + half][r];
+        if (ci == 0x7fffffff) break;  // the partner's list is shorter (V < W * K)
+        topk_insert(lv, li, cv, ci, K, lane);
+      }
+    __syncthreads();
+  }
+  if (w == 0 && lane < k) out[(size_t)blockIdx.x * k + lane] = li;
+}
+
+int topk_rows(const float* logits, int vocab, int n, int k, int32_t* d_out, cudaStream_t st) {
+  TP_CHECK(n >= 1 && k >= 1 && k <= 32 && k <= vocab, TP_ESHAPE, "top-k: need 1 <= k <= min(32, vocab)");
+  ::tp::count_launch();
+  if (k <= 4)
+    TP_CUDA(launch_pdl(topk_rows_kernel<4>, dim3(n), dim3(1024), 0, st, logits, vocab, k, d_out));
+  else if (k <= 8)
+    TP_CUDA(launch_pdl(topk_rows_kernel<8>, dim3(n), dim3(1024), 0, st, logits, vocab, k, d_out));
+  else if (k <= 16)
+    TP_CUDA(launch_pdl(topk_rows_kernel<16>, dim3(n), dim3(1024), 0, st, logits, vocab, k, d_out));
+  else
+    TP_CUDA(launch_pdl(topk_rows_kernel<32>, dim3(n), dim3(1024), 0, st, logits, vocab, k, d_out));
+  TP_CUDA(cudaGetLastError());
+  return TP_OK;
+}
+
+}  // namespace tp
+
+// Draft-model proposals: the k best token ids of each of n logit rows (fp32, device).
+extern "C" int tp_topk_rows(int32_t device, const void* logits_dev, int32_t vocab, int32_t n_rows, int32_t k,
+                            void* out_dev, void* stream) {
+  TP_CUDA(cudaSetDevice(device));
+  return tp::topk_rows(static_cast<const float*>(logits_dev), vocab, n_rows, k, static_cast<int32_t*>(out_dev),
+                       (cudaStream_t)stream);
+}

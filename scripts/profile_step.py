@@ -25,6 +25,7 @@ ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--warmup", type=int, default=16)
 ap.add_argument("--prompt-len", type=int, default=512)
 ap.add_argument("--timeline", action="store_true", help="print host-side timing of each phase")
+ap.add_argument("--draft-model", default="68m", choices=["68m", "none"], help="draft model forward each step (bench default)")
 args = ap.parse_args()
 
 cfg = model_cfg(args.model)
@@ -33,8 +34,9 @@ prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, a
 ref = tp.sequential_decode(m, prompt, args.warmup + args.steps + 24)
 draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(seed=0), cfg.vocab)
 draft.bind_reference(tuple(prompt) + tuple(ref))
+dm = LlamaModel(tp.LlamaConfig.llama_68m(), max_nodes=64) if args.draft_model == "68m" else None
 r = PipelineRunner(m, PipelineConfig(num_stages=8), tp.BeamConfig(w=64, k=16), draft, collect_trace=False,
-                   kv_capacity=2048, check_invariants=False)
+                   kv_capacity=2048, check_invariants=False, draft_model=dm)
 r.prefill(prompt)
 for _ in range(args.warmup):
     r.decode_step()

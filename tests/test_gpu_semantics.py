@@ -173,3 +173,22 @@ def test_k4_argmax_first_max_nan_and_child_match():
     out = np.zeros(9, dtype=np.int32)
     _lib.check(lib.tp_debug_argmax(0, C.c_void_p(t.data_ptr()), 0, 32000, 9, None, 0, out.ctypes.data))
     assert out.tolist() == [int(np.argmax(r)) for r in rows]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [1, 4, 16, 32])
+def test_topk_rows_vs_torch(k):
+    """The draft model's top-k kernel: ids of the k largest logits per row, value
+    descending, lowest id first on ties (checked on rows with planted ties)."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(k)
+    logits = torch.randn(37, 32000, device="cuda", generator=g)
+    logits[3, 100] = logits[3, 7] = 50.0  # a tie at the top: id 7 first
+    m = tp.LlamaModel(tp.LlamaConfig(vocab=512, hidden=256, layers=1, heads=2, kv_heads=1, ffn=512), max_nodes=16)
+    got = m.topk_many(logits, k).cpu()
+    want = torch.topk(logits, k, dim=1)
+    assert torch.equal(torch.gather(logits.cpu(), 1, got.long()), want.values.cpu())
+    assert int(got[3, 0]) == 7 and (k == 1 or int(got[3, 1]) == 100)
+    vals = torch.gather(logits.cpu(), 1, got.long())
+    assert bool((vals[:, :-1] >= vals[:, 1:]).all())

@@ -334,7 +334,10 @@ def run_reference(args):
               f"{sched_steps}-step control-only run in this process")
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": args.gpus, "steps": timed,
             "warmup": warm, "ms_per_step": round(float(np.mean(step_ms)), 2), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload(args),
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {**workload(args), "draft_model": (
+                "not run by the CPU port: the draft's proposals come from the same SyntheticDraft; its forward "
+                "(68M shape) is ~1 % of a 7B step's node-layer FLOPs") if draft_model_name(args) else None},
             "impl": "reference", "steps_per_token": round(spt, 4), "node_layers_per_step": round(nl_per_step, 1),
             "measured_steps_ms": [round(x, 1) for x in step_ms], "measured_node_layers": nls,
             "ms_per_node_layer": round(per_nl, 3), "head_ms": round(head_ms, 2), "setup_s": round(setup_s, 1),

@@ -599,7 +599,10 @@ def run_ours(args, rank, world):
     pe1.record(streams[0])
     sync_all()
     _lib.profile_enable(False)
-    gemm_ms, gemm_bytes, gemm_n = _lib.profile_read()
+    by_members = _lib.profile_read_members()
+    gemm_ms = sum(r[0] for r in by_members)
+    gemm_bytes = sum(r[1] for r in by_members)
+    gemm_n = sum(r[2] for r in by_members)
     prof_total_ms = pe0.elapsed_time(pe1)
     peak, peak_src = peaks()
     achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
@@ -632,7 +635,12 @@ def run_ours(args, rank, world):
                                          if cap else None),
                      "peak_source": peak_src,
                      "gemm_share_of_step": round(gemm_ms / prof_total_ms, 4) if prof_total_ms else None,
-                     "gemm_launches": gemm_n, "bytes_per_launch": round(gemm_bytes / max(1, gemm_n))},
+                     "gemm_launches": gemm_n, "bytes_per_launch": round(gemm_bytes / max(1, gemm_n)),
+                     "by_members": {str(i + 1): {"launches": r[2], "frac": round(r[1] / (r[0] * 1e-3) / 1e9 / peak, 4),
+                                                 "ms_per_step": round(r[0] / max(1, len(children[pre + args.steps + 8:])), 4)}
+                                    for i, r in enumerate(by_members) if r[2]},
+                     "by_members_note": "launches by member count: the grouped stage forwards (3+ members), the "
+                                        "verify stage (+ the fused draft model: 2), the LM heads (1)"},
         "step_roofline": {"bound": "hbm", "algorithmic_bytes_per_step": round(step_bytes / max(1, len(resident))),
                           "ideal_ms_per_step": round(step_bytes / max(1, len(resident)) / (peak * 1e6), 4),
                           "achieved": round(step_bytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1),

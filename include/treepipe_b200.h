@@ -245,6 +245,9 @@ int tp_io_bytes(int64_t* h2d, int64_t* d2h);
  * tp_profile_read returns summed ms, algorithmic bytes and launch count, then resets. */
 int tp_profile_enable(int32_t on);
 int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* launches);
+// The same per-launch records split by the launch's member count: arrays of 8
+// (index = members - 1: 1 = a lone stage, 2 = a stage + the fused draft model, ...).
+int tp_profile_read_members(double* gemm_ms, double* gemm_bytes, int64_t* launches);
 
 /* ---- test hook (no reference counterpart): the K2 weight-streaming GEMM alone.
  * out[n][n_out] (f32, dev) = x[n][k] (bf16, dev) . w[n_out][k]^T (bf16, dev).   */

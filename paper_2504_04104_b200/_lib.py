@@ -113,6 +113,7 @@ _SIGS = {
     "tp_launch_count": (C.c_int, [C.POINTER(C.c_int64)]),
     "tp_io_bytes": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tp_profile_enable": (C.c_int, [_I]),
+    "tp_profile_read_members": (C.c_int, [_P, _P, _P]),
     "tp_profile_read": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }
 
@@ -150,6 +151,13 @@ class profile_paused:
         if self._was:
             check(load().tp_profile_enable(1))
         return False
+
+
+def profile_read_members() -> list[tuple[float, float, int]]:
+    """(ms, bytes, launches) of the profiled GEMM launches, by member count 1..8."""
+    ms, by, n = (C.c_double * 8)(), (C.c_double * 8)(), (C.c_int64 * 8)()
+    check(load().tp_profile_read_members(ms, by, n))
+    return [(ms[i], by[i], n[i]) for i in range(8)]
 
 
 def profile_read() -> tuple[float, float, int]:

@@ -360,11 +360,17 @@ __global__ void __maxnreg__(TP_GEMM_MAXNREG)
 #else
 __global__ void __launch_bounds__(kThreads, 1)
 #endif
-    sk_gemm_kernel(const __grid_constant__ GemmGroupT<MG> grp, SkPlan p, int stages, int nbuf, int fixup_mode) {
+    sk_gemm_kernel(const __grid_constant__ GemmGroupT<MG> grp, int stages, int nbuf, int fixup_mode) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int c = blockIdx.x;
-  const int t0 = sk_begin(p, c), t1 = sk_begin(p, c + 1);
+  // member g's k-block range of this CTA under the member's own plan (empty when
+  // the member has fewer work units than the grid has CTAs)
+  auto range = [&](int g, int& t0, int& t1) {
+    const SkPlan& p = grp.m[g].p;
+    t0 = min(p.total, sk_begin(p, c));
+    t1 = min(p.total, sk_begin(p, c + 1));
+  };
   const int bmax = grp.max_npad * 128;  // ring slot bytes for the node tile
   uint8_t* sA = smem;
   uint8_t* sB = smem + stages * kABytes;
@@ -407,16 +413,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
       // member 0's weights do not depend on the previous kernel: fill the ring now
       const int nbox0 = grp.m[0].n_pad / 16;
-      const int npre = min(stages, t1 - t0);
+      const SkPlan& p0 = grp.m[0].p;
+      int a0, b0;
+      range(0, a0, b0);
+      const int npre = min(stages, b0 - a0);
       for (int j = 0; j < npre; ++j) {
-        const int t = t0 + j;
+        const int t = a0 + j;
         mbar_expect_tx(&full[j], kABytes + nbox0 * 2048);
-        tma_load_2d(sA + j * kABytes, &grp.m[0].a, (t % p.KB) * kBK, (t / p.KB) * kBM, &full[j], pol_w);
+        tma_load_2d(sA + j * kABytes, &grp.m[0].a, (t % p0.KB) * kBK, (t / p0.KB) * kBM, &full[j], pol_w);
       }
       pdl_wait();  // node rows X come from the previous kernel
       pdl_trigger();
       for (int j = 0; j < npre; ++j) {
-        const int kb = (t0 + j) % p.KB;
+        const int kb = (a0 + j) % p0.KB;
         for (int b = 0; b < nbox0; ++b)
           tma_load_2d(sB + j * bmax + b * 2048, &grp.m[0].b, kb * kBK, b * 16, &full[j], pol_x);
       }
@@ -426,6 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* ma = &grp.m[g].a;
         const CUtensorMap* mb = &grp.m[g].b;
         const int nbox = grp.m[g].n_pad / 16;
+        const SkPlan& p = grp.m[g].p;
+        int t0, t1;
+        range(g, t0, t1);
         for (int t = (g == 0 ? t0 + npre : t0); t < t1; ++t) {
           const int mt = t / p.KB, kb = t % p.KB;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -446,6 +458,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int g = 0; g < grp.count; ++g) {
         const int npad = grp.m[g].n_pad;
+        const SkPlan& p = grp.m[g].p;
+        int t0, t1;
+        range(g, t0, t1);
         const uint32_t idesc = idesc_bf16_f32(kBM, npad);
         int t = t0;
         while (t < t1) {
@@ -488,6 +503,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int g = 0; g < grp.count; ++g) {
       const GemmEpi& e = grp.m[g].e;
       const int n = grp.m[g].n, npad = grp.m[g].n_pad;
+      const SkPlan& p = grp.m[g].p;
+      int t0, t1;
+      range(g, t0, t1);
       int* arrive = e.counters;
       int t = t0;
       while (t < t1) {
@@ -565,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it.g < 0) break;
       const GemmEpi& e = grp.m[it.g].e;
       const int n = grp.m[it.g].n;
+      const SkPlan& p = grp.m[it.g].p;
       const int cend = sk_begin(p, it.clast + 1) <= (it.mt + 1) * p.KB ? it.clast : it.clast - 1;
       const int E = cend - it.cfirst + 1, rank = c - it.cfirst;
       if (rt == 0 && fixup_mode != 3) {  // counters only grow: this launch's arrivals are complete at (epoch+1)*cnt
@@ -589,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 struct ProfRec {
   cudaEvent_t a, b;
   double bytes;
+  int members;
 };
 static std::vector<ProfRec> g_prof;
 static bool g_prof_on = false;
@@ -613,12 +633,23 @@ void sk_counters_forget(const void* base, size_t bytes) {
 
 int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
   GemmGroup grp = grp_in;
+  for (int g = 0; g < grp.count; ++g) grp.m[g].p = p;  // one plan for every member (same shape)
+  return sk_gemm_group(grp, st);
+}
+
+// Members carry their own plans (shapes may differ: e.g. a draft model's layer
+// grouped with a target stage's); CTA c streams its range of each member in turn.
+int sk_gemm_group(const GemmGroup& grp_in, cudaStream_t st) {
+  GemmGroup grp = grp_in;
+  int grid = 1;
+  for (int g = 0; g < grp.count; ++g) grid = std::max(grid, grp.m[g].p.G);
   {
     std::lock_guard<std::mutex> lk(g_epoch_mu);
     for (int g = 0; g < grp.count; ++g) {
       int& ep = g_epochs[grp.m[g].e.counters];
-      if ((int64_t)(ep + 2) * p.max_contrib >= (1 << 30)) {  // ~7M launches: restart the count
-        TP_CUDA(cudaMemsetAsync(grp.m[g].e.counters, 0, (size_t)p.mtiles * sizeof(int), st));
+      const SkPlan& pg = grp.m[g].p;
+      if ((int64_t)(ep + 2) * pg.max_contrib >= (1 << 30)) {  // ~7M launches: restart the count
+        TP_CUDA(cudaMemsetAsync(grp.m[g].e.counters, 0, (size_t)pg.mtiles * sizeof(int), st));
         ep = 0;
       }
       grp.m[g].e.epoch = ep++;
@@ -664,11 +695,13 @@ int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
     TP_CUDA(cudaEventCreate(&rec.b));
     TP_CUDA(cudaEventRecord(rec.a, st));
     rec.bytes = 0.0;
+    rec.members = grp.count;
     for (int g = 0; g < grp.count; ++g)
-      rec.bytes += (double)p.mtiles * kBM * p.KB * kBK * 2.0 + (double)grp.m[g].n * p.KB * kBK * 2.0;
+      rec.bytes += (double)grp.m[g].p.mtiles * kBM * grp.m[g].p.KB * kBK * 2.0 +
+                   (double)grp.m[g].n * grp.m[g].p.KB * kBK * 2.0;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.G);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -683,9 +716,9 @@ int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
     g1.m[0] = grp.m[0];
     g1.count = 1;
     g1.max_npad = grp.max_npad;
-    TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel<1>, g1, p, stages, nbuf, g_knob_fixup));
+    TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel<1>, g1, stages, nbuf, g_knob_fixup));
   } else {
-    TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel<kMaxGroup>, grp, p, stages, nbuf, g_knob_fixup));
+    TP_CUDA(cudaLaunchKernelEx(&cfg, sk_gemm_kernel<kMaxGroup>, grp, stages, nbuf, g_knob_fixup));
   }
   if (g_prof_on) {
     TP_CUDA(cudaEventRecord(rec.b, st));
@@ -703,8 +736,9 @@ int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, con
   grp.m[0].e = epi;
   grp.m[0].n = p.n;
   grp.m[0].n_pad = p.n_pad;
+  grp.m[0].p = p;
   grp.max_npad = p.n_pad;
-  return sk_gemm_group(grp, p, st);
+  return sk_gemm_group(grp, st);
 }
 
 }  // namespace tp
@@ -729,6 +763,28 @@ extern "C" int tp_profile_read(double* gemm_ms, double* gemm_bytes, int64_t* lau
   *gemm_ms = ms;
   *gemm_bytes = bytes;
   *launches = (int64_t)tp::g_prof.size();
+  tp::g_prof.clear();
+  return TP_OK;
+}
+
+// The same records split by the launches' member count (index count - 1).
+extern "C" int tp_profile_read_members(double* gemm_ms, double* gemm_bytes, int64_t* launches) {
+  std::lock_guard<std::mutex> g(tp::g_prof_mu);
+  for (int i = 0; i < tp::kMaxGroup; ++i) {
+    gemm_ms[i] = gemm_bytes[i] = 0.0;
+    launches[i] = 0;
+  }
+  for (auto& r : tp::g_prof) {
+    float t = 0.f;
+    TP_CUDA(cudaEventSynchronize(r.b));
+    TP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    const int k = std::min(std::max(r.members, 1), tp::kMaxGroup) - 1;
+    gemm_ms[k] += t;
+    gemm_bytes[k] += r.bytes;
+    launches[k] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
   tp::g_prof.clear();
   return TP_OK;
 }

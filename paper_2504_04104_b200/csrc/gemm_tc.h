@@ -73,6 +73,7 @@ struct GemmMember {
   CUtensorMap b;  // node rows [n_pad, K]
   GemmEpi e;
   int n, n_pad;
+  SkPlan p;  // this member's stream-K plan (its own (N_out, K))
 };
 
 template <int MG>
@@ -95,6 +96,8 @@ inline size_t sk_part_floats(const SkPlan& p) { return (size_t)p.mtiles * p.max_
 int sk_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const SkPlan& p, const GemmEpi& epi, cudaStream_t st);
 // Grouped launch (members share p's shape; p.n / p.n_pad are ignored).
 int sk_gemm_group(const GemmGroup& grp, const SkPlan& p, cudaStream_t st);
+// Grouped launch of members with their own plans (m[g].p; shapes may differ).
+int sk_gemm_group(const GemmGroup& grp, cudaStream_t st);
 // Forget the launch epochs of counter arrays in [base, base+bytes) (call whenever
 // such memory is (re)allocated and zeroed).
 void sk_counters_forget(const void* base, size_t bytes);

@@ -17,6 +17,7 @@
 // Numerics (mirrored by oracle/llama.py): GEMM inputs bf16, accumulation and
 // residual fp32; RoPE (HF rotate-half, angle in fp64) on the fp32 GEMM
 // output, then rounded to bf16 for the cache / attention; softmax fp32.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -148,6 +149,8 @@ struct RowCopyGroup {
   float* dst[kMaxBatchItems];
   __nv_bfloat16* xd[kMaxBatchItems];  // the first layer's RMSNorm output (nullptr: none)
   int rows[kMaxBatchItems];
+  int d[kMaxBatchItems];      // the item's model width
+  float eps[kMaxBatchItems];  // and RMSNorm epsilon
 };
 // token rows of several items -> their residual-stream rows (fp32), one launch
 struct EmbedGroup {
@@ -155,6 +158,9 @@ struct EmbedGroup {
   float* out[kMaxBatchItems];
   __nv_bfloat16* xd[kMaxBatchItems];  // the first layer's RMSNorm output (nullptr: none)
   int n[kMaxBatchItems];
+  const __nv_bfloat16* E[kMaxBatchItems];  // the item's model's embedding table
+  int d[kMaxBatchItems];
+  float eps[kMaxBatchItems];
 };
 // hidden rows handed over from the previous stage -> the member's residual stream
 
@@ -162,6 +168,7 @@ struct RopeGroup {
   const int32_t* pos[kMaxBatchItems];
   float* out[kMaxBatchItems];
   int n[kMaxBatchItems];
+  double theta[kMaxBatchItems];
 };
 
 // The prep of a forward call as ONE launch (each a separate grid before: every
@@ -174,9 +181,7 @@ struct PrepGroup {
   RopeGroup r;
   int ne, nc, nr;
 };
-__global__ void __launch_bounds__(1024) prep_group_kernel(const __nv_bfloat16* __restrict__ E,
-                                                          const __grid_constant__ PrepGroup P, int d, double theta,
-                                                          float eps) {
+__global__ void __launch_bounds__(1024) prep_group_kernel(const __grid_constant__ PrepGroup P) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[33];
@@ -186,11 +191,13 @@ __global__ void __launch_bounds__(1024) prep_group_kernel(const __nv_bfloat16* _
     const bool emb = y < P.ne;
     const int k = emb ? y : y - P.ne;
     if (x >= (emb ? P.e.n[k] : P.c.rows[k])) return;
+    const int d = emb ? P.e.d[k] : P.c.d[k];
+    const float eps = emb ? P.e.eps[k] : P.c.eps[k];
     float* o = (emb ? P.e.out[k] : P.c.dst[k]) + (size_t)x * d;
     __nv_bfloat16* xd = emb ? P.e.xd[k] : P.c.xd[k];
     float v[kNormPerRow];
     if (emb) {
-      const __nv_bfloat16* e = E + (size_t)P.e.tok[k][x] * d;
+      const __nv_bfloat16* e = P.e.E[k] + (size_t)P.e.tok[k][x] * d;
 #pragma unroll
       for (int u = 0; u < kNormPerRow; ++u) {
         const int j = threadIdx.x + u * 1024;
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(1024) prep_group_kernel(const __nv_bfloat16* _
   y -= P.ne + P.nc;
   const int i = threadIdx.x;
   if (x >= P.r.n[y] || i >= 64) return;
-  const double inv = pow(theta, -2.0 * (double)i / 128.0);
+  const double inv = pow(P.r.theta[y], -2.0 * (double)i / 128.0);
   double sn, cs;
   sincos((double)P.r.pos[y][x] * inv, &sn, &cs);
   P.r.out[y][((size_t)x * 64 + i) * 2] = (float)cs;
@@ -437,14 +444,17 @@ struct NormGroup {
   const float* x[kMaxGroup];
   __nv_bfloat16* xd[kMaxGroup];
   int n[kMaxGroup];
+  int d[kMaxGroup];
+  float eps[kMaxGroup];
 };
 
-__global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __grid_constant__ NormGroup ng, int d,
-                                                                     float eps) {
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __grid_constant__ NormGroup ng) {
   pdl_wait();
   pdl_trigger();
   const int g = blockIdx.y;
   if ((int)blockIdx.x >= ng.n[g]) return;
+  const int d = ng.d[g];
+  const float eps = ng.eps[g];
   __shared__ float red[33];
   const float* xr = ng.x[g] + (size_t)blockIdx.x * d;
   float v[kNormPerRow];
@@ -482,20 +492,28 @@ void* g_dbg_dump = nullptr;
 
 int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int ws_base) {
   TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ECONFIG, "member group size outside [1, 8]");
-  tp_model* m0 = mem[0].items[0].s->m;
-  TP_TRY(build_model_ext(m0));
-  LlamaModelExt* me = mext(m0);
-  std::lock_guard<std::mutex> lk(me->mu);
-  const tp_model_config& c = m0->cfg;
-  const int d = c.hidden, H = c.heads, KV = c.kv_heads, f = c.ffn;
-  const int q = H * 128, kvd = KV * 128;
+  // Members may belong to different model objects of the same device (a draft
+  // model's level grouped with a target stage's): every shape, weight and
+  // workspace below is the member's own model's; each model's enqueue lock is
+  // taken once, in address order.
+  tp_model* mg[kMaxGroup];
+  std::vector<tp_model*> models;
+  for (int g = 0; g < count; ++g) {
+    mg[g] = mem[g].items[0].s->m;
+    TP_TRY(build_model_ext(mg[g]));
+    if (std::find(models.begin(), models.end(), mg[g]) == models.end()) models.push_back(mg[g]);
+  }
+  std::sort(models.begin(), models.end());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (tp_model* m : models) locks.emplace_back(mext(m)->mu);
   LlamaWs* ws[kMaxGroup];
   std::vector<int> offs[kMaxGroup];
   struct Copy {
     const float* src;
     float* dst;
     __nv_bfloat16* xd;
-    int rows;
+    int rows, d;
+    float eps;
   };
   std::vector<Copy> copies;
   struct Embed {
@@ -503,19 +521,24 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     float* out;
     __nv_bfloat16* xd;
     int n;
+    const __nv_bfloat16* E;
+    int d;
+    float eps;
   };
   std::vector<Embed> embeds;
   int ntot[kMaxGroup], lo[kMaxGroup], hi[kMaxGroup];
   int slots = 0;
   for (int g = 0; g < count; ++g) {
     const FwdMember& M = mem[g];
+    const tp_model_config& c = mg[g]->cfg;
+    const int d = c.hidden;
     TP_CHECK(M.count >= 1 && M.x, TP_ECONFIG, "empty forward member");
     int cap_max = 1, n = 0;
     lo[g] = M.items[0].lv.layer_lo;
     hi[g] = M.items[0].lv.layer_hi;
     for (int r = 0; r < M.count; ++r) {
       const FwdItem& it = M.items[r];
-      TP_CHECK(it.s->m == m0, TP_ECONFIG, "grouped stages must share one model object");
+      TP_CHECK(it.s->m == mg[g], TP_ECONFIG, "the items of a member must share one model object");
       TP_CHECK(it.lv.layer_lo == lo[g] && it.lv.layer_hi == hi[g], TP_ECONFIG,
                "items of a member must run the same layers");
       cap_max = std::max(cap_max, it.s->cap);
@@ -524,7 +547,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     }
     TP_CHECK(n <= c.max_nodes, TP_ESHAPE, "ragged member exceeds max_nodes");
     ntot[g] = n;
-    TP_TRY(ws_get(m0, ws_base + g, chunks_for_cap(cap_max), &ws[g]));
+    TP_TRY(ws_get(mg[g], ws_base + g, chunks_for_cap(cap_max), &ws[g]));
     for (int r = 0; r < M.count; ++r) {
       const FwdItem& it = M.items[r];
       float* x = M.x + (size_t)offs[g][r] * d;
@@ -532,10 +555,10 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       // "copied" onto themselves so that every row of a member with layers gets it)
       __nv_bfloat16* xd = hi[g] > lo[g] ? ws[g]->Xd + (size_t)offs[g][r] * d : nullptr;
       if (it.hin) {
-        if (it.hin != x || xd) copies.push_back({(const float*)it.hin, x, xd, it.lv.n});
+        if (it.hin != x || xd) copies.push_back({(const float*)it.hin, x, xd, it.lv.n, d, c.norm_eps});
       } else {
-        TP_CHECK(m0->embed, TP_ECONFIG, "model has no embedding table");
-        embeds.push_back({it.lv.tokens, x, xd, it.lv.n});
+        TP_CHECK(mg[g]->embed, TP_ECONFIG, "model has no embedding table");
+        embeds.push_back({it.lv.tokens, x, xd, it.lv.n, (const __nv_bfloat16*)mg[g]->embed, d, c.norm_eps});
       }
     }
     slots = std::max(slots, hi[g] - lo[g]);
@@ -545,13 +568,15 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       const int32_t* pos;
       float* out;
       int n;
+      double theta;
     };
     std::vector<Rope> ropes;
     for (int g = 0; g < count && slots > 0; ++g) {
       if (hi[g] == lo[g]) continue;
       for (int r = 0; r < mem[g].count; ++r) {
         const FwdItem& it = mem[g].items[r];
-        ropes.push_back({it.lv.positions, ws[g]->rope + (size_t)offs[g][r] * 128, it.lv.n});
+        ropes.push_back({it.lv.positions, ws[g]->rope + (size_t)offs[g][r] * 128, it.lv.n,
+                         (double)mg[g]->cfg.rope_theta});
       }
     }
     size_t ie = 0, ic = 0, ir = 0;
@@ -562,28 +587,35 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       P.nr = (int)std::min<size_t>(kMaxBatchItems, ropes.size() - ir);
       int mx = 1;
       for (int k = 0; k < P.ne; ++k) {
-        P.e.tok[k] = embeds[ie + k].tok;
-        P.e.out[k] = embeds[ie + k].out;
-        P.e.xd[k] = embeds[ie + k].xd;
-        P.e.n[k] = embeds[ie + k].n;
-        mx = std::max(mx, P.e.n[k]);
+        const Embed& e = embeds[ie + k];
+        P.e.tok[k] = e.tok;
+        P.e.out[k] = e.out;
+        P.e.xd[k] = e.xd;
+        P.e.n[k] = e.n;
+        P.e.E[k] = e.E;
+        P.e.d[k] = e.d;
+        P.e.eps[k] = e.eps;
+        mx = std::max(mx, e.n);
       }
       for (int k = 0; k < P.nc; ++k) {
-        P.c.src[k] = copies[ic + k].src;
-        P.c.dst[k] = copies[ic + k].dst;
-        P.c.xd[k] = copies[ic + k].xd;
-        P.c.rows[k] = copies[ic + k].rows;
-        mx = std::max(mx, P.c.rows[k]);
+        const Copy& cp = copies[ic + k];
+        P.c.src[k] = cp.src;
+        P.c.dst[k] = cp.dst;
+        P.c.xd[k] = cp.xd;
+        P.c.rows[k] = cp.rows;
+        P.c.d[k] = cp.d;
+        P.c.eps[k] = cp.eps;
+        mx = std::max(mx, cp.rows);
       }
       for (int k = 0; k < P.nr; ++k) {
         P.r.pos[k] = ropes[ir + k].pos;
         P.r.out[k] = ropes[ir + k].out;
         P.r.n[k] = ropes[ir + k].n;
+        P.r.theta[k] = ropes[ir + k].theta;
         mx = std::max(mx, P.r.n[k]);
       }
       ::tp::count_launch();
-      TP_CUDA(launch_pdl(prep_group_kernel, dim3(mx, P.ne + P.nc + P.nr), dim3(1024), 0, st,
-                         (const __nv_bfloat16*)m0->embed, P, d, (double)c.rope_theta, c.norm_eps));
+      TP_CUDA(launch_pdl(prep_group_kernel, dim3(mx, P.ne + P.nc + P.nr), dim3(1024), 0, st, P));
       ie += P.ne;
       ic += P.nc;
       ir += P.nr;
@@ -611,8 +643,16 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       qnode[g] = reinterpret_cast<const int32_t*>(dptr + sizeof(QkvItem) * M.count);
     }
   }
-  const SkPlan pqkv = sk_plan(q + 2 * kvd, d, 1), po = sk_plan(d, q, 1), pgu = sk_plan(2 * f, d, 1),
-               pdn = sk_plan(d, f, 1);
+  // each member's plans (one set per distinct shape; identical to its ungrouped launches)
+  SkPlan pqkv[kMaxGroup], po[kMaxGroup], pgu[kMaxGroup], pdn[kMaxGroup];
+  for (int g = 0; g < count; ++g) {
+    const tp_model_config& c = mg[g]->cfg;
+    const int q = c.heads * 128, kvd = c.kv_heads * 128;
+    pqkv[g] = sk_plan(q + 2 * kvd, c.hidden, 1);
+    po[g] = sk_plan(c.hidden, q, 1);
+    pgu[g] = sk_plan(2 * c.ffn, c.hidden, 1);
+    pdn[g] = sk_plan(c.hidden, c.ffn, 1);
+  }
   timeline_mark("fwd_prep", st);
   std::vector<AttnArgs> aa;
   std::vector<LevelDev> al;
@@ -629,6 +669,10 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     for (int a = 0; a < na; ++a) {
       const int g = idx[a];
       const FwdMember& M = mem[g];
+      const tp_model_config& c = mg[g]->cfg;
+      LlamaModelExt* me = mext(mg[g]);
+      const int d = c.hidden, H = c.heads, KV = c.kv_heads, f = c.ffn;
+      const int q = H * 128, kvd = KV * 128;
       LlamaWs* e = ws[g];
       const int layer = lo[g] + j, li = layer - c.layer_lo;
       const int n = ntot[g], npad = std::max(16, (n + 15) / 16 * 16);
@@ -637,6 +681,8 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       ng.x[a] = M.x;
       ng.xd[a] = e->Xd;
       ng.n[a] = n;
+      ng.d[a] = d;
+      ng.eps[a] = c.norm_eps;
       const FwdItem& i0 = M.items[0];
       GemmEpi eq = epi_base(e, kCtrQkv);
       eq.op = kOpQkv;
@@ -665,17 +711,19 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       eg.op = kOpSwiglu;
       eg.xf = e->Xf;
       eg.f = f;
-      auto set = [&](GemmGroup& gg, const CUtensorMap& wa, const CUtensorMap& xb, const GemmEpi& ep) {
+      auto set = [&](GemmGroup& gg, const CUtensorMap& wa, const CUtensorMap& xb, const GemmEpi& ep,
+                     const SkPlan& p) {
         gg.m[a].a = wa;
         gg.m[a].b = xb;
         gg.m[a].e = ep;
         gg.m[a].n = n;
         gg.m[a].n_pad = npad;
+        gg.m[a].p = p;
       };
-      set(gq, me->qkv[li], e->mXd, eq);
-      set(go, me->o[li], e->mXo, er);
-      set(ggu, me->gu[li], e->mXd, eg);
-      set(gdn, me->down[li], e->mXf, ed);
+      set(gq, me->qkv[li], e->mXd, eq, pqkv[g]);
+      set(go, me->o[li], e->mXo, er, po[g]);
+      set(ggu, me->gu[li], e->mXd, eg, pgu[g]);
+      set(gdn, me->down[li], e->mXf, ed, pdn[g]);
       for (int r = 0; r < M.count; ++r) {
         const FwdItem& it = M.items[r];
         const size_t off = offs[g][r];
@@ -704,38 +752,40 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     gq.max_npad = go.max_npad = ggu.max_npad = gdn.max_npad = mx;
     // (slot 0's input RMSNorm ran inside the prep launch)
     char* dump = (j == 0 && g_dbg_dump) ? static_cast<char*>(g_dbg_dump) : nullptr;
-    const size_t dn = (size_t)ntot[idx[0]];
+    const int g0 = idx[0];
+    const size_t dn = (size_t)ntot[g0];
+    const size_t dd = mg[g0]->cfg.hidden, dq = (size_t)mg[g0]->cfg.heads * 128, df = mg[g0]->cfg.ffn;
     auto dump_cp = [&](const void* src, size_t bytes) -> int {
       if (!dump) return TP_OK;
       TP_CUDA(cudaMemcpyAsync(dump, src, bytes, cudaMemcpyDeviceToDevice, st));
       dump += bytes;
       return TP_OK;
     };
-    TP_TRY(dump_cp(ws[idx[0]]->Xd, dn * d * 2));
-    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gq, pqkv, st));
+    TP_TRY(dump_cp(ws[g0]->Xd, dn * dd * 2));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gq, st));
     timeline_mark("gemm_qkv", st);
-    TP_TRY(dump_cp(ws[idx[0]]->Xq, dn * q * 2));
+    TP_TRY(dump_cp(ws[g0]->Xq, dn * dq * 2));
     for (size_t a0 = 0; a0 < aa.size() && !(g_dbg_skip & 1); a0 += kAttnMaxGroup) {
       const int cnt = (int)std::min<size_t>(kAttnMaxGroup, aa.size() - a0);
       TP_TRY(attn_tree_group(aa.data() + a0, al.data() + a0, cnt, st));
     }
-    TP_TRY(dump_cp(ws[idx[0]]->Xo, dn * q * 2));
-    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(go, po, st));
+    TP_TRY(dump_cp(ws[g0]->Xo, dn * dq * 2));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(go, st));
     timeline_mark("gemm_o", st);
-    TP_TRY(dump_cp(ng.x[0], dn * d * 4));
+    TP_TRY(dump_cp(ng.x[0], dn * dd * 4));
     if (!(g_dbg_skip & 2)) {
       ::tp::count_launch();
-      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng, d, c.norm_eps));
+      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng));
       TP_CUDA(cudaGetLastError());
     }
     timeline_mark("rmsnorm", st);
-    TP_TRY(dump_cp(ws[idx[0]]->Xd, dn * d * 2));
-    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(ggu, pgu, st));
+    TP_TRY(dump_cp(ws[g0]->Xd, dn * dd * 2));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(ggu, st));
     timeline_mark("gemm_gate_up", st);
-    TP_TRY(dump_cp(ws[idx[0]]->Xf, dn * f * 2));
-    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gdn, pdn, st));
+    TP_TRY(dump_cp(ws[g0]->Xf, dn * df * 2));
+    if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gdn, st));
     timeline_mark("gemm_down", st);
-    TP_TRY(dump_cp(ng.x[0], dn * d * 4));
+    TP_TRY(dump_cp(ng.x[0], dn * dd * 4));
     if (dump) g_dbg_dump = nullptr;
     // input norm of the next slot, for the members that continue
     int nc = 0, maxc = 0;
@@ -745,12 +795,14 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
         nn.x[nc] = ng.x[a];
         nn.xd[nc] = ng.xd[a];
         nn.n[nc] = ng.n[a];
+        nn.d[nc] = ng.d[a];
+        nn.eps[nc] = ng.eps[a];
         maxc = std::max(maxc, ng.n[a]);
         ++nc;
       }
     if (nc && !(g_dbg_skip & 2)) {
       ::tp::count_launch();
-      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxc, nc), dim3(kNormThreads), 0, st, nn, d, c.norm_eps));
+      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxc, nc), dim3(kNormThreads), 0, st, nn));
       TP_CUDA(cudaGetLastError());
       timeline_mark("rmsnorm", st);
     }

@@ -284,6 +284,27 @@ __device__ __forceinline__ void topk_insert(float& lv, int& li, float cv, int ci
   }
 }
 
+// Merge two descending K-lists (K <= 16) held by one warp: lanes 0-15 its own
+// list, lanes 16-31 the partner's reversed (a bitonic sequence of 32); five
+// compare-exchange steps leave the best 16 in lanes 0-15, descending.
+__device__ __forceinline__ void topk_bitonic16(float& lv, int& li, float pv, int pi, int lane) {
+  if (lane >= 16) {
+    lv = pv;
+    li = pi;
+  }
+#pragma unroll
+  for (int st = 16; st >= 1; st >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, lv, st);
+    const int oi = __shfl_xor_sync(0xffffffffu, li, st);
+    const bool lower = (lane & st) == 0;
+    const bool other_better = better(ov, oi, lv, li);
+    if (lower == other_better) {
+      lv = ov;
+      li = oi;
+    }
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(1024) topk_rows_kernel(const float* __restrict__ logits, int V, int k,
                                                          int32_t* __restrict__ out) {
@@ -292,12 +313,34 @@ __global__ void __launch_bounds__(1024) topk_rows_kernel(const float* __restrict
   constexpr int W = 32, U = 8;  // warps; batches loaded per round trip
   __shared__ float sv[W][32];
   __shared__ int si[W][32];
+  __shared__ float smax[W];
   const float* row = logits + (size_t)blockIdx.x * V;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float lv = -INFINITY;
   int li = 0x7fffffff;
-  float tv = -INFINITY;
-  int ti = 0x7fffffff;
+  // A lower bound T on the row's K-th value: the K-th largest of the 32 warps'
+  // first-batch maxima (K distinct row elements are >= it).  Elements below T
+  // are never candidates, which keeps the insertions per warp to a few.
+  float T = -INFINITY;
+  {
+    const int j = w * 32 + lane;
+    const float x = j < V ? __ldg(row + j) : -INFINITY;
+    float m = x != x ? INFINITY : x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) smax[w] = m;
+    __syncthreads();
+    if (V >= W * 32) {
+      const float mine = smax[lane];
+      int above = 0;
+      for (int q = 0; q < W; ++q) above += smax[q] > mine || (smax[q] == mine && q < lane);
+      const unsigned sel = __ballot_sync(0xffffffffu, above == K - 1);
+      T = __shfl_sync(0xffffffffu, mine, __ffs(sel) - 1);
+    }
+  }
+  // candidates: !(x < thr) — NaN, ties and larger values; topk_insert then
+  // applies the exact order (a tie or a stale threshold only costs a no-op insert)
+  float thr = T;
   for (int base0 = w * 32; base0 < V; base0 += U * W * 32) {
     float xs[U];
 #pragma unroll
@@ -309,32 +352,43 @@ __global__ void __launch_bounds__(1024) topk_rows_kernel(const float* __restrict
     for (int u = 0; u < U; ++u) {
       const int j = base0 + u * W * 32 + lane;
       const float x = xs[u];
-      unsigned m = __ballot_sync(0xffffffffu, j < V && better(x, j, tv, ti));
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const float cv = __shfl_sync(0xffffffffu, x, src);
-        const int ci = __shfl_sync(0xffffffffu, j, src);
-        topk_insert(lv, li, cv, ci, K, lane);
+      unsigned m = __ballot_sync(0xffffffffu, !(x < thr) && j < V);
+      if (m) {
+        do {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          const float cv = __shfl_sync(0xffffffffu, x, src);
+          const int ci = __shfl_sync(0xffffffffu, j, src);
+          topk_insert(lv, li, cv, ci, K, lane);
+        } while (m);
+        const float kth = __shfl_sync(0xffffffffu, lv, K - 1);
+        thr = kth != kth ? kth : fmaxf(T, kth);  // a NaN K-th entry: every element stays a candidate
       }
-      tv = __shfl_sync(0xffffffffu, lv, K - 1);
-      ti = __shfl_sync(0xffffffffu, li, K - 1);
     }
   }
-  // tree merge: at each level warp w < half inserts warp w + half's list
+  // tree merge: at each level warp w < half takes in warp w + half's list
   for (int half = W / 2; half >= 1; half >>= 1) {
     if (w >= half && w < 2 * half) {
       sv[w][lane] = lv;
       si[w][lane] = li;
     }
     __syncthreads();
-    if (w < half)
-      for (int r = 0; r < K; ++r) {
-        const float cv = sv[w + half][r];
-        const int ci = si[w + half][r];
-        if (ci == 0x7fffffff) break;  // the partner's list is shorter (V < W * K)
-        topk_insert(lv, li, cv, ci, K, lane);
+    if (w < half) {
+      if (K <= 16) {
+        topk_bitonic16(lv, li, sv[w + half][31 - lane], si[w + half][31 - lane], lane);
+        if (lane >= K) {
+          lv = -INFINITY;
+          li = 0x7fffffff;
+        }
+      } else {
+        for (int r = 0; r < K; ++r) {
+          const float cv = sv[w + half][r];
+          const int ci = si[w + half][r];
+          if (ci == 0x7fffffff) break;  // the partner's list is shorter
+          topk_insert(lv, li, cv, ci, K, lane);
+        }
       }
+    }
     __syncthreads();
   }
   if (w == 0 && lane < k) out[(size_t)blockIdx.x * k + lane] = li;

@@ -262,6 +262,9 @@ int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void* x_dev, in
 int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
                               const int32_t* n, int32_t n_out, int32_t k, void* const* out_dev, int32_t iters,
                               float* ms_per_launch, void* stream);
+// Tests: one heterogeneous grouped K2 launch (member g: its own shape and plan).
+int tp_debug_gemm_hetero(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
+                         const int32_t* n, const int32_t* n_out, const int32_t* k, void* const* out_dev, void* stream);
 /* K4 on caller-provided device logits (tests): n_rows == 1 with children -> out[0] = first argmax,
  * out[1] = first child whose token equals it (or -1); otherwise out[r] = first argmax of row r (fp32). */
 int tp_debug_argmax(int32_t device, const void* logits_dev, int32_t is_f64, int32_t vocab, int32_t n_rows,

@@ -909,3 +909,42 @@ extern "C" int tp_debug_gemm_timed(int32_t device, const void* w_dev, const void
   TP_CUDA(cudaFree(e.counters));
   return TP_OK;
 }
+
+// Diagnostics / tests: ONE heterogeneous grouped launch — member g has its own
+// weights [n_out[g], k[g]], node rows [n[g], k[g]] and plan (kOpStore into out[g]).
+extern "C" int tp_debug_gemm_hetero(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
+                                    const int32_t* n, const int32_t* n_out, const int32_t* k, void* const* out_dev,
+                                    void* stream) {
+  using namespace tp;
+  TP_CUDA(cudaSetDevice(device));
+  TP_CHECK(count >= 1 && count <= kMaxGroup, TP_ESHAPE, "debug GEMM group size");
+  cudaStream_t st = (cudaStream_t)stream;
+  GemmGroup grp;
+  grp.count = count;
+  grp.max_npad = 16;
+  std::vector<void*> bufs;
+  for (int g = 0; g < count; ++g) {
+    TP_CHECK(n[g] >= 1 && n[g] <= 256 && n_out[g] % 128 == 0 && k[g] % 64 == 0, TP_ESHAPE, "debug GEMM shape");
+    GemmMember& m = grp.m[g];
+    TP_TRY(make_tmap_kmajor(&m.a, w_dev[g], n_out[g], k[g], 128));
+    TP_TRY(make_tmap_kmajor(&m.b, x_dev[g], n[g], k[g], 16));
+    m.n = n[g];
+    m.n_pad = std::max(16, (n[g] + 15) / 16 * 16);
+    m.p = sk_plan(n_out[g], k[g], n[g]);
+    grp.max_npad = std::max(grp.max_npad, m.n_pad);
+    m.e = GemmEpi();
+    m.e.op = kOpStore;
+    m.e.out = (float*)out_dev[g];
+    m.e.out_ld = n_out[g];
+    TP_CUDA(cudaMalloc((void**)&m.e.part, sk_part_floats(m.p) * 4));
+    TP_CUDA(cudaMalloc((void**)&m.e.counters, 2 * m.p.mtiles * 4));
+    sk_counters_forget(m.e.counters, 2 * m.p.mtiles * 4);
+    TP_CUDA(cudaMemsetAsync(m.e.counters, 0, 2 * m.p.mtiles * 4, st));
+    bufs.push_back(m.e.part);
+    bufs.push_back(m.e.counters);
+  }
+  TP_TRY(sk_gemm_group(grp, st));
+  TP_CUDA(cudaStreamSynchronize(st));
+  for (void* q : bufs) cudaFree(q);
+  return TP_OK;
+}

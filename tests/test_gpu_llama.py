@@ -51,6 +51,31 @@ def test_tcgen05_gemm_batch_invariant():
         assert torch.equal(part, full[:n]), n
 
 
+def test_tcgen05_gemm_heterogeneous_group_bitwise():
+    """One grouped K2 launch over members of DIFFERENT shapes (each with its own
+    stream-K plan: a draft model's layer next to a target stage's) is bit-identical
+    to each member's own launch."""
+    import ctypes as C
+
+    from paper_2504_04104_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    shapes = [(12288, 4096, 3), (2304, 768, 40), (768, 3072, 17), (4096, 4096, 1)]
+    ws = [(torch.randn((no, k), device="cuda", generator=g) * 0.05).to(torch.bfloat16) for no, k, _ in shapes]
+    xs = [torch.randn((n, k), device="cuda", generator=g).to(torch.bfloat16) for _, k, n in shapes]
+    outs = [torch.zeros((n, no), device="cuda") for no, _, n in shapes]
+    cnt = len(shapes)
+    arr = lambda ts: (C.c_void_p * cnt)(*[t.data_ptr() for t in ts])  # noqa: E731
+    i32 = lambda v: (C.c_int32 * cnt)(*v)  # noqa: E731
+    _lib.check(_lib.lib().tp_debug_gemm_hetero(0, cnt, arr(ws), arr(xs), i32([s[2] for s in shapes]),
+                                               i32([s[0] for s in shapes]), i32([s[1] for s in shapes]), arr(outs),
+                                               torch.cuda.current_stream().cuda_stream))
+    for w, x, o in zip(ws, xs, outs):
+        assert torch.equal(o, gemm(w, x))
+        ref = x.float() @ w.float().t()
+        assert float((o - ref).abs().max()) <= 1e-4 * float(ref.abs().max())
+
+
 def tiny_model(**kw):
     cfg = LlamaConfig(**{**TINY, **kw})
     return cfg, LlamaModel(cfg, max_nodes=64), LlamaOracle(**{**TINY, **kw})

@@ -8,7 +8,9 @@ mode), verification and pruning (oracle/pipeline.py).
 
 Numerics mirrored from csrc/llama.cu and csrc/attn.cu:
   weights      f64 LCG sample * sqrt(3/fan_in)/0.1 -> f32 -> bf16 (RNE)
-  rmsnorm      r = 1/sqrt(mean(x^2) + eps) (f32); h = bf16(x*r)
+  rmsnorm      r = 1/sqrt(mean(x^2) + eps) (f32), folded into the GEMMs as the GPU does:
+               projections of the normed rows = (bf16(x) . W) * r; the LM head's
+               input keeps h = bf16(x*r)
   projections  bf16 inputs, f32 accumulation; residual stream f32
   rope         HF rotate-half, angle = pos * theta^(-2i/128) in f64
   attention    bf16 q/k/v, f32 softmax, P rounded to bf16 before P.V
@@ -148,6 +150,12 @@ class LlamaOracle:
         r = F32(1.0) / np.sqrt(np.mean(x * x, dtype=F32) + F32(self.eps), dtype=F32)
         return bf16(x * r)
 
+    def norm_split(self, x):
+        """The folded RMSNorm: (bf16(x), r) — a projection of the normed row is (h @ W) * r."""
+        x = x.astype(F32)
+        r = F32(1.0) / np.sqrt(np.mean(x * x, dtype=F32) + F32(self.eps), dtype=F32)
+        return bf16(x), r
+
     def rope(self, y, pos):
         ang = pos * self._inv
         c, s = np.cos(ang).astype(F32), np.sin(ang).astype(F32)
@@ -166,10 +174,10 @@ class LlamaOracle:
 
     def block(self, layer, x, kv: OracleKv, rows, append, pos):
         w = self.blocks[layer]
-        h = self.norm(x)
-        q = self.rope(h @ w["wq"], pos)
-        k = self.rope(h @ w["wk"], pos)
-        v = h @ w["wv"]
+        h, r = self.norm_split(x)
+        q = self.rope((h @ w["wq"]) * r, pos)
+        k = self.rope((h @ w["wk"]) * r, pos)
+        v = (h @ w["wv"]) * r
         qb, kb, vb = bf16(q), bf16(k), bf16(v)
         if append:
             kv.put(layer, kb, vb)
@@ -186,9 +194,9 @@ class LlamaOracle:
             p = np.exp(s - s.max()).astype(F32)
             out[hh * 128:(hh + 1) * 128] = (bf16(p) @ vmat) / p.sum(dtype=F32)
         x = x + bf16(out) @ w["wo"]
-        h2 = self.norm(x)
-        g = h2 @ w["wg"]
-        u = h2 @ w["wu"]
+        h2, r2 = self.norm_split(x)
+        g = (h2 @ w["wg"]) * r2
+        u = (h2 @ w["wu"]) * r2
         a = bf16((g / (F32(1.0) + np.exp(-g))) * u)
         return (x + a @ w["wd"]).astype(F32)
 
@@ -213,6 +221,11 @@ class LlamaOracle:
         r = F32(1.0) / np.sqrt(np.mean(x * x, axis=1, dtype=F32) + F32(self.eps), dtype=F32)
         return bf16(x * r[:, None])
 
+    def norm_split_rows(self, x):
+        x = x.astype(F32)
+        r = F32(1.0) / np.sqrt(np.mean(x * x, axis=1, dtype=F32) + F32(self.eps), dtype=F32)
+        return bf16(x), r[:, None]
+
     def rope_rows(self, y, pos):
         ang = np.asarray(pos, dtype=np.float64)[:, None] * self._inv[None, :]
         c, s = np.cos(ang).astype(F32)[:, None, :], np.sin(ang).astype(F32)[:, None, :]
@@ -228,10 +241,10 @@ class LlamaOracle:
         rows are stored first (rows len(kv)-n .. in node order)."""
         w = self.blocks[layer]
         n = x.shape[0]
-        h = self.norm_rows(x)
-        qb = bf16(self.rope_rows(h @ w["wq"], pos))
-        kb = bf16(self.rope_rows(h @ w["wk"], pos))
-        vb = bf16(h @ w["wv"])
+        h, r = self.norm_split_rows(x)
+        qb = bf16(self.rope_rows((h @ w["wq"]) * r, pos))
+        kb = bf16(self.rope_rows((h @ w["wk"]) * r, pos))
+        vb = bf16((h @ w["wv"]) * r)
         if append:
             kv.put_many(layer, kb, vb)
         g = self.heads // self.kv_heads
@@ -247,9 +260,9 @@ class LlamaOracle:
             o = np.einsum("kgr,rkd->kgd", bf16(p), vs) / p.sum(axis=2, dtype=F32)[..., None]
             out[i] = o.reshape(-1)
         x = x + bf16(out) @ w["wo"]
-        h2 = self.norm_rows(x)
-        gg = h2 @ w["wg"]
-        u = h2 @ w["wu"]
+        h2, r2 = self.norm_split_rows(x)
+        gg = (h2 @ w["wg"]) * r2
+        u = (h2 @ w["wu"]) * r2
         a = bf16((gg / (F32(1.0) + np.exp(-gg))) * u)
         return (x + a @ w["wd"]).astype(F32)
 
@@ -258,10 +271,10 @@ class LlamaOracle:
         `pipeline.py:247-254`), computed as one masked attention per KV head."""
         w = self.blocks[layer]
         n = x.shape[0]
-        h = self.norm_rows(x)
-        qb = bf16(self.rope_rows(h @ w["wq"], pos))
-        kb = bf16(self.rope_rows(h @ w["wk"], pos))
-        vb = bf16(h @ w["wv"])
+        h, r = self.norm_split_rows(x)
+        qb = bf16(self.rope_rows((h @ w["wq"]) * r, pos))
+        kb = bf16(self.rope_rows((h @ w["wk"]) * r, pos))
+        vb = bf16((h @ w["wv"]) * r)
         kv.put_many(layer, kb, vb)
         tot = kv.filled[layer]
         r0 = tot - n
@@ -279,9 +292,9 @@ class LlamaOracle:
             p = np.exp(sc - sc.max(axis=1, keepdims=True)).astype(F32)
             out[:, hh] = (bf16(p) @ V[:, kh]) / p.sum(axis=1, dtype=F32)[:, None]
         x = x + bf16(out.reshape(n, -1)) @ w["wo"]
-        h2 = self.norm_rows(x)
-        gg = h2 @ w["wg"]
-        u = h2 @ w["wu"]
+        h2, r2 = self.norm_split_rows(x)
+        gg = (h2 @ w["wg"]) * r2
+        u = (h2 @ w["wu"]) * r2
         a = bf16((gg / (F32(1.0) + np.exp(-gg))) * u)
         return (x + a @ w["wd"]).astype(F32)
 

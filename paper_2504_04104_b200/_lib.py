@@ -16,6 +16,8 @@ from .errors import ConfigError, ContractViolation, InvariantViolation, ShapeErr
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtreepipe_b200.so")
+if os.environ.get("TP_LIB_VARIANT"):  # A/B experiments: an in-tree build variant, libtreepipe_b200.<name>.so
+    LIB_PATH = os.path.join(HERE, f"libtreepipe_b200.{os.environ['TP_LIB_VARIANT']}.so")
 
 TP_OK, TP_ESHAPE, TP_ECONTRACT, TP_EINVARIANT, TP_ECONFIG, TP_ECUDA = range(6)
 ARCH_TOY, ARCH_LLAMA = 0, 1

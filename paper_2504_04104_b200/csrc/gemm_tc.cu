@@ -59,6 +59,7 @@ constexpr int kRedWarps = TP_RED_WARPS;  // stream-K fix-up reducers, fed throug
 constexpr int kThreads = 64 + 32 * (kDrainWarps + kRedWarps);
 constexpr int kRedSlots = kMaxGroup + 1;  // <= one reduction per member per CTA, plus the end sentinel
 constexpr int kBarBytes = 1024;           // mbarriers, TMEM holder, reduction queue
+constexpr int kRsBytes = kMaxGroup * 256 * 4;  // per member and node: the folded RMSNorm scale r
 struct RedItem {
   int g, mt, cnt, cfirst, clast;
 };
@@ -144,11 +145,12 @@ static int g_knob_fixup = 0;  // diagnostics only: 1 skips the reduction, 2 also
 
 static int stages_for(int n_pad) {
   const int per = kABytes + n_pad * 128;
-  return std::min(std::min(kMaxStages, g_knob_max_stages), (g_knob_smem_kb * 1024 - kXchBytes - 1024 - kBarBytes) / per);
+  return std::min(std::min(kMaxStages, g_knob_max_stages),
+                  (g_knob_smem_kb * 1024 - kXchBytes - 1024 - kBarBytes - kRsBytes) / per);
 }
 
 static size_t smem_for(int n_pad) {
-  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + kBarBytes;
+  return (size_t)stages_for(n_pad) * (kABytes + n_pad * 128) + kXchBytes + 1024 /*align*/ + kBarBytes + kRsBytes;
 }
 
 // ---- device --------------------------------------------------------------------
@@ -167,21 +169,28 @@ __device__ __forceinline__ float4 shfl_xor4(float4 v, int m) {
   return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
 }
-__device__ __forceinline__ void st_bf16x4(__nv_bfloat16* p, float a, float b, float c, float d) {
-  uint2 u;
-  u.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
-        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
-  u.y = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(c)) |
-        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d)) << 16);
-  *reinterpret_cast<uint2*>(p) = u;
-}
-
 // Operands the op reads besides y (issued for a batch of nodes before any store).
 struct EpiAux {
   float4 a, b;
+  float r;  // the node's RMSNorm scale (consumers of a folded norm), else 1
 };
 
-__device__ __forceinline__ void epi_aux(const GemmEpi& e, int mt, int f, int c, EpiAux& x) {
+// A node's RMSNorm scale from the producer's per-m-tile partials, in one fixed
+// order (the only place r is ever formed, so this order is the definition): lane l
+// sums partials l, l+32, ... in order, then a butterfly over the lanes;
+// r = 1/sqrt(ss/d + eps).  Warp-uniform.  (Measured: one warp per node beats one
+// thread per node with 8 loads in flight — 1845 vs 1905 us for a lone n=44 forward.)
+__device__ __forceinline__ float norm_scale_from_partials(const float* ssp, int n_part, float d, float eps,
+                                                          int lane) {
+  float s = 0.f;
+  for (int i = lane; i < n_part; i += 32) s = __fadd_rn(s, __ldcg(ssp + i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return 1.0f / sqrtf(s / d + eps);
+}
+
+__device__ __forceinline__ void epi_aux(const GemmEpi& e, int mt, int f, int c, EpiAux& x, const float* rs) {
+  x.r = 1.f;
   if (e.op == kOpResid) {
     x.a = ld4(e.out + (size_t)c * e.out_ld + mt * kBM + f);
   } else if (e.op == kOpQkv && mt < e.H + e.KV) {
@@ -189,25 +198,32 @@ __device__ __forceinline__ void epi_aux(const GemmEpi& e, int mt, int f, int c, 
     x.a = ld4(p);
     x.b = ld4(p + 4);
   }
+  if (e.ssp_in)  // once per node at the kernel's start (lone launches), else here per (node, m-tile)
+    x.r = rs ? rs[c] : norm_scale_from_partials(e.ssp_in + (size_t)c * e.ssp_ld, e.ssp_n, e.norm_d, e.norm_eps, f >> 2);
 }
 
-__device__ __forceinline__ float rope1(float y, float pr, float cs, float sn, bool lo) {
-  return lo ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn));
-}
-__device__ __forceinline__ float silu_mul(float g, float u) {
-  return __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+__device__ __forceinline__ float4 scale4(float4 y, float r) {
+  return make_float4(__fmul_rn(y.x, r), __fmul_rn(y.y, r), __fmul_rn(y.z, r), __fmul_rn(y.w, r));
 }
 
 // Warp-uniform: every lane of the warp calls this for the same node c.
 __device__ __forceinline__ void epi_finish(const GemmEpi& e, int mt, int lane, int c, float4 y, const EpiAux& x) {
   const int f = lane * 4;
+  if (e.ssp_in) y = scale4(y, x.r);  // the folded RMSNorm of this GEMM's input rows
   switch (e.op) {
     case kOpStore:
       st4(e.out + (size_t)c * e.out_ld + mt * kBM + f, y);
       break;
-    case kOpResid:
-      st4(e.out + (size_t)c * e.out_ld + mt * kBM + f, add4(x.a, y));
+    case kOpResid: {
+      const float4 v = add4(x.a, y);
+      st4(e.out + (size_t)c * e.out_ld + mt * kBM + f, v);
+      if (e.xd_out) st_bf16x4(e.xd_out + (size_t)c * e.xd_ld + mt * kBM + f, v.x, v.y, v.z, v.w);
+      if (e.ssp_out) {
+        const float s = tile_sumsq(v);
+        if (lane == 0) e.ssp_out[(size_t)c * e.ssp_ld + mt] = s;
+      }
       break;
+    }
     case kOpSwiglu: {
       const float4 u = shfl_xor4(y, 16);
       if (lane < 16)
@@ -273,7 +289,7 @@ __device__ __forceinline__ float4 sum_partials(const float* base, size_t slot, i
 // reducer warps take nodes round-robin, two per warp in flight.
 template <int NW>
 __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int n, int mt, int cnt, int lo,
-                                             int hi, int ew, int lane) {
+                                             int hi, int ew, int lane, const float* rs) {
   const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
   const size_t slot = (size_t)n * kBM;
   const int f = lane * 4;
@@ -290,7 +306,7 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
         const int c = c0 + r * NW;
         x[r] = EpiAux{};
         if (c < hi) {
-          epi_aux(e, mt, f, c, x[r]);
+          epi_aux(e, mt, f, c, x[r], rs);
           const float* b = base + (size_t)c * kBM + f;
 #pragma unroll
           for (int s = 0; s < 4; ++s) v[r][s] = s < cnt ? ld4cg(b + s * slot) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -314,8 +330,8 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
     const int c2 = c + NW;
     const bool two = c2 < hi;
     EpiAux x0{}, x1{};  // operands of the op first: their loads overlap the partial loads
-    epi_aux(e, mt, f, c, x0);
-    if (two) epi_aux(e, mt, f, c2, x1);
+    epi_aux(e, mt, f, c, x0, rs);
+    if (two) epi_aux(e, mt, f, c2, x1, rs);
     const float4 y0 = sum_partials(base, slot, cnt, c, f);
     const float4 y1 = two ? sum_partials(base, slot, cnt, c2, f) : y0;
     epi_finish(e, mt, lane, c, y0, x0);
@@ -325,7 +341,8 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
 
 // Apply nodes c0 .. c0+cn-1 staged in xch[node][feature] (sole-contributor path).
 template <int NW>
-__device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int cn, const float* xch, int ew,
+__device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int cn, const float* xch, const float* rs,
+                                           int ew,
                                            int lane) {
   const int f = lane * 4;
   for (int cc = ew; cc < cn; cc += 2 * NW) {
@@ -334,8 +351,8 @@ __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int
     const float4 y0 = *reinterpret_cast<const float4*>(xch + cc * kXchLd + f);
     const float4 y1 = two ? *reinterpret_cast<const float4*>(xch + cc2 * kXchLd + f) : y0;
     EpiAux x0{}, x1{};
-    epi_aux(e, mt, f, c0 + cc, x0);
-    if (two) epi_aux(e, mt, f, c0 + cc2, x1);
+    epi_aux(e, mt, f, c0 + cc, x0, rs);
+    if (two) epi_aux(e, mt, f, c0 + cc2, x1, rs);
     epi_finish(e, mt, lane, c0 + cc, y0, x0);
     if (two) epi_finish(e, mt, lane, c0 + cc2, y1, x1);
   }
@@ -380,8 +397,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kMaxStages;
   uint64_t* tempty = tfull + kMaxTmemBufs;
   uint64_t* rfull = tempty + kMaxTmemBufs;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(rfull + kRedSlots);
+  uint64_t* rready = rfull + kRedSlots;  // reducer warps -> all epilogues: rsc is filled
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(rready + 1);
   RedItem* rq = reinterpret_cast<RedItem*>(tholder + 4);
+  float* rsc = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + kBarBytes);  // [member][256]
+  // A lone launch forms each node's folded-RMSNorm scale once, up front; a grouped
+  // one forms it in the epilogues (measured faster there: 2024 vs 1983 us for the
+  // 7-stage forward, while the lone n=44 forward gains 1993 -> 1842 us up front).
+#ifndef TP_PRE_R
+#define TP_PRE_R 1  // 0: always in the epilogues, 1: up front for lone launches, 2: always up front
+#endif
+  constexpr bool kPreR = TP_PRE_R == 2 || (TP_PRE_R == 1 && MG == 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ncols = 32;
   while (ncols < (uint32_t)(nbuf * grp.max_npad)) ncols <<= 1;
@@ -396,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[b], kDrainWarps);
     }
     for (int q = 0; q < kRedSlots; ++q) mbar_init(&rfull[q], 1);
+    mbar_init(rready, kRedWarps);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tholder, ncols);
@@ -500,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int et = threadIdx.x - 64;
     int seg = 0, nq = 0;
+    mbar_wait(rready, 0);  // the members' RMSNorm scales (folded norm) are in rsc
     for (int g = 0; g < grp.count; ++g) {
       const GemmEpi& e = grp.m[g].e;
       const int n = grp.m[g].n, npad = grp.m[g].n_pad;
@@ -530,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (col0 + i < n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
             }
             drain_bar();
-            smem_apply<kDrainWarps>(e, mt, c0, cn, xch, ew, lane);
+            smem_apply<kDrainWarps>(e, mt, c0, cn, xch, kPreR ? rsc + g * 256 : nullptr, ew, lane);
             drain_bar();
           }
           tc_fence_before();
@@ -577,6 +605,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     // waiting on anything but their own MMA: no cycle.
     const int rw = warp - 2 - kDrainWarps;
     const int rt = threadIdx.x - 64 - 32 * kDrainWarps;
+    // first: every member's per-node RMSNorm scale r (a folded norm's consumer), once
+    // per kernel instead of once per (node, m-tile) in the epilogues
+    bool any = false;
+    for (int g = 0; g < grp.count; ++g) any |= grp.m[g].e.ssp_in != nullptr;
+    if (kPreR && any) {
+      pdl_wait();  // the partials come from the previous kernel
+      for (int g = 0; g < grp.count; ++g) {  // one node per reducer warp
+        const GemmEpi& e = grp.m[g].e;
+        if (!e.ssp_in) continue;
+        for (int c = rw; c < grp.m[g].n; c += kRedWarps) {
+          const float rr = norm_scale_from_partials(e.ssp_in + (size_t)c * e.ssp_ld, e.ssp_n, e.norm_d, e.norm_eps,
+                                                    lane);
+          if (lane == 0) rsc[g * 256 + c] = rr;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(rready);
+    mbar_wait(rready, 0);
     for (int q = 0;; ++q) {
       mbar_wait(&rfull[q], 0);
       const RedItem it = rq[q];
@@ -592,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       red_bar();
-      reduce_apply<kRedWarps>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane);
+      reduce_apply<kRedWarps>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane,
+                              kPreR ? rsc + it.g * 256 : nullptr);
     }
   }
   __syncthreads();

@@ -54,6 +54,17 @@ struct GemmEpi {
   // kOpSwiglu
   __nv_bfloat16* xf = nullptr;
   int f = 0;
+  // RMSNorm folded into the GEMMs (no norm kernel): the residual producer (kOpResid)
+  // also writes xd_out = bf16(x) and, per (node, m-tile), the sum of squares of the
+  // tile's 128 new residual values; the consumer (kOpQkv / kOpSwiglu, whose B
+  // operand is that bf16(x)) scales each node's accumulator by
+  // r = 1/sqrt(sum(ssp)/d + eps) before its op (norm weights are 1).
+  __nv_bfloat16* xd_out = nullptr;  // producer: [n][xd_ld]
+  int xd_ld = 0;
+  float* ssp_out = nullptr;  // producer: [n][ssp_ld]
+  const float* ssp_in = nullptr;  // consumer: [n][ssp_ld], ssp_n partials per node
+  int ssp_ld = 0, ssp_n = 0;
+  float norm_d = 1.f, norm_eps = 0.f;
   // stream-K fix-up state
   float* part = nullptr;  // [mtiles][max_contrib][n][128]
   int* counters = nullptr;  // [mtiles] arrival counters, monotonic across launches (see epoch)
@@ -85,6 +96,34 @@ struct GemmGroupT {
 // Host-side group; a launch copies it into a GemmGroupT<1> when it has one member
 // (kernel parameters are copied per launch: ~0.5 KB instead of ~3.6 KB).
 using GemmGroup = GemmGroupT<kMaxGroup>;
+
+__device__ __forceinline__ void st_bf16x4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  uint2 u;
+  u.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+  u.y = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(c)) |
+        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d)) << 16);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+// Sum of squares of a warp's 128 values (lane = 4 consecutive), in the one order
+// every producer of RMSNorm partials uses (the residual epilogue, the prep launch).
+__device__ __forceinline__ float tile_sumsq(float4 v) {
+  float s = __fmul_rn(v.x, v.x);
+  s = __fmaf_rn(v.y, v.y, s);
+  s = __fmaf_rn(v.z, v.z, s);
+  s = __fmaf_rn(v.w, v.w, s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return s;
+}
+
+__device__ __forceinline__ float rope1(float y, float pr, float cs, float sn, bool lo) {
+  return lo ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn));
+}
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  return __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+}
 
 int num_sms();
 int make_tmap_kmajor(CUtensorMap* map, const void* gptr, int64_t rows, int64_t k, int box_rows);

@@ -43,6 +43,7 @@ struct LlamaWs {
   int* counters = nullptr;  // [kCtrKinds][ctr_stride]
   int ctr_stride = 0;
   float* rope = nullptr;  // [np][64][2]
+  float* ssp = nullptr;   // [np][d / 128] RMSNorm partials of the rows in Xd (folded norm)
   CUtensorMap mXd, mXo, mXf;
   CUtensorMap mXq3;  // query rows for the attention run kernel (make_tmap_q3d)
   float *pm = nullptr, *pl = nullptr, *po = nullptr;
@@ -91,28 +92,6 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// RMSNorm of one row held as v[u] = x[threadIdx.x + u * kNormThreads] (1024 threads):
-// the single definition of its arithmetic (rmsnorm_group_kernel and the fused
-// first-layer norm of prep_group_kernel), so a row's bits do not depend on which
-// kernel normalised it.
-constexpr int kNormPerRow = 8;  // d <= 8192
-__device__ __forceinline__ void norm_row(const float (&v)[kNormPerRow], int d, float eps, __nv_bfloat16* out,
-                                         float* red) {
-  float ss = 0.f;
-#pragma unroll
-  for (int u = 0; u < kNormPerRow; ++u) {
-    const int j = threadIdx.x + u * 1024;
-    if (j < d) ss += v[u] * v[u];
-  }
-  ss = block_sum(ss, red);
-  const float r = 1.0f / sqrtf(ss / (float)d + eps);
-#pragma unroll
-  for (int u = 0; u < kNormPerRow; ++u) {
-    const int j = threadIdx.x + u * 1024;
-    if (j < d) out[j] = __float2bfloat16_rn(v[u] * r);
-  }
-}
-
 // Xd[c] = bf16(x[c] * 1/sqrt(mean(x[c]^2) + eps)); one CTA per node row, the
 // same reduction shape at every call site (stage boundaries included).
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
@@ -149,8 +128,8 @@ struct RowCopyGroup {
   float* dst[kMaxBatchItems];
   __nv_bfloat16* xd[kMaxBatchItems];  // the first layer's RMSNorm output (nullptr: none)
   int rows[kMaxBatchItems];
-  int d[kMaxBatchItems];      // the item's model width
-  float eps[kMaxBatchItems];  // and RMSNorm epsilon
+  int d[kMaxBatchItems];  // the item's model width
+  float* ssp[kMaxBatchItems];  // the first layer's RMSNorm partials [rows][d / 128] (with xd)
 };
 // token rows of several items -> their residual-stream rows (fp32), one launch
 struct EmbedGroup {
@@ -160,7 +139,7 @@ struct EmbedGroup {
   int n[kMaxBatchItems];
   const __nv_bfloat16* E[kMaxBatchItems];  // the item's model's embedding table
   int d[kMaxBatchItems];
-  float eps[kMaxBatchItems];
+  float* ssp[kMaxBatchItems];
 };
 // hidden rows handed over from the previous stage -> the member's residual stream
 
@@ -184,39 +163,47 @@ struct PrepGroup {
 __global__ void __launch_bounds__(1024) prep_group_kernel(const __grid_constant__ PrepGroup P) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float red[33];
   int y = blockIdx.y;
   const int x = blockIdx.x;
-  if (y < P.ne + P.nc) {  // one residual-stream row (+ its first-layer RMSNorm)
+  if (y < P.ne + P.nc) {  // one residual-stream row (+ its first layer's bf16 operand and RMSNorm partials)
     const bool emb = y < P.ne;
     const int k = emb ? y : y - P.ne;
     if (x >= (emb ? P.e.n[k] : P.c.rows[k])) return;
     const int d = emb ? P.e.d[k] : P.c.d[k];
-    const float eps = emb ? P.e.eps[k] : P.c.eps[k];
     float* o = (emb ? P.e.out[k] : P.c.dst[k]) + (size_t)x * d;
     __nv_bfloat16* xd = emb ? P.e.xd[k] : P.c.xd[k];
-    float v[kNormPerRow];
+    float v[kNormPer];
     if (emb) {
       const __nv_bfloat16* e = P.e.E[k] + (size_t)P.e.tok[k][x] * d;
 #pragma unroll
-      for (int u = 0; u < kNormPerRow; ++u) {
+      for (int u = 0; u < kNormPer; ++u) {
         const int j = threadIdx.x + u * 1024;
         v[u] = j < d ? __bfloat162float(e[j]) : 0.f;
       }
     } else {
       const float* src = P.c.src[k] + (size_t)x * d;
 #pragma unroll
-      for (int u = 0; u < kNormPerRow; ++u) {
+      for (int u = 0; u < kNormPer; ++u) {
         const int j = threadIdx.x + u * 1024;
         v[u] = j < d ? src[j] : 0.f;
       }
     }
 #pragma unroll
-    for (int u = 0; u < kNormPerRow; ++u) {
+    for (int u = 0; u < kNormPer; ++u) {
       const int j = threadIdx.x + u * 1024;
       if (j < d) o[j] = v[u];
     }
-    if (xd) norm_row(v, d, eps, xd + (size_t)x * d, red);
+    if (xd) {  // bf16(x) and the per-128-column sums of squares, exactly as the residual epilogue
+      float* ssp = emb ? P.e.ssp[k] : P.c.ssp[k];
+      __syncthreads();  // the row's fp32 values are in global memory
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+      for (int mt = w; mt * 128 < d; mt += 32) {
+        const float4 vv = *reinterpret_cast<const float4*>(o + mt * 128 + 4 * l);
+        st_bf16x4(xd + (size_t)x * d + mt * 128 + 4 * l, vv.x, vv.y, vv.z, vv.w);
+        const float s = tile_sumsq(vv);
+        if (l == 0) ssp[(size_t)x * (d / 128) + mt] = s;
+      }
+    }
     return;
   }
   y -= P.ne + P.nc;
@@ -256,7 +243,8 @@ static int build_model_ext(tp_model* m) {
 static void ws_free(LlamaWs* e) {
   if (!e) return;
   for (void* p : {(void*)e->Xd, (void*)e->Xo, (void*)e->Xf, (void*)e->Xq, (void*)e->kself, (void*)e->vself,
-                  (void*)e->part, (void*)e->counters, (void*)e->rope, (void*)e->pm, (void*)e->pl, (void*)e->po})
+                  (void*)e->part, (void*)e->counters, (void*)e->rope, (void*)e->ssp, (void*)e->pm, (void*)e->pl,
+                  (void*)e->po})
     if (p) cudaFree(p);
   delete e;
 }
@@ -326,6 +314,8 @@ static int ws_get(tp_model* m, int g, int min_chunks, LlamaWs** out) {
     TP_CUDA(cudaMalloc(&e->kself, np * kv * 2));
     TP_CUDA(cudaMalloc(&e->vself, np * kv * 2));
     TP_CUDA(cudaMalloc(&e->rope, np * 64 * 2 * 4));
+    TP_CUDA(cudaMalloc(&e->ssp, np * (d / 128) * 4));
+    TP_CUDA(cudaMemset(e->ssp, 0, np * (d / 128) * 4));
     TP_CUDA(cudaMemset(e->Xd, 0, np * d * 2));
     TP_CUDA(cudaMemset(e->Xo, 0, np * q * 2));
     TP_CUDA(cudaMemset(e->Xf, 0, np * f * 2));
@@ -439,33 +429,6 @@ int llama_greedy_rows_wait(tp_model* m, int n, int32_t* out) {
   return TP_OK;
 }
 
-// Grouped rmsnorm: one CTA per (node row, member).
-struct NormGroup {
-  const float* x[kMaxGroup];
-  __nv_bfloat16* xd[kMaxGroup];
-  int n[kMaxGroup];
-  int d[kMaxGroup];
-  float eps[kMaxGroup];
-};
-
-__global__ void __launch_bounds__(kNormThreads) rmsnorm_group_kernel(const __grid_constant__ NormGroup ng) {
-  pdl_wait();
-  pdl_trigger();
-  const int g = blockIdx.y;
-  if ((int)blockIdx.x >= ng.n[g]) return;
-  const int d = ng.d[g];
-  const float eps = ng.eps[g];
-  __shared__ float red[33];
-  const float* xr = ng.x[g] + (size_t)blockIdx.x * d;
-  float v[kNormPerRow];
-#pragma unroll
-  for (int u = 0; u < kNormPerRow; ++u) {
-    const int j = threadIdx.x + u * kNormThreads;
-    v[u] = j < d ? xr[j] : 0.f;
-  }
-  norm_row(v, d, eps, ng.xd[g] + (size_t)blockIdx.x * d, red);
-}
-
 int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* hidden_out, cudaStream_t st) {
   FwdItem it{s, lv, hidden_in};
   FwdMember mb{&it, 1, (float*)hidden_out};
@@ -513,7 +476,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     float* dst;
     __nv_bfloat16* xd;
     int rows, d;
-    float eps;
+    float* ssp;
   };
   std::vector<Copy> copies;
   struct Embed {
@@ -523,7 +486,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     int n;
     const __nv_bfloat16* E;
     int d;
-    float eps;
+    float* ssp;
   };
   std::vector<Embed> embeds;
   int ntot[kMaxGroup], lo[kMaxGroup], hi[kMaxGroup];
@@ -551,14 +514,15 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     for (int r = 0; r < M.count; ++r) {
       const FwdItem& it = M.items[r];
       float* x = M.x + (size_t)offs[g][r] * d;
-      // the first layer's RMSNorm is fused into the prep launch (rows in place are
-      // "copied" onto themselves so that every row of a member with layers gets it)
+      // the first layer's GEMM operand bf16(x) and RMSNorm partials come from the prep
+      // launch (rows in place are "copied" onto themselves so that every row gets them)
       __nv_bfloat16* xd = hi[g] > lo[g] ? ws[g]->Xd + (size_t)offs[g][r] * d : nullptr;
+      float* ssp = ws[g]->ssp + (size_t)offs[g][r] * (d / 128);
       if (it.hin) {
-        if (it.hin != x || xd) copies.push_back({(const float*)it.hin, x, xd, it.lv.n, d, c.norm_eps});
+        if (it.hin != x || xd) copies.push_back({(const float*)it.hin, x, xd, it.lv.n, d, ssp});
       } else {
         TP_CHECK(mg[g]->embed, TP_ECONFIG, "model has no embedding table");
-        embeds.push_back({it.lv.tokens, x, xd, it.lv.n, (const __nv_bfloat16*)mg[g]->embed, d, c.norm_eps});
+        embeds.push_back({it.lv.tokens, x, xd, it.lv.n, (const __nv_bfloat16*)mg[g]->embed, d, ssp});
       }
     }
     slots = std::max(slots, hi[g] - lo[g]);
@@ -594,7 +558,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
         P.e.n[k] = e.n;
         P.e.E[k] = e.E;
         P.e.d[k] = e.d;
-        P.e.eps[k] = e.eps;
+        P.e.ssp[k] = e.ssp;
         mx = std::max(mx, e.n);
       }
       for (int k = 0; k < P.nc; ++k) {
@@ -604,7 +568,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
         P.c.xd[k] = cp.xd;
         P.c.rows[k] = cp.rows;
         P.c.d[k] = cp.d;
-        P.c.eps[k] = cp.eps;
+        P.c.ssp[k] = cp.ssp;
         mx = std::max(mx, cp.rows);
       }
       for (int k = 0; k < P.nr; ++k) {
@@ -660,10 +624,9 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     int idx[kMaxGroup], na = 0;
     for (int g = 0; g < count; ++g)
       if (lo[g] + j < hi[g]) idx[na++] = g;
-    NormGroup ng;
     GemmGroup gq, go, ggu, gdn;
     gq.count = go.count = ggu.count = gdn.count = na;
-    int mx = 16, maxn = 0;
+    int mx = 16;
     aa.clear();
     al.clear();
     for (int a = 0; a < na; ++a) {
@@ -677,14 +640,17 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       const int layer = lo[g] + j, li = layer - c.layer_lo;
       const int n = ntot[g], npad = std::max(16, (n + 15) / 16 * 16);
       mx = std::max(mx, npad);
-      maxn = std::max(maxn, n);
-      ng.x[a] = M.x;
-      ng.xd[a] = e->Xd;
-      ng.n[a] = n;
-      ng.d[a] = d;
-      ng.eps[a] = c.norm_eps;
       const FwdItem& i0 = M.items[0];
+      // RMSNorm folded into the GEMMs: the residual epilogues (o, down) write bf16(x)
+      // and per-m-tile sums of squares; qkv and gate/up scale their rows by r
+      auto norm_in = [&](GemmEpi& ep) {
+        ep.ssp_in = e->ssp;
+        ep.ssp_ld = ep.ssp_n = d / 128;
+        ep.norm_d = (float)d;
+        ep.norm_eps = c.norm_eps;
+      };
       GemmEpi eq = epi_base(e, kCtrQkv);
+      norm_in(eq);
       eq.op = kOpQkv;
       eq.H = H;
       eq.KV = KV;
@@ -705,9 +671,15 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
       er.op = kOpResid;
       er.out = M.x;
       er.out_ld = d;
+      er.xd_out = e->Xd;
+      er.xd_ld = d;
+      er.ssp_out = e->ssp;
+      er.ssp_ld = d / 128;
       GemmEpi ed = er;
       ed.counters = e->counters + (size_t)kCtrDown * e->ctr_stride;
+      if (layer + 1 >= hi[g]) ed.xd_out = nullptr, ed.ssp_out = nullptr;  // the stage's last layer: no consumer
       GemmEpi eg = epi_base(e, kCtrGu);
+      norm_in(eg);
       eg.op = kOpSwiglu;
       eg.xf = e->Xf;
       eg.f = f;
@@ -772,40 +744,15 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     TP_TRY(dump_cp(ws[g0]->Xo, dn * dq * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(go, st));
     timeline_mark("gemm_o", st);
-    TP_TRY(dump_cp(ng.x[0], dn * dd * 4));
-    if (!(g_dbg_skip & 2)) {
-      ::tp::count_launch();
-      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxn, na), dim3(kNormThreads), 0, st, ng));
-      TP_CUDA(cudaGetLastError());
-    }
-    timeline_mark("rmsnorm", st);
+    TP_TRY(dump_cp(mem[g0].x, dn * dd * 4));
     TP_TRY(dump_cp(ws[g0]->Xd, dn * dd * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(ggu, st));
     timeline_mark("gemm_gate_up", st);
     TP_TRY(dump_cp(ws[g0]->Xf, dn * df * 2));
     if (!(g_dbg_skip & 4)) TP_TRY(sk_gemm_group(gdn, st));
     timeline_mark("gemm_down", st);
-    TP_TRY(dump_cp(ng.x[0], dn * dd * 4));
+    TP_TRY(dump_cp(mem[g0].x, dn * dd * 4));
     if (dump) g_dbg_dump = nullptr;
-    // input norm of the next slot, for the members that continue
-    int nc = 0, maxc = 0;
-    NormGroup nn;
-    for (int a = 0; a < na; ++a)
-      if (lo[idx[a]] + j + 1 < hi[idx[a]]) {
-        nn.x[nc] = ng.x[a];
-        nn.xd[nc] = ng.xd[a];
-        nn.n[nc] = ng.n[a];
-        nn.d[nc] = ng.d[a];
-        nn.eps[nc] = ng.eps[a];
-        maxc = std::max(maxc, ng.n[a]);
-        ++nc;
-      }
-    if (nc && !(g_dbg_skip & 2)) {
-      ::tp::count_launch();
-      TP_CUDA(launch_pdl(rmsnorm_group_kernel, dim3(maxc, nc), dim3(kNormThreads), 0, st, nn));
-      TP_CUDA(cudaGetLastError());
-      timeline_mark("rmsnorm", st);
-    }
   }
   return TP_OK;
 }

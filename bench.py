@@ -737,7 +737,7 @@ def stage_profile(args, cfg, model_arg, splits, mean_nodes, ctx, steps_per_token
         pre = np.full(n, ctx, dtype=np.int32)
         bits = ((np.uint64(1) << d.astype(np.uint64)) - np.uint64(1)).reshape(n, 1).astype(np.uint64)
         with torch.cuda.device(dev):
-            x = (torch.randn(n, cfg.hidden, device=f"cuda:{dev}") * 0.5).to(torch.bfloat16)
+            x = torch.randn(n, cfg.hidden, device=f"cuda:{dev}") * 0.5  # fp32 residual-stream rows
             item = (stage.kv, stage.model, x, None, (ctx + d).tolist(), stage.layer_range, False, list(range(n)),
                     False, (pre, ctx, 1, bits))
             last = si == len(r.stages) - 1

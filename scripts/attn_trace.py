@@ -34,7 +34,7 @@ for s, n in zip(r.stages, ns):
     d = rng.integers(0, depth, n)
     pre = np.full(n, prefix, dtype=np.int32)
     bits = ((np.uint64(1) << d.astype(np.uint64)) - np.uint64(1)).reshape(n, 1).astype(np.uint64)
-    x = (torch.randn(n, cfg.hidden, device="cuda") * 0.5).to(torch.bfloat16)
+    x = torch.randn(n, cfg.hidden, device="cuda") * 0.5  # fp32 residual-stream rows
     items.append((s.kv, m, x, None, (prefix + d).tolist(), s.layer_range, False, list(range(n)), False,
                   (pre, prefix, 1, bits)))
 lib = _lib.lib()

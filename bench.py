@@ -743,13 +743,17 @@ def stage_profile(args, cfg, model_arg, splits, mean_nodes, ctx, steps_per_token
             last = si == len(r.stages) - 1
 
             def once():
+                # K4 enqueued, its 16-byte result read by the host once per forward: on its own GPU
+                # the verify stage's next forward does not wait for that read (the pipeline reads
+                # it while the GPU goes on), so the wait is not inside the timed sequence
                 o = forward_members([[item]])[0]
                 if last:
                     stage.model.verify_async(o[0][0:1] if isinstance(o, list) else o[0:1])
-                    stage.model.verify_wait()
 
             for _ in range(3):
                 once()
+                if last:
+                    stage.model.verify_wait()
             torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -757,6 +761,8 @@ def stage_profile(args, cfg, model_arg, splits, mean_nodes, ctx, steps_per_token
                 once()
             e1.record()
             torch.cuda.synchronize(dev)
+            if last:
+                stage.model.verify_wait()
         ms = e0.elapsed_time(e1) / iters
         nl = stage.layer_range[1] - stage.layer_range[0]
         b = nl * (layer_w + (ctx + depth) * 2 * kv_ * 2 + n * 2 * kv_ * 2)

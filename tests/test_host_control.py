@@ -163,3 +163,15 @@ def test_batched_expand_equals_per_node(w, k, levels):
         assert a == b
         tree = tp.layer_append(tree, a)
     assert fast_d._calls == slow_d.inner._calls
+
+
+def test_draft_model_shapes():
+    """The draft-model configs the bench runs (BASELINE configs 2 and 4): the 68M
+    shape with the kernels' 128-wide heads keeps JackFram/llama-68m's parameter
+    count; the 7B draft of config 4 is the 7B target shape with its own seed."""
+    from paper_2504_04104_b200.model import LlamaConfig
+
+    c = LlamaConfig.llama_68m()
+    assert (c.hidden, c.layers, c.ffn, c.vocab, c.heads * c.head_dim) == (768, 2, 3072, 32000, 768)
+    assert abs(c.param_count - 68.0e6) < 0.5e6
+    assert c.seed != LlamaConfig.llama2_7b().seed

@@ -139,7 +139,7 @@ SkPlan sk_plan(int n_out, int k, int n) {
 }
 
 // Tuning knobs (tp_debug_gemm_knob): ring depth cap and smem budget.
-static int g_knob_max_stages = 8;
+static int g_knob_max_stages = getenv("TP_GEMM_MAX_STAGES") ? atoi(getenv("TP_GEMM_MAX_STAGES")) : 8;
 static int g_knob_smem_kb = getenv("TP_GEMM_SMEM_KB") ? atoi(getenv("TP_GEMM_SMEM_KB")) : 200;
 static int g_knob_fixup = 0;  // diagnostics only: 1 skips the reduction, 2 also the partial publish, 3 reduces without waiting for arrivals (WRONG results)
 

@@ -154,6 +154,21 @@ static size_t smem_for(int n_pad) {
 }
 
 // ---- device --------------------------------------------------------------------
+// Diagnostics (built with -DTP_GEMM_TRACE): per-CTA globaltimer stamps of the
+// kernel's phases into a device buffer set by tp_debug_gemm_trace ([grid][16] u64).
+__device__ unsigned long long* g_gemm_trace = nullptr;
+#ifdef TP_GEMM_TRACE
+__device__ __forceinline__ void gemm_stamp(int slot) {
+  unsigned long long* b = g_gemm_trace;
+  if (!b) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  b[blockIdx.x * 16 + slot] = t;
+}
+#define GSTAMP(slot) gemm_stamp(slot)
+#else
+#define GSTAMP(slot) ((void)0)
+#endif
 __device__ __forceinline__ void drain_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kDrainWarps) : "memory"); }
 __device__ __forceinline__ void red_bar() { asm volatile("bar.sync 2, %0;" ::"n"(32 * kRedWarps) : "memory"); }
 
@@ -409,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
   constexpr bool kPreR = TP_PRE_R == 2 || (TP_PRE_R == 1 && MG == 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GSTAMP(0);
   uint32_t ncols = 32;
   while (ncols < (uint32_t)(nbuf * grp.max_npad)) ncols <<= 1;
 
@@ -450,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sA + j * kABytes, &grp.m[0].a, (t % p0.KB) * kBK, (t / p0.KB) * kBM, &full[j], pol_w);
       }
       pdl_wait();  // node rows X come from the previous kernel
+      GSTAMP(1);
       pdl_trigger();
       for (int j = 0; j < npre; ++j) {
         const int kb = (a0 + j) % p0.KB;
@@ -500,6 +517,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = taddr + buf * grp.max_npad;
           for (; t < seg_end; ++t) {
             mbar_wait(&full[stage], phase);
+#ifdef TP_GEMM_TRACE
+            if (g == 0 && t == seg_start && seg == 0) GSTAMP(2);
+#endif
             tc_fence_after();
             const uint64_t ad = desc_kmajor_sw128(sA + stage * kABytes);
             const uint64_t bd = desc_kmajor_sw128(sB + stage * bmax);
@@ -513,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           mma_commit(&tfull[buf]);
+          GSTAMP(3);  // the last one written is the CTA's last accumulator
           ++seg;
         }
       }
@@ -595,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (et == 0) {
+      GSTAMP(4);
       rq[nq].g = -1;
       mbar_arrive(&rfull[nq]);
     }
@@ -635,15 +657,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int E = cend - it.cfirst + 1, rank = c - it.cfirst;
       if (rt == 0 && fixup_mode != 3) {  // counters only grow: this launch's arrivals are complete at (epoch+1)*cnt
         const int target = (e.epoch + 1) * it.cnt;
+        GSTAMP(5);
         while (ld_acquire(&e.counters[it.mt]) < target) {
         }
+        GSTAMP(6);
       }
       red_bar();
       reduce_apply<kRedWarps>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane,
                               kPreR ? rsc + it.g * 256 : nullptr);
+      if (rt == 0) GSTAMP(7);
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) GSTAMP(8);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(taddr, ncols);
@@ -994,5 +1020,12 @@ extern "C" int tp_debug_gemm_hetero(int32_t device, int32_t count, const void* c
   TP_TRY(sk_gemm_group(grp, st));
   TP_CUDA(cudaStreamSynchronize(st));
   for (void* q : bufs) cudaFree(q);
+  return TP_OK;
+}
+
+extern "C" int tp_debug_gemm_trace(int32_t device, void* dev_buf) {
+  TP_CUDA(cudaSetDevice(device));
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  TP_CUDA(cudaMemcpyToSymbol(tp::g_gemm_trace, &p, sizeof(p)));
   return TP_OK;
 }

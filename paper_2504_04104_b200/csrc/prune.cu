@@ -19,6 +19,10 @@
 //                      peer device's buffer: the receiver-side compaction of the
 //                      send-before-verify hand-off).
 // The host reads tau only for its own tree update, after both are enqueued.
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "internal.h"
 
 namespace tp {
@@ -257,6 +261,20 @@ extern "C" int tp_peer_copy(void* dst, int32_t dst_device, const void* src, int3
   TP_CHECK(bytes >= 0 && (bytes == 0 || (dst && src)), TP_ECONFIG, "null argument");
   if (bytes == 0) return TP_OK;
   TP_CUDA(cudaSetDevice(src_device));
+  if (dst_device != src_device) {  // NVLink P2P between the two GPUs, enabled once per ordered pair
+    static std::mutex mu;
+    static std::set<std::pair<int, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({src_device, dst_device}).second) {
+      int can = 0;
+      TP_CUDA(cudaDeviceCanAccessPeer(&can, src_device, dst_device));
+      if (can) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dst_device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) TP_CUDA(e);
+        cudaGetLastError();  // clear an "already enabled"
+      }
+    }
+  }
   TP_CUDA(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, (size_t)bytes, (cudaStream_t)stream));
   return TP_OK;
 }

@@ -409,14 +409,19 @@ def test_sharded_models_pipeline_lossless():
 
 
 @pytest.mark.gpu
-def test_cross_shard_protocol_on_one_gpu():
+@pytest.mark.parametrize("threads", [False, True])
+def test_cross_shard_protocol_on_one_gpu(threads, monkeypatch):
     """The stage-per-GPU step protocol (send-before-verify hand-offs by
     tp_peer_copy, K4's result mirrored to every shard by tp_result_mirror,
     per-shard tp_prune_device with receiver-side compaction of the hand-offs)
     exercised on one GPU with one stream per shard: tokens equal the greedy
     decode, and every step's device keep lists equal the single-shard run's."""
+    import paper_2504_04104_b200.pipeline as PL
     from paper_2504_04104_b200.pipeline import PipelineRunner, split_layers
 
+    # threads: each shard's launches and K3 issued from its own host thread (the
+    # multi-device mode), forced on one device
+    monkeypatch.setattr(PL, "_SHARD_THREADS_FORCE", threads)
     cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=6, heads=2, kv_heads=1, ffn=512)
     full = tp.LlamaModel(cfg, max_nodes=64)
     stages = 6

@@ -448,6 +448,13 @@ def run_ours(args, rank, world):
 
     streams = [torch.cuda.current_stream(d) for d in range(ngpu)]
 
+    def joined(runner):
+        """Device 0's current stream after every shard stream of ``runner`` (stage per GPU:
+        the work runs on shard streams, so an end event must wait for them)."""
+        for st in getattr(runner, "_shard_streams", None) or []:
+            streams[0].wait_stream(st)
+        return streams[0]
+
     def sync_all():
         for d in range(ngpu):
             torch.cuda.synchronize(d)
@@ -484,7 +491,7 @@ def run_ours(args, rank, world):
         ev[0].record(streams[0])
         for _ in range(args.steps):
             runner.decode_step()
-        ev[1].record(streams[-1] if ngpu > 1 else streams[0])
+        ev[1].record(joined(runner))
         sync_all()
         t_wall = time.perf_counter() - t_wall
     gc.enable()
@@ -541,7 +548,7 @@ def run_ours(args, rank, world):
             step_bytes += 2.0 * (dc.layers * (dc.hidden * (dq + 2 * dkv) + dq * dc.hidden + 3 * dc.hidden * dc.ffn)
                                  + dc.vocab * dc.hidden)
         replay.step(ch)
-    e1.record(streams[0])
+    e1.record(joined(replay))
     host_loop_s = time.perf_counter() - th
     sync_all()
     gc.enable()
@@ -565,7 +572,7 @@ def run_ours(args, rank, world):
         d0.record(streams[0])
         for ch in children[pre : pre + args.steps]:
             nd.step(ch)
-        d1.record(streams[0])
+        d1.record(joined(nd))
         sync_all()
         gc.enable()
         no_draft_ms = d0.elapsed_time(d1) / max(1, len(nd.emitted) - ntok0)
@@ -596,7 +603,7 @@ def run_ours(args, rank, world):
     pe0.record(streams[0])
     for ch in children[pre + args.steps + 8 :]:
         replay.step(ch)
-    pe1.record(streams[0])
+    pe1.record(joined(replay))
     sync_all()
     _lib.profile_enable(False)
     by_members = _lib.profile_read_members()
@@ -682,7 +689,7 @@ def run_ours(args, rank, world):
         nsteps = min(args.steps, max(8, len(ref) - len(pr.emitted) - args.stages - 2))
         for _ in range(nsteps):
             pr.decode_step()
-        f1.record(streams[0])
+        f1.record(joined(pr))
         sync_all()
         gc.enable()
         ptok = len(pr.emitted) - pt0

@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--draft-model", default="auto", choices=["auto", "none", "68m", "7b"],
                     help="draft model whose forward runs each step (auto: 68m for 7b/13b targets, 7b for 70b)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-gpus", type=int, default=1,
+                    help="diagnostics: the --gpus N placement (N shard objects, stage-per-GPU protocol on shard "
+                         "streams) on GPU 0")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 leg vs the unmodified reference")
     ap.add_argument("--no-comparators", action="store_true", help="skip the vanilla-PP / cuBLAS comparators")
     ap.add_argument("--no-perfect", action="store_true", help="skip the perfect-draft TBT field")
@@ -350,7 +353,10 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- GPU arm
 
 
-def build_shards(cfg, stages, ngpu, max_nodes):
+def build_shards(cfg, stages, ngpu, max_nodes, emulate=False):
+    """One model object per GPU holding its stages' layers (stage s on GPU s*N/stages);
+    ``emulate``: the same N shard objects all on GPU 0 (the stage-per-GPU protocol on
+    one device, shard streams)."""
     from paper_2504_04104_b200.model import LlamaModel
     from paper_2504_04104_b200.pipeline import split_layers
 
@@ -360,7 +366,7 @@ def build_shards(cfg, stages, ngpu, max_nodes):
     for dev in sorted(set(dev_of)):
         mine = [splits[s] for s in range(stages) if dev_of[s] == dev]
         lo, hi = mine[0][0], mine[-1][1]
-        shards[dev] = LlamaModel(cfg, device=dev, max_nodes=max_nodes, layer_range=(lo, hi),
+        shards[dev] = LlamaModel(cfg, device=0 if emulate else dev, max_nodes=max_nodes, layer_range=(lo, hi),
                                  with_embed=(lo == 0), with_head=(hi == cfg.layers))
     return [shards[dev_of[s]] for s in range(stages)], splits
 
@@ -421,17 +427,19 @@ def run_ours(args, rank, world):
     torch.cuda.set_device(0)
     cfg = model_cfg(args.model)
     t0 = time.perf_counter()
-    shards, splits = build_shards(cfg, args.stages, ngpu, max_nodes=max(64, args.w))
+    emu = args.emulate_gpus > 1
+    shards, splits = build_shards(cfg, args.stages, args.emulate_gpus if emu else ngpu, max_nodes=max(64, args.w),
+                                  emulate=emu)
     torch.cuda.synchronize()
     init_s = time.perf_counter() - t0
     prompt = [int(t) for t in np.random.default_rng([0, 0]).integers(0, cfg.vocab, args.prompt_len)]
     fill = args.stages  # untimed pipeline-fill steps before the W warm-up steps (the pipeline is m deep)
     pre = fill + args.warmup
     n_ref = pre + args.steps + args.profile_steps + 2 * args.stages + 16
-    ref = sequential_decode_staged(shards if ngpu > 1 else shards[0], splits, prompt, n_ref)
+    ref = sequential_decode_staged(shards if (ngpu > 1 or emu) else shards[0], splits, prompt, n_ref)
     pcfg = PipelineConfig(num_stages=args.stages, layer_splits=tuple(splits))
     beam = tp.BeamConfig(w=args.w, k=args.k)
-    model_arg = shards if ngpu > 1 else shards[0]
+    model_arg = shards if (ngpu > 1 or emu) else shards[0]
     dm_name = draft_model_name(args)
     dmodel = None
     if dm_name:
@@ -442,7 +450,8 @@ def run_ours(args, rank, world):
     def fresh(draft, with_draft_model=True):
         r = PipelineRunner(model_arg, pcfg, beam, draft, collect_trace=False,
                            kv_capacity=args.prompt_len + n_ref + args.w * (args.stages + 2) + 64,
-                           check_invariants=False, draft_model=dmodel if with_draft_model else None)
+                           check_invariants=False, draft_model=dmodel if with_draft_model else None,
+                           shard_streams=emu)
         r.prefill(prompt)
         return r
 

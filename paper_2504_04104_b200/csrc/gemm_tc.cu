@@ -28,9 +28,15 @@
 //     SwiGLU, or a plain store).  A sole contributor applies it straight from
 //     TMEM.  The epilogue runs one warp per node row (lane = 4 features, the
 //     RoPE / SwiGLU partner feature is lane^16), two rows in flight per warp.
+//   * folded RMSNorm: residual epilogues also write bf16(x) and per-(node,
+//     m-tile) sums of squares; the consuming GEMM scales each node's fp32
+//     accumulator by r before its op (see GemmEpi in gemm_tc.h);
+//   * members of a grouped launch carry their own stream-K plans, so a launch
+//     may mix shapes (a draft model's layer next to a target stage's).
 // Determinism / batch invariance: segment boundaries depend only on
-// (N_out, K, #SMs); partials are summed in contributor order whichever CTA
-// reduces them; each output column's accumulation chain is the same for any n.
+// (N_out, K, #SMs) of each member; partials are summed in contributor order
+// whichever CTA reduces them; each output column's accumulation chain is the
+// same for any n.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

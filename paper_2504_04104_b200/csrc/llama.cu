@@ -1,22 +1,26 @@
 // Llama-shape stage compute: bf16 weights in HBM, fp32 residual stream.
 //
 // Per layer (reference layer_step structure, `/root/reference/pkg/src/treepipe/
-// model.py:250-280`, with the Llama block: RMSNorm, RoPE, GQA, SwiGLU):
+// model.py:250-280`, with the Llama block: RMSNorm, RoPE, GQA, SwiGLU), with the
+// RMSNorms folded into the GEMMs (no norm kernels):
 //
-//   QKV  = Xd . Wqkv^T      K2 (epilogue: RoPE(q,k); q -> Xq; k,v -> KV rows in place)
-//   attn = tree-attention(Xq, KV, ancestor bits)      K1 (attn.cu)      -> Xo
-//   x   += Xo . Wo^T        K2 (epilogue: residual add)
-//   Xd   = rmsnorm(x)
-//   Xf   = silu(G) * U      K2 over the gate/up weights (64-row interleave; epilogue: SwiGLU)
-//   x   += Xf . Wdown^T     K2 (epilogue: residual add)
-//   Xd   = rmsnorm(x)                                   (input of the next layer)
+//   QKV  = r . (Xd . Wqkv^T)   K2 (epilogue: scale by the node's r, RoPE(q,k); q -> Xq;
+//                                 k,v -> paged KV rows in place)
+//   attn = tree-attention(Xq, KV, ancestor bits)      K1 (attn.cu, 2 launches) -> Xo
+//   x   += Xo . Wo^T           K2 (epilogue: residual add; Xd = bf16(x); per (node,
+//                                 m-tile) sums of squares -> r of the next GEMM)
+//   Xf   = silu(r G) * (r U)   K2 over the gate/up weights (64-row interleave)
+//   x   += Xf . Wdown^T        K2 (epilogue: residual add, Xd = bf16(x) and the sums
+//                                 of squares for the next layer's QKV)
 //
-// 9 launches per layer; every GEMM is a programmatic-dependent launch whose
-// weight prologue overlaps the preceding kernel.
+// 6 launches per layer (plus one prep launch per forward call, which writes the
+// first layer's Xd and sums of squares); every kernel is a programmatic-dependent
+// launch whose prologue overlaps the preceding kernel where resources allow.
 //
 // Numerics (mirrored by oracle/llama.py): GEMM inputs bf16, accumulation and
-// residual fp32; RoPE (HF rotate-half, angle in fp64) on the fp32 GEMM
-// output, then rounded to bf16 for the cache / attention; softmax fp32.
+// residual fp32; r = 1/sqrt(mean(x^2) + eps) applied to the fp32 GEMM output;
+// RoPE (HF rotate-half, angle in fp64) on the fp32 output, then rounded to bf16
+// for the cache / attention; softmax fp32.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -444,7 +448,7 @@ int llama_forward(tp_stage* s, const LevelDev& lv, const void* hidden_in, void* 
 // K/V rows are scattered to each request's cache, and attention runs per item.
 // Diagnostics only (tp_debug_attn_knob 3): skip kernel classes in the layer loop
 // to measure each one's marginal cost inside the PDL chain — results are WRONG
-// while set.  Bits: 1 attention, 2 RMSNorm, 4 GEMMs.
+// while set.  Bits: 1 attention, 4 GEMMs (2, the RMSNorm kernels, no longer exists: folded).
 int g_dbg_skip = 0;
 // Diagnostics only (tp_debug_dump): device buffer receiving member 0's slot-0
 // intermediates of the next forward call: Xd (input RMSNorm, bf16 n x d), Xq

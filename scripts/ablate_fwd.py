@@ -25,7 +25,7 @@ ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--prefix", type=int, default=512)
 ap.add_argument("--n", default="45,35,29,23,17,11,3")
 ap.add_argument("--run", type=int, default=0, help="attention chunks per run (knob 1; 0 = built-in)")
-ap.add_argument("--masks", default="1,2,3,4,7")
+ap.add_argument("--masks", default="1,4,7")
 ap.add_argument("--timeline", action="store_true", help="per kernel-class timeline of each forward (CUDA events)")
 ap.add_argument("--sib", type=float, default=0.0, help="mean sibling-group size (0: every node its own chain)")
 args = ap.parse_args()
@@ -86,7 +86,7 @@ if args.timeline:
         tl = {k: round(v * 1e3 / args.iters, 1) for k, v in sorted(_lib.timeline_read().items(), key=lambda kv: -kv[1])}
         print(f"{name} timeline us/forward: {tl} total {round(sum(tl.values()), 1)}", flush=True)
 
-labels = {0: "full", 1: "-attention", 2: "-rmsnorm", 3: "-attn-norm", 4: "-gemm", 7: "host+prep only"}
+labels = {0: "full", 1: "-attention", 2: "(no-op: norm folded)", 3: "-attention", 4: "-gemm", 7: "host+prep only"}
 for name, members in (("group of %d" % len(ns), [[it] for it in items]), ("single (n=1)", [[items[-1]]])):
     base = timed(members, 0)
     print(f"{name}: full forward {base:8.1f} us", flush=True)

@@ -96,6 +96,37 @@ class DenseKv(OracleKv):
         self.prefix = [self.prefix[i] for i in keep]
 
 
+def _butterfly32(v: np.ndarray) -> np.ndarray:
+    """A warp's xor-butterfly sum over the last axis (32 lanes), float32 adds in the
+    GPU's order (every lane ends with the same value)."""
+    v = v.astype(F32)
+    lanes = np.arange(32)
+    for o in (16, 8, 4, 2, 1):
+        v = (v + v[..., lanes ^ o]).astype(F32)
+    return v[..., 0]
+
+
+def rms_scale_gpu_order(x: np.ndarray, eps: float) -> np.ndarray:
+    """r = 1/sqrt(mean(x^2) + eps) per row, with the GPU's summation order
+    (csrc/gemm_tc.h tile_sumsq and gemm_tc.cu norm_scale_from_partials): per
+    128-column tile, lane l takes columns 4l..4l+3 as x0*x0 then three fused
+    multiply-adds, a 32-lane butterfly gives the tile's partial; lane l then sums
+    partials l, l+32, ... in order and a second butterfly gives the total."""
+    x = np.atleast_2d(np.asarray(x, dtype=F32))
+    n, d = x.shape
+    q = x.reshape(n, d // 128, 32, 4).astype(np.float64)
+    s = (q[..., 0] * q[..., 0]).astype(F32)
+    for j in (1, 2, 3):  # fma: exact product + sum in float64, one rounding to float32
+        s = (q[..., j] * q[..., j] + s.astype(np.float64)).astype(F32)
+    part = _butterfly32(s)  # [n, tiles]
+    tiles = part.shape[1]
+    lanes = np.zeros((n, 32), dtype=F32)
+    for i in range(tiles):
+        lanes[:, i % 32] = (lanes[:, i % 32] + part[:, i]).astype(F32)
+    ss = _butterfly32(lanes)
+    return (F32(1.0) / np.sqrt((ss / F32(d)).astype(F32) + F32(eps), dtype=F32)).astype(F32)
+
+
 def bf16(x) -> np.ndarray:
     """Round float32 values to bfloat16 precision (round-to-nearest-even), kept as float32."""
     a = np.ascontiguousarray(x, dtype=F32)
@@ -153,8 +184,7 @@ class LlamaOracle:
     def norm_split(self, x):
         """The folded RMSNorm: (bf16(x), r) — a projection of the normed row is (h @ W) * r."""
         x = x.astype(F32)
-        r = F32(1.0) / np.sqrt(np.mean(x * x, dtype=F32) + F32(self.eps), dtype=F32)
-        return bf16(x), r
+        return bf16(x), rms_scale_gpu_order(x, self.eps)[0]
 
     def rope(self, y, pos):
         ang = pos * self._inv
@@ -223,8 +253,7 @@ class LlamaOracle:
 
     def norm_split_rows(self, x):
         x = x.astype(F32)
-        r = F32(1.0) / np.sqrt(np.mean(x * x, axis=1, dtype=F32) + F32(self.eps), dtype=F32)
-        return bf16(x), r[:, None]
+        return bf16(x), rms_scale_gpu_order(x, self.eps)[:, None]
 
     def rope_rows(self, y, pos):
         ang = np.asarray(pos, dtype=np.float64)[:, None] * self._inv[None, :]

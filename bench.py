@@ -623,7 +623,7 @@ def run_ours(args, rank, world):
     peak, peak_src = peaks()
     achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
     try:  # measured DRAM traffic of the same kernel (committed ncu capture, see profiles/)
-        with open(os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02f_gemm_traffic.json")) as fh:
             cap = json.load(fh)
     except Exception:  # noqa: BLE001
         cap = None

@@ -23,7 +23,7 @@ wr = sum(v["dram__bytes_write.sum"] for v in per.values()) / n
 alg = float(re.search(r"algorithmic_bytes_per_launch=(\d+)", open(sys.argv[2]).read()).group(1))
 out = {"kernel": "sk_gemm_kernel",
        "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --cache-control none "
-                 "-k regex:sk_gemm, python scripts/profile_step.py --steps 2 (7B, 8 stages, bench workload)",
+                 "-k regex:sk_gemm, python scripts/profile_step.py --steps 2 --draft-model none (7B, 8 stages, bench workload; target GEMMs only)",
        "launches": n, "dram_read_bytes_per_launch": round(rd), "dram_write_bytes_per_launch": round(wr),
        "traffic_bytes_per_launch": round(rd + wr), "algorithmic_bytes_per_launch": round(alg),
        "traffic_over_algorithmic": round((rd + wr) / alg, 3),

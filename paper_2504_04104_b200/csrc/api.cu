@@ -35,6 +35,8 @@ struct TlRec {
 static std::vector<TlRec> g_tl;
 static bool g_tl_on = false;
 static std::mutex g_tl_mu;
+bool timeline_on() { return g_tl_on; }
+
 void timeline_mark(const char* tag, cudaStream_t st) {
   if (!g_tl_on) return;
   cudaEvent_t e;

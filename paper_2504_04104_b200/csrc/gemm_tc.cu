@@ -711,6 +711,28 @@ void sk_counters_forget(const void* base, size_t bytes) {
   }
 }
 
+std::vector<int> sk_epochs_get(const std::vector<int*>& ctr) {
+  std::lock_guard<std::mutex> lk(g_epoch_mu);
+  std::vector<int> v;
+  for (int* c : ctr) {
+    auto it = g_epochs.find(c);
+    v.push_back(it == g_epochs.end() ? -1 : it->second);
+  }
+  return v;
+}
+
+void sk_epochs_set(const std::vector<int*>& ctr, const std::vector<int>& v) {
+  std::lock_guard<std::mutex> lk(g_epoch_mu);
+  for (size_t i = 0; i < ctr.size(); ++i) {
+    if (v[i] < 0)
+      g_epochs.erase(ctr[i]);
+    else
+      g_epochs[ctr[i]] = v[i];
+  }
+}
+
+bool gemm_profile_on() { return g_prof_on; }
+
 int sk_gemm_group(const GemmGroup& grp_in, const SkPlan& p, cudaStream_t st) {
   GemmGroup grp = grp_in;
   for (int g = 0; g < grp.count; ++g) grp.m[g].p = p;  // one plan for every member (same shape)

@@ -3,6 +3,8 @@
 
 #include <cuda.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace tp {
@@ -140,6 +142,10 @@ int sk_gemm_group(const GemmGroup& grp, cudaStream_t st);
 // Forget the launch epochs of counter arrays in [base, base+bytes) (call whenever
 // such memory is (re)allocated and zeroed).
 void sk_counters_forget(const void* base, size_t bytes);
+// The launch epochs of counter arrays (-1: none yet), and setting them back (a
+// captured sequence that is discarded before running).
+std::vector<int> sk_epochs_get(const std::vector<int*>& ctr);
+void sk_epochs_set(const std::vector<int*>& ctr, const std::vector<int>& v);
 
 
 }  // namespace tp

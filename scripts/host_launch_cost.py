@@ -27,6 +27,10 @@ bits = np.zeros((n, 1), dtype=np.uint64)
 x = torch.randn(n, cfg.hidden, device="cuda")
 item = (st.kv, m, x, None, [512] * n, (0, 4), False, list(range(n)), False, (pre, 512, 1, bits))
 lib = _lib.lib()
+side = torch.cuda.Stream()  # a capturable stream (TP_GRAPH=1 engages on non-default streams)
+side.wait_stream(torch.cuda.current_stream())
+ctx = torch.cuda.stream(side)
+ctx.__enter__()
 for mask, label in ((0, "full"), (5, "prep only (GEMM + attention launches skipped)")):
     _lib.check(lib.tp_debug_attn_knob(3, mask))
     for _ in range(20):
@@ -34,13 +38,26 @@ for mask, label in ((0, "full"), (5, "prep only (GEMM + attention launches skipp
     torch.cuda.synchronize()
     l0 = _lib.launch_count()
     dts = []
+    n_calls = 50
     for _ in range(50):  # one call at a time on an idle GPU: no launch-queue back-pressure
         torch.cuda.synchronize()
         t = time.perf_counter()
         forward_members([[item]])
         dts.append(time.perf_counter() - t)
-    dt = float(np.median(dts))
-    nl = (_lib.launch_count() - l0) / 50
+        torch.cuda.synchronize()
+    for _ in range(3):  # and the GPU time of one call
+        forward_members([[item]])
     torch.cuda.synchronize()
-    print(f"{label}: {dt * 1e6:.1f} us host per forward call, {nl:.0f} launches", flush=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        forward_members([[item]])
+    e1.record()
+    torch.cuda.synchronize()
+    gpu_us = e0.elapsed_time(e1) * 1e3 / 20
+    dt = float(np.median(dts))
+    nl = (_lib.launch_count() - l0) / (n_calls + 23)
+    torch.cuda.synchronize()
+    print(f"{label}: {dt * 1e6:.1f} us host per forward call, {nl:.0f} launches, {gpu_us:.1f} us GPU per call "
+          f"(back to back)", flush=True)
 _lib.check(lib.tp_debug_attn_knob(3, 0))

@@ -239,6 +239,8 @@ int tp_synthetic_draft_batch(int32_t count, uint64_t seed, int64_t call_index0, 
 /* ---- instrumentation (no reference counterpart; used by bench.py) ---------- */
 /* Kernels launched by this library since load (every launch site counts). */
 int tp_launch_count(int64_t* out);
+// Instrumentation: CUDA-graph replays of lone forwards so far (TP_GRAPH mode, llama.cu).
+int tp_graph_launches(int64_t* n);
 /* Host<->device bytes moved by this library's own copies since load. */
 int tp_io_bytes(int64_t* h2d, int64_t* d2h);
 /* Time every K2 GEMM launch with CUDA events on its stream while enabled;

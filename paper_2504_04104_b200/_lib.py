@@ -103,6 +103,7 @@ _SIGS = {
     "tp_topk_rows": (C.c_int, [_I, _P, _I, _I, _I, _P, _P]),
     "tp_debug_gemm_hetero": (C.c_int, [_I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "tp_debug_gemm_trace": (C.c_int, [_I, _P]),
+    "tp_graph_launches": (C.c_int, [_P]),
     "tp_debug_gemm_knob": (C.c_int, [_I, _I]),
     "tp_synthetic_draft": (C.c_int, [C.c_uint64, C.c_int64, _I, C.c_double, C.c_double, C.c_double, _I, _I,
                                       _P, _P]),

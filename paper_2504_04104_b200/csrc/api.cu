@@ -49,6 +49,7 @@ void timeline_mark(const char* tag, cudaStream_t st) {
 
 namespace tp {
 extern int g_dbg_skip;
+extern bool g_graph_env;
 extern void* g_dbg_dump;
 }
 
@@ -70,6 +71,10 @@ extern "C" int tp_debug_attn_knob(int32_t knob, int32_t value) {
     return TP_OK;
   }
   if (knob == 1) return tp::attn_set_run(value);
+  if (knob == 5) {  // CUDA-graph mode of lone forwards on capturable streams (llama.cu)
+    tp::g_graph_env = value != 0;
+    return TP_OK;
+  }
   // knobs 0 (tile path) and 2 (shared-prefix tail) were removed
   return (knob == 0 || knob == 2) && value == 0 ? TP_OK : TP_ECONFIG;
 }

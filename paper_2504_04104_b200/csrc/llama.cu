@@ -22,6 +22,7 @@
 // RoPE (HF rotate-half, angle in fp64) on the fp32 output, then rounded to bf16
 // for the cache / attention; softmax fp32.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -466,7 +467,8 @@ void* g_dbg_dump = nullptr;
 // stage: 153 -> 88 us of host time per forward call, 406 -> 398 us of GPU time; but
 // the emulated 8-GPU bench (8 shards on one GPU) shows no end-to-end change (same
 // box: 5.34 / 5.41 vs 5.35 / 5.33 ms/token), so it stays opt-in.
-static const bool g_graph_env = getenv("TP_GRAPH") && atoi(getenv("TP_GRAPH")) != 0;
+bool g_graph_env = getenv("TP_GRAPH") && atoi(getenv("TP_GRAPH")) != 0;  // also tp_debug_attn_knob(5, on)
+std::atomic<long long> g_graph_launches{0};  // graph replays (tp_graph_launches)
 bool timeline_on();
 bool gemm_profile_on();
 
@@ -819,6 +821,7 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
     }
     if (!ok && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
     cudaGraphDestroy(graph);
+    if (exec) g_graph_launches.fetch_add(1, std::memory_order_relaxed);
     if (!exec || cudaGraphLaunch(exec, st) != cudaSuccess) {  // the capture never ran: same fallback
       cudaGetLastError();
       if (exec) cudaGraphExecDestroy(exec);
@@ -832,3 +835,8 @@ int llama_forward_members(const FwdMember* mem, int count, cudaStream_t st, int 
 }
 
 }  // namespace tp
+
+extern "C" int tp_graph_launches(int64_t* n) {
+  *n = tp::g_graph_launches.load();
+  return TP_OK;
+}

@@ -409,8 +409,8 @@ def test_sharded_models_pipeline_lossless():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("threads", [False, True])
-def test_cross_shard_protocol_on_one_gpu(threads, monkeypatch):
+@pytest.mark.parametrize("threads,graphs", [(False, False), (True, False), (False, True)])
+def test_cross_shard_protocol_on_one_gpu(threads, graphs, monkeypatch):
     """The stage-per-GPU step protocol (send-before-verify hand-offs by
     tp_peer_copy, K4's result mirrored to every shard by tp_result_mirror,
     per-shard tp_prune_device with receiver-side compaction of the hand-offs)
@@ -422,6 +422,10 @@ def test_cross_shard_protocol_on_one_gpu(threads, monkeypatch):
     # threads: each shard's launches and K3 issued from its own host thread (the
     # multi-device mode), forced on one device
     monkeypatch.setattr(PL, "_SHARD_THREADS_FORCE", threads)
+    # graphs: each shard's lone forward captured and replayed as a CUDA graph (TP_GRAPH)
+    from paper_2504_04104_b200 import _lib
+
+    _lib.check(_lib.lib().tp_debug_attn_knob(5, int(graphs)))
     cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=6, heads=2, kv_heads=1, ffn=512)
     full = tp.LlamaModel(cfg, max_nodes=64)
     stages = 6
@@ -464,6 +468,7 @@ def test_cross_shard_protocol_on_one_gpu(threads, monkeypatch):
     assert dev1 == dev2
     r1.close()
     r2.close()
+    _lib.check(_lib.lib().tp_debug_attn_knob(5, 0))
 
 
 @pytest.mark.gpu
@@ -521,3 +526,50 @@ def test_draft_model_stage(cross):
     assert r.emitted[:20] == ref[:20]
     assert checked >= 2
     r.release()
+
+
+@pytest.mark.gpu
+def test_cross_shard_graphs_lossless():
+    """One shard per stage (the --gpus 8 placement) on shard streams with the
+    CUDA-graph mode on: every lone stage forward is a graph replay, and tokens and
+    device keep lists equal the same run without graphs."""
+    import ctypes as C
+
+    from paper_2504_04104_b200 import _lib
+    from paper_2504_04104_b200.pipeline import PipelineRunner, split_layers
+
+    cfg = tp.LlamaConfig(vocab=512, hidden=256, layers=6, heads=2, kv_heads=1, ffn=512)
+    full = tp.LlamaModel(cfg, max_nodes=64)
+    stages = 6
+    splits = split_layers(cfg.layers, stages)
+    shards = [tp.LlamaModel(cfg, max_nodes=64, layer_range=sp, with_embed=sp[0] == 0, with_head=sp[1] == cfg.layers)
+              for sp in splits]
+    prompt = [int(t) for t in np.random.default_rng(22).integers(0, cfg.vocab, 60)]
+    ref = tp.sequential_decode(full, prompt, 34)
+
+    def run(graphs):
+        _lib.check(_lib.lib().tp_debug_attn_knob(5, int(graphs)))
+        draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=0.6, rank_decay=0.5, miss_prob=0.1, seed=7),
+                                  cfg.vocab)
+        draft.bind_reference(tuple(prompt) + tuple(ref))
+        r = PipelineRunner(shards, tp.PipelineConfig(num_stages=stages, layer_splits=tuple(splits)),
+                           tp.BeamConfig(w=8, k=4), draft, collect_trace=False, shard_streams=True)
+        r.prefill(prompt)
+        keeps = []
+        while len(r.emitted) < 24:
+            r.decode_step()
+            keeps.append([list(x) for x in r.last_keeps] if r.last_keeps else None)
+        torch.cuda.synchronize()
+        r.release()
+        _lib.check(_lib.lib().tp_debug_attn_knob(5, 0))
+        return r.emitted[:24], keeps
+
+    n0 = C.c_int64()
+    _lib.check(_lib.lib().tp_graph_launches(C.byref(n0)))
+    e_graph, k_graph = run(True)
+    n1 = C.c_int64()
+    _lib.check(_lib.lib().tp_graph_launches(C.byref(n1)))
+    e_plain, k_plain = run(False)
+    assert e_graph == e_plain == ref[:24]
+    assert k_graph == k_plain
+    assert n1.value - n0.value > 24  # lone stage forwards actually ran as graphs

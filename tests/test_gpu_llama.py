@@ -573,3 +573,41 @@ def test_cross_shard_graphs_lossless():
     assert e_graph == e_plain == ref[:24]
     assert k_graph == k_plain
     assert n1.value - n0.value > 24  # lone stage forwards actually ran as graphs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(6))
+def test_pipeline_lossless_randomized(seed):
+    """Losslessness (acceptance 1) over randomized configurations: stage count,
+    beam width / branching, MHA / GQA, a fused draft model, one shard per stage on
+    shard streams (the stage-per-GPU protocol) or one model object — the pipeline's
+    tokens always equal the GPU greedy decode."""
+    from paper_2504_04104_b200.pipeline import PipelineRunner, split_layers
+
+    rng = np.random.default_rng(100 + seed)
+    heads, kv = [(2, 1), (2, 2), (4, 1)][seed % 3]
+    layers = int(rng.integers(4, 9))
+    stages = int(rng.integers(2, min(6, layers) + 1))
+    cfg = tp.LlamaConfig(vocab=512, hidden=128 * heads, layers=layers, heads=heads, kv_heads=kv, ffn=512,
+                         seed=seed)
+    full = tp.LlamaModel(cfg, max_nodes=64)
+    splits = split_layers(layers, stages)
+    sharded = bool(seed % 2)
+    models = ([tp.LlamaModel(cfg, max_nodes=64, layer_range=sp, with_embed=sp[0] == 0, with_head=sp[1] == layers)
+               for sp in splits] if sharded else full)
+    dm = (tp.LlamaModel(tp.LlamaConfig(vocab=512, hidden=256, layers=1, heads=2, kv_heads=2, ffn=256, seed=50 + seed),
+                        max_nodes=64) if seed % 3 != 1 else None)
+    prompt = [int(t) for t in rng.integers(0, cfg.vocab, int(rng.integers(20, 90)))]
+    ref = tp.sequential_decode(full, prompt, 30)
+    w, k = int(rng.integers(2, 17)), int(rng.integers(2, 7))
+    draft = tp.SyntheticDraft(tp.SyntheticDraftConfig(top1_hit=float(rng.uniform(0.3, 0.8)), rank_decay=0.5,
+                                                      miss_prob=float(rng.uniform(0.0, 0.2)), seed=seed), cfg.vocab)
+    draft.bind_reference(tuple(prompt) + tuple(ref))
+    r = PipelineRunner(models, tp.PipelineConfig(num_stages=stages, layer_splits=tuple(splits)), tp.BeamConfig(w=w, k=k),
+                       draft, collect_trace=False, shard_streams=sharded, draft_model=dm)
+    r.prefill(prompt)
+    while len(r.emitted) < 20:
+        r.decode_step()
+    torch.cuda.synchronize()
+    assert r.emitted[:20] == ref[:20], (seed, stages, w, k, heads, kv, sharded, dm is not None)
+    r.release()

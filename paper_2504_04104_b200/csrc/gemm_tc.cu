@@ -162,14 +162,23 @@ static size_t smem_for(int n_pad) {
 // ---- device --------------------------------------------------------------------
 // Diagnostics (built with -DTP_GEMM_TRACE): per-CTA globaltimer stamps of the
 // kernel's phases into a device buffer set by tp_debug_gemm_trace ([grid][16] u64).
+// Launches are numbered in start order (every CTA of launch i starts before any of
+// launch i+1: PDL releases a dependent only after all CTAs triggered), so a chain
+// of launches lands in consecutive [launch][grid][16] records (kTraceLaunches max).
 __device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ unsigned int g_gemm_trace_ctr = 0;
+constexpr int kTraceLaunches = 64;
 #ifdef TP_GEMM_TRACE
 __device__ __forceinline__ void gemm_stamp(int slot) {
   unsigned long long* b = g_gemm_trace;
   if (!b) return;
+  __shared__ unsigned int s_launch;
+  if (slot == 0) s_launch = atomicAdd(&g_gemm_trace_ctr, 1u) / gridDim.x;
+  const unsigned int l = s_launch;
+  if (l >= kTraceLaunches) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  b[blockIdx.x * 16 + slot] = t;
+  b[((size_t)l * gridDim.x + blockIdx.x) * 16 + slot] = t;
 }
 #define GSTAMP(slot) gemm_stamp(slot)
 #else
@@ -246,10 +255,13 @@ __device__ __forceinline__ void epi_finish(const GemmEpi& e, int mt, int lane, i
       break;
     }
     case kOpSwiglu: {
-      const float4 u = shfl_xor4(y, 16);
-      if (lane < 16)
-        st_bf16x4(e.xf + (size_t)c * e.f + mt * 64 + f, silu_mul(y.x, u.x), silu_mul(y.y, u.y), silu_mul(y.z, u.z),
-                  silu_mul(y.w, u.w));
+      // lanes 0-15 hold gate features 4l..4l+3, lanes 16-31 the matching up features:
+      // after the exchange each half forms two of the four outputs (all 32 lanes busy)
+      const float4 p = shfl_xor4(y, 16);
+      const bool lo = lane < 16;
+      const float g0 = lo ? y.x : p.z, g1 = lo ? y.y : p.w;
+      const float u0 = lo ? p.x : y.z, u1 = lo ? p.y : y.w;
+      st_bf16x2(e.xf + (size_t)c * e.f + mt * 64 + (lane & 15) * 4 + (lo ? 0 : 2), silu_mul(g0, u0), silu_mul(g1, u1));
       break;
     }
     default: {  // kOpQkv: tile mt is head mt of [q heads | k heads | v heads]
@@ -574,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[buf], bphase);
         tc_fence_after();
         const uint32_t tbase = taddr + ((uint32_t)(quarter * 32) << 16) + buf * grp.max_npad;
+        if (et == 0) GSTAMP(cnt == 1 ? 9 : 11);  // the accumulator is ready (sole-owner / partial segment)
         if (cnt == 1) {
           for (int c0 = 0; c0 < n; c0 += kXchNodes) {
             const int cn = min(kXchNodes, n - c0);
@@ -585,12 +598,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (col0 + i < n) xch[(col0 - c0 + i) * kXchLd + r] = v[i];
             }
             drain_bar();
+            if (et == 0 && c0 == 0) GSTAMP(14);
             smem_apply<kDrainWarps>(e, mt, c0, cn, xch, kPreR ? rsc + g * 256 : nullptr, ew, lane);
             drain_bar();
+            if (et == 0 && c0 == 0) GSTAMP(15);
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
+          if (et == 0) GSTAMP(10);
         } else {
           // stream-K fix-up: publish this CTA's fp32 partial of the m-tile
           float* dst = e.part + ((size_t)(mt * p.max_contrib + (c - cfirst)) * n) * kBM + r;
@@ -606,6 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM free: the MMA may go on
           drain_bar();
           if (et == 0) {  // barrier + one gpu-scope fence publishes every drain thread's stores
+            GSTAMP(12);
             red_release_add(&arrive[mt], 1);  // release: every drain thread's partial stores (ordered by the barrier)
             // the contributors whose ranges end inside the tile reduce it, each a
             // slice of the nodes (they finish together; one CTA reducing a whole
@@ -652,6 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(rready);
     mbar_wait(rready, 0);
+    if (rt == 0) GSTAMP(13);
     for (int q = 0;; ++q) {
       mbar_wait(&rfull[q], 0);
       const RedItem it = rq[q];
@@ -782,7 +800,12 @@ int sk_gemm_group(const GemmGroup& grp_in, cudaStream_t st) {
       const int need = (int)std::max(smem_for(256), smem_for(16));
       int optin = 0;
       TP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-      const int lim = std::max(need, std::min(optin, 232448));
+      cudaFuncAttributes fa{};  // static shared memory (trace builds) comes off the opt-in ceiling
+      if (one)
+        TP_CUDA(cudaFuncGetAttributes(&fa, sk_gemm_kernel<1>));
+      else
+        TP_CUDA(cudaFuncGetAttributes(&fa, sk_gemm_kernel<kMaxGroup>));
+      const int lim = std::max(need, std::min(optin - (int)fa.sharedSizeBytes, 232448));
       if (one)
         TP_CUDA(cudaFuncSetAttribute(sk_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
       else
@@ -1055,5 +1078,7 @@ extern "C" int tp_debug_gemm_trace(int32_t device, void* dev_buf) {
   TP_CUDA(cudaSetDevice(device));
   unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
   TP_CUDA(cudaMemcpyToSymbol(tp::g_gemm_trace, &p, sizeof(p)));
+  const unsigned int zero = 0;
+  TP_CUDA(cudaMemcpyToSymbol(tp::g_gemm_trace_ctr, &zero, sizeof(zero)));
   return TP_OK;
 }

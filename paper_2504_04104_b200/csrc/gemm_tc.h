@@ -108,6 +108,11 @@ __device__ __forceinline__ void st_bf16x4(__nv_bfloat16* p, float a, float b, fl
   *reinterpret_cast<uint2*>(p) = u;
 }
 
+__device__ __forceinline__ void st_bf16x2(__nv_bfloat16* p, float a, float b) {
+  *reinterpret_cast<uint32_t*>(p) = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+                                    ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+}
+
 // Sum of squares of a warp's 128 values (lane = 4 consecutive), in the one order
 // every producer of RMSNorm partials uses (the residual epilogue, the prep launch).
 __device__ __forceinline__ float tile_sumsq(float4 v) {
@@ -123,8 +128,12 @@ __device__ __forceinline__ float tile_sumsq(float4 v) {
 __device__ __forceinline__ float rope1(float y, float pr, float cs, float sn, bool lo) {
   return lo ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(pr, sn));
 }
+// silu(g) * u with the approximate exp / divide (ex2.approx, rcp.approx: a few ulp,
+// far below the bf16 rounding of the result).  The IEEE expf + __fdiv_rn chain
+// cost ~2 us of a gate/up launch's tail at n=45 (its epilogue is latency-bound on
+// 4 or 8 warps; scripts/gemm_chain_trace.py).
 __device__ __forceinline__ float silu_mul(float g, float u) {
-  return __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+  return __fmul_rn(__fdividef(g, __fadd_rn(1.0f, __expf(-g))), u);
 }
 
 int num_sms();

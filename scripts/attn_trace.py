@@ -22,7 +22,7 @@ mask = int(os.environ.get("MASK", "0"))
 prefix = int(os.environ.get("PREFIX", "512"))
 cfg = model_cfg("7b")
 m = LlamaModel(cfg, max_nodes=64)
-ns = [45, 35, 29, 23, 17, 11, 3]
+ns = [int(x) for x in os.environ.get("NS", "45,35,29,23,17,11,3").split(",")]
 depth = 12
 prompt = [int(t) for t in np.random.default_rng(1).integers(0, cfg.vocab, prefix + depth)]
 r = PipelineRunner(m, PipelineConfig(num_stages=8), tp.BeamConfig(w=64, k=16), None, collect_trace=False,

@@ -14,7 +14,7 @@ Numerics mirrored from csrc/llama.cu and csrc/attn.cu:
   projections  bf16 inputs, f32 accumulation; residual stream f32
   rope         HF rotate-half, angle = pos * theta^(-2i/128) in f64
   attention    bf16 q/k/v, f32 softmax, P rounded to bf16 before P.V
-  swiglu       bf16(g / (1 + exp(-g)) * u)
+  swiglu       bf16(g / (1 + exp(-g)) * u)  (the GPU: ex2.approx / rcp.approx, a few ulp before the bf16 rounding)
 The GPU accumulates in different orders (tensor-core tiles, online softmax
 over 64-slot chunks), so comparisons use a stated tolerance.
 """

@@ -267,7 +267,7 @@ int tp_debug_gemm_group_timed(int32_t device, int32_t count, const void* const* 
 // Tests: one heterogeneous grouped K2 launch (member g: its own shape and plan).
 int tp_debug_gemm_hetero(int32_t device, int32_t count, const void* const* w_dev, const void* const* x_dev,
                          const int32_t* n, const int32_t* n_out, const int32_t* k, void* const* out_dev, void* stream);
-// Diagnostics: device buffer [launch < 64][grid][16] u64 receiving K2 phase timestamps, launches numbered
+// Diagnostics: device buffer [launch < 64][grid][32] u64 receiving K2 phase timestamps, launches numbered
 // from this call in start order (builds with -DTP_GEMM_TRACE).
 int tp_debug_gemm_trace(int32_t device, void* dev_buf);
 /* K4 on caller-provided device logits (tests): n_rows == 1 with children -> out[0] = first argmax,

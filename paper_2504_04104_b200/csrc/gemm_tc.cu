@@ -178,7 +178,7 @@ __device__ __forceinline__ void gemm_stamp(int slot) {
   if (l >= kTraceLaunches) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  b[((size_t)l * gridDim.x + blockIdx.x) * 16 + slot] = t;
+  b[((size_t)l * gridDim.x + blockIdx.x) * 32 + slot] = t;
 }
 #define GSTAMP(slot) gemm_stamp(slot)
 #else
@@ -441,12 +441,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define TP_PRE_R 1  // 0: always in the epilogues, 1: up front for lone launches, 2: always up front
 #endif
   constexpr bool kPreR = TP_PRE_R == 2 || (TP_PRE_R == 1 && MG == 1);
+#ifndef TP_EARLY_PROLOGUE
+#define TP_EARLY_PROLOGUE 1
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GSTAMP(0);
   uint32_t ncols = 32;
   while (ncols < (uint32_t)(nbuf * grp.max_npad)) ncols <<= 1;
 
+  // member 0's first k-blocks: their weights do not depend on the previous kernel
+  const int nbox0 = grp.m[0].n_pad / 16;
+  int a0, b0;
+  range(0, a0, b0);
+  const int npre = min(stages, b0 - a0);
   if (warp == 0 && lane == 0) {
+#if TP_EARLY_PROLOGUE
+    // the tensor maps are the first thing fetched (parameter space, cold at each
+    // launch), and the weight ring is filled before the CTA-wide barrier
+    for (int g = 0; g < grp.count; ++g) {
+      tma_prefetch(&grp.m[g].a);
+      tma_prefetch(&grp.m[g].b);
+    }
+#endif
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -458,31 +474,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int q = 0; q < kRedSlots; ++q) mbar_init(&rfull[q], 1);
     mbar_init(rready, kRedWarps);
     fence_barrier_init();
+    GSTAMP(16);
+#if TP_EARLY_PROLOGUE
+    const SkPlan& p0 = grp.m[0].p;
+    const uint64_t pol_w = policy_evict_first();
+    for (int j = 0; j < npre; ++j) {
+      const int t = a0 + j;
+      mbar_expect_tx(&full[j], kABytes + nbox0 * 2048);
+      tma_load_2d(sA + j * kABytes, &grp.m[0].a, (t % p0.KB) * kBK, (t / p0.KB) * kBM, &full[j], pol_w);
+    }
+    GSTAMP(20);
+#endif
   }
-  if (warp == 1) tmem_alloc(tholder, ncols);
+  if (warp == 1) {
+    tmem_alloc(tholder, ncols);
+    if (lane == 0) GSTAMP(17);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t taddr = *tholder;
+  if (threadIdx.x == 0) GSTAMP(18);
 
   if (warp == 0) {
     if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      const SkPlan& p0 = grp.m[0].p;
+#if !TP_EARLY_PROLOGUE
       for (int g = 0; g < grp.count; ++g) {
         tma_prefetch(&grp.m[g].a);
         tma_prefetch(&grp.m[g].b);
       }
-      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-      // member 0's weights do not depend on the previous kernel: fill the ring now
-      const int nbox0 = grp.m[0].n_pad / 16;
-      const SkPlan& p0 = grp.m[0].p;
-      int a0, b0;
-      range(0, a0, b0);
-      const int npre = min(stages, b0 - a0);
+      GSTAMP(19);
       for (int j = 0; j < npre; ++j) {
         const int t = a0 + j;
         mbar_expect_tx(&full[j], kABytes + nbox0 * 2048);
         tma_load_2d(sA + j * kABytes, &grp.m[0].a, (t % p0.KB) * kBK, (t / p0.KB) * kBM, &full[j], pol_w);
       }
+      GSTAMP(20);
+#endif
       pdl_wait();  // node rows X come from the previous kernel
       GSTAMP(1);
       pdl_trigger();

@@ -44,7 +44,7 @@ lib = _lib.lib()
 for _ in range(5):
     forward_members(members)
 torch.cuda.synchronize()
-buf = torch.zeros(64 * 148 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(64 * 148 * 32, dtype=torch.int64, device="cuda")
 _lib.check(lib.tp_debug_gemm_trace(0, buf.data_ptr()))
 torch.cuda.profiler.start()  # ncu --profile-from-start off captures this forward only
 forward_members(members)
@@ -54,7 +54,7 @@ _lib.check(lib.tp_debug_gemm_trace(0, None))
 if not (buf != 0).any():
     print("no trace (library built without -DTP_GEMM_TRACE)")
     sys.exit(0)
-t = buf.view(64, 148, 16)[:, :, :16].cpu().numpy().astype(np.float64)
+t = buf.view(64, 148, 32)[:, :, :21].cpu().numpy().astype(np.float64)
 live = [i for i in range(64) if (t[i, :, 0] > 0).any()]
 t0 = t[live[0], :, 0][t[live[0], :, 0] > 0].min()
 ops = ["qkv", "o", "gu", "down"]
@@ -81,9 +81,20 @@ if os.environ.get("DETAIL"):  # the latest-ending CTAs of one launch, all stamps
     ok = np.nonzero(a[:, 0] > 0)[0]
     s0 = a[ok, 0].min()
     names = ["start", "pdl", "mma0", "mmaN", "drain", "spin0", "spin1", "red", "end", "sole0", "sole1", "part0",
-             "part1", "rsc", "stg0", "app0"]
+             "part1", "rsc", "stg0", "app0", "bar_init", "tmem", "sync", "tmap_pf", "w_issued"]
     for c in ok[np.argsort(-a[ok, 8])][:12]:
         print(f"cta {c:3d}: " + " ".join(f"{nm} {(a[c, k] - s0) / 1e3:5.1f}" if a[c, k] > 0 else f"{nm}   -  "
                                          for k, nm in enumerate(names)))
     med = np.nanmedian(np.where(a[ok] > 0, a[ok] - s0, np.nan) / 1e3, axis=0)
     print("median : " + " ".join(f"{nm} {med[k]:5.1f}" for k, nm in enumerate(names)))
+if os.environ.get("PROLOGUE"):  # per-CTA prologue, us from each CTA's own start (median / p90 over CTAs and launches)
+    cols = [("bar_init", 16), ("tmem", 17), ("sync", 18), ("tmap_pf", 19), ("w_issued", 20), ("pdl", 1), ("mma0", 2)]
+    for j, op in enumerate(ops):
+        rel = {nm: [] for nm, _ in cols}
+        for i in live[j::4]:
+            a = t[i]
+            ok = (a[:, 0] > 0)
+            for nm, k in cols:
+                v = a[ok, k] - a[ok, 0]
+                rel[nm] += list(v[a[ok, k] > 0] / 1e3)
+        print(f"{op:4s} " + "  ".join(f"{nm} {np.median(v):4.2f}/{np.percentile(v, 90):4.2f}" for nm, v in rel.items() if v))

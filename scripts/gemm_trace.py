@@ -23,7 +23,7 @@ ap.add_argument("--n", default="1,48")
 args = ap.parse_args()
 lib = _lib.lib()
 st = torch.cuda.current_stream().cuda_stream
-buf = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 names = ["start", "tma_pdl", "mma_first", "mma_last", "drain_done", "spin_start", "spin_end", "red_done", "end"]
 for shape in args.shape.split(","):
     n_out, k = SH[shape]
@@ -39,7 +39,7 @@ for shape in args.shape.split(","):
         _lib.check(lib.tp_debug_gemm_timed(0, w.data_ptr(), x.data_ptr(), n, n_out, k, out.data_ptr(), 1,
                                            C.byref(ms), st))
         _lib.check(lib.tp_debug_gemm_trace(0, None))
-        t = buf.view(148, 16)[:, :9].cpu().numpy().astype(np.float64)
+        t = buf.view(148, 32)[:, :9].cpu().numpy().astype(np.float64)
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
         row = []

@@ -319,20 +319,26 @@ __device__ __forceinline__ float4 sum_partials(const float* base, size_t slot, i
 }
 
 // Reduce + apply nodes [lo, hi) of m-tile mt from the global partials; the NW
-// reducer warps take nodes round-robin, two per warp in flight.
+// reducer warps take nodes round-robin.
 template <int NW>
 __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int n, int mt, int cnt, int lo,
                                              int hi, int ew, int lane, const float* rs) {
   const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
   const size_t slot = (size_t)n * kBM;
   const int f = lane * 4;
-  if (cnt <= 4) {
+  // Every inlined copy of the epilogue op is instruction footprint the kernel's
+  // tail pays for in instruction-cache misses (the dominant stall of the
+  // epilogues, ncu source counters): two rows per batch and one row at a time
+  // elsewhere (measured against four rows / two rows in flight, same box: lone
+  // n=1 / n=44 forwards -1.7 % / -2.7 %, the 7-stage group -1.1 %).
+  constexpr int kMaxC = 4;
+  if (cnt <= kMaxC) {
     // The tail of the kernel: every load of a batch of kRows rows (their cnt
     // partials and the op's operands) is issued before any arithmetic, so the
-    // reduction costs one L2 round trip per batch instead of one per row pair.
-    constexpr int kRows = 4;
+    // reduction costs one L2 round trip per batch instead of one per row.
+    constexpr int kRows = 2;
     for (int c0 = lo + ew; c0 < hi; c0 += kRows * NW) {
-      float4 v[kRows][4];
+      float4 v[kRows][kMaxC];
       EpiAux x[kRows];
 #pragma unroll
       for (int r = 0; r < kRows; ++r) {
@@ -342,7 +348,7 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
           epi_aux(e, mt, f, c, x[r], rs);
           const float* b = base + (size_t)c * kBM + f;
 #pragma unroll
-          for (int s = 0; s < 4; ++s) v[r][s] = s < cnt ? ld4cg(b + s * slot) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int s = 0; s < kMaxC; ++s) v[r][s] = s < cnt ? ld4cg(b + s * slot) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
 #pragma unroll
@@ -351,7 +357,7 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
         if (c < hi) {
           float4 acc = v[r][0];  // contributor order, as sum_partials
 #pragma unroll
-          for (int s = 1; s < 4; ++s)
+          for (int s = 1; s < kMaxC; ++s)
             if (s < cnt) acc = add4(acc, v[r][s]);
           epi_finish(e, mt, lane, c, acc, x[r]);
         }
@@ -359,16 +365,10 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
     }
     return;
   }
-  for (int c = lo + ew; c < hi; c += 2 * NW) {
-    const int c2 = c + NW;
-    const bool two = c2 < hi;
-    EpiAux x0{}, x1{};  // operands of the op first: their loads overlap the partial loads
+  for (int c = lo + ew; c < hi; c += NW) {
+    EpiAux x0{};
     epi_aux(e, mt, f, c, x0, rs);
-    if (two) epi_aux(e, mt, f, c2, x1, rs);
-    const float4 y0 = sum_partials(base, slot, cnt, c, f);
-    const float4 y1 = two ? sum_partials(base, slot, cnt, c2, f) : y0;
-    epi_finish(e, mt, lane, c, y0, x0);
-    if (two) epi_finish(e, mt, lane, c2, y1, x1);
+    epi_finish(e, mt, lane, c, sum_partials(base, slot, cnt, c, f), x0);
   }
 }
 
@@ -378,16 +378,11 @@ __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int
                                            int ew,
                                            int lane) {
   const int f = lane * 4;
-  for (int cc = ew; cc < cn; cc += 2 * NW) {
-    const int cc2 = cc + NW;
-    const bool two = cc2 < cn;
+  for (int cc = ew; cc < cn; cc += NW) {
     const float4 y0 = *reinterpret_cast<const float4*>(xch + cc * kXchLd + f);
-    const float4 y1 = two ? *reinterpret_cast<const float4*>(xch + cc2 * kXchLd + f) : y0;
-    EpiAux x0{}, x1{};
+    EpiAux x0{};
     epi_aux(e, mt, f, c0 + cc, x0, rs);
-    if (two) epi_aux(e, mt, f, c0 + cc2, x1, rs);
     epi_finish(e, mt, lane, c0 + cc, y0, x0);
-    if (two) epi_finish(e, mt, lane, c0 + cc2, y1, x1);
   }
 }
 

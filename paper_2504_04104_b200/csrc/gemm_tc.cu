@@ -219,6 +219,9 @@ __device__ __forceinline__ float norm_scale_from_partials(const float* ssp, int 
   return 1.0f / sqrtf(s / d + eps);
 }
 
+// PRE: the node scales r were formed up front into rs (lone launches); else each
+// epilogue forms r from the partials (a compile-time choice: one path per kernel).
+template <bool PRE>
 __device__ __forceinline__ void epi_aux(const GemmEpi& e, int mt, int f, int c, EpiAux& x, const float* rs) {
   x.r = 1.f;
   if (e.op == kOpResid) {
@@ -228,8 +231,12 @@ __device__ __forceinline__ void epi_aux(const GemmEpi& e, int mt, int f, int c, 
     x.a = ld4(p);
     x.b = ld4(p + 4);
   }
-  if (e.ssp_in)  // once per node at the kernel's start (lone launches), else here per (node, m-tile)
-    x.r = rs ? rs[c] : norm_scale_from_partials(e.ssp_in + (size_t)c * e.ssp_ld, e.ssp_n, e.norm_d, e.norm_eps, f >> 2);
+  if (e.ssp_in) {  // once per node at the kernel's start (lone launches), else here per (node, m-tile)
+    if constexpr (PRE)
+      x.r = rs[c];
+    else
+      x.r = norm_scale_from_partials(e.ssp_in + (size_t)c * e.ssp_ld, e.ssp_n, e.norm_d, e.norm_eps, f >> 2);
+  }
 }
 
 __device__ __forceinline__ float4 scale4(float4 y, float r) {
@@ -320,7 +327,7 @@ __device__ __forceinline__ float4 sum_partials(const float* base, size_t slot, i
 
 // Reduce + apply nodes [lo, hi) of m-tile mt from the global partials; the NW
 // reducer warps take nodes round-robin.
-template <int NW>
+template <int NW, bool PRE>
 __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, int n, int mt, int cnt, int lo,
                                              int hi, int ew, int lane, const float* rs) {
   const float* base = e.part + (size_t)mt * p.max_contrib * n * kBM;
@@ -345,7 +352,7 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
         const int c = c0 + r * NW;
         x[r] = EpiAux{};
         if (c < hi) {
-          epi_aux(e, mt, f, c, x[r], rs);
+          epi_aux<PRE>(e, mt, f, c, x[r], rs);
           const float* b = base + (size_t)c * kBM + f;
 #pragma unroll
           for (int s = 0; s < kMaxC; ++s) v[r][s] = s < cnt ? ld4cg(b + s * slot) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -367,13 +374,13 @@ __device__ __forceinline__ void reduce_apply(const GemmEpi& e, const SkPlan& p, 
   }
   for (int c = lo + ew; c < hi; c += NW) {
     EpiAux x0{};
-    epi_aux(e, mt, f, c, x0, rs);
+    epi_aux<PRE>(e, mt, f, c, x0, rs);
     epi_finish(e, mt, lane, c, sum_partials(base, slot, cnt, c, f), x0);
   }
 }
 
 // Apply nodes c0 .. c0+cn-1 staged in xch[node][feature] (sole-contributor path).
-template <int NW>
+template <int NW, bool PRE>
 __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int cn, const float* xch, const float* rs,
                                            int ew,
                                            int lane) {
@@ -381,7 +388,7 @@ __device__ __forceinline__ void smem_apply(const GemmEpi& e, int mt, int c0, int
   for (int cc = ew; cc < cn; cc += NW) {
     const float4 y0 = *reinterpret_cast<const float4*>(xch + cc * kXchLd + f);
     EpiAux x0{};
-    epi_aux(e, mt, f, c0 + cc, x0, rs);
+    epi_aux<PRE>(e, mt, f, c0 + cc, x0, rs);
     epi_finish(e, mt, lane, c0 + cc, y0, x0);
   }
 }
@@ -624,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             drain_bar();
             if (et == 0 && c0 == 0) GSTAMP(14);
-            smem_apply<kDrainWarps>(e, mt, c0, cn, xch, kPreR ? rsc + g * 256 : nullptr, ew, lane);
+            smem_apply<kDrainWarps, kPreR>(e, mt, c0, cn, xch, rsc + g * 256, ew, lane);
             drain_bar();
             if (et == 0 && c0 == 0) GSTAMP(15);
           }
@@ -712,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         GSTAMP(6);
       }
       red_bar();
-      reduce_apply<kRedWarps>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane,
+      reduce_apply<kRedWarps, kPreR>(e, p, n, it.mt, it.cnt, n * rank / E, n * (rank + 1) / E, rw, lane,
                               kPreR ? rsc + it.g * 256 : nullptr);
       if (rt == 0) GSTAMP(7);
     }

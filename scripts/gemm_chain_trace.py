@@ -24,6 +24,7 @@ from paper_2504_04104_b200.pipeline import PipelineConfig, PipelineRunner  # noq
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=45)
 ap.add_argument("--prefix", type=int, default=512)
+ap.add_argument("--group", default="", help="grouped forward instead: node counts of stages 1..7, e.g. 45,35,29,23,17,11,3")
 args = ap.parse_args()
 cfg = model_cfg("7b")
 m = LlamaModel(cfg, max_nodes=64)
@@ -40,6 +41,14 @@ bits = ((np.uint64(1) << d.astype(np.uint64)) - np.uint64(1)).reshape(n, 1).asty
 x = torch.randn(n, cfg.hidden, device="cuda") * 0.5
 members = [[(s.kv, m, x, None, (args.prefix + d).tolist(), s.layer_range, False, list(range(n)), False,
              (pre, args.prefix, 1, bits))]]
+if args.group:  # one member per stage, as the bench's phase-1 grouped launch
+    members = []
+    for st, ng in zip(r.stages, [int(v) for v in args.group.split(",")]):
+        dg = rng.integers(0, depth, ng)
+        bg = ((np.uint64(1) << dg.astype(np.uint64)) - np.uint64(1)).reshape(ng, 1).astype(np.uint64)
+        members.append([(st.kv, m, torch.randn(ng, cfg.hidden, device="cuda") * 0.5, None, (args.prefix + dg).tolist(),
+                         st.layer_range, False, list(range(ng)), False, (np.full(ng, args.prefix, dtype=np.int32),
+                                                                         args.prefix, 1, bg))])
 lib = _lib.lib()
 for _ in range(5):
     forward_members(members)

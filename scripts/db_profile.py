@@ -76,9 +76,10 @@ def timed(name, fn):
     return w
 
 
-sched._combined_compute = timed("combined_compute", sched._combined_compute)
+sched._combined_launch = timed("combined_launch", sched._combined_launch)
+sched._combined_wait = timed("combined_wait", sched._combined_wait)
 for slot in sched.active:
-    slot.runner.decode_step = timed("decode_step", slot.runner.decode_step)
+    slot.runner.draft_children = timed("draft_children", slot.runner.draft_children)
     slot.runner.step = timed("step", slot.runner.step)
 M._launch_restrict = timed("flush_restrict", M._launch_restrict)
 M._launch_rows = timed("flush_rows", M._launch_rows)

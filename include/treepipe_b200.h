@@ -47,7 +47,7 @@ typedef struct tp_model_config {
   int32_t layer_lo, layer_hi;                /* layers hosted by this object        */
   int32_t with_embed, with_head;             /* embedding table / final norm + head */
   int32_t device;
-  int32_t max_nodes;                         /* nodes per forward launch            */
+  int32_t max_nodes;                         /* nodes per forward launch (<= 1024; Llama <= 256) */
   float rope_theta, norm_eps;
   int32_t weight_scale;                      /* llama: 1 = x sqrt(3/fan_in)/0.1     */
 } tp_model_config;

@@ -352,6 +352,9 @@ int tp_model_create(const tp_model_config* cfg, tp_model** out) {
   TP_CHECK(0 <= c.layer_lo && c.layer_lo <= c.layer_hi && c.layer_hi <= c.layers, TP_ECONFIG,
            "hosted layer range outside the model");
   TP_CHECK(c.max_nodes >= 1 && c.max_nodes <= 1024, TP_ECONFIG, "max_nodes must lie in [1, 1024]");
+  // a Llama forward is one K2 GEMM per layer slot over all of a member's rows
+  TP_CHECK(c.arch != TP_ARCH_LLAMA || c.max_nodes <= 256, TP_ECONFIG,
+           "Llama max_nodes must lie in [1, 256] (rows per K2 GEMM)");
   TP_CUDA(cudaSetDevice(c.device));
   tp_model* m = new tp_model();
   m->cfg = c;

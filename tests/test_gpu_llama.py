@@ -611,3 +611,14 @@ def test_pipeline_lossless_randomized(seed):
     torch.cuda.synchronize()
     assert r.emitted[:20] == ref[:20], (seed, stages, w, k, heads, kv, sharded, dm is not None)
     r.release()
+
+
+@pytest.mark.gpu
+def test_llama_max_nodes_limit():
+    """A Llama forward is one K2 GEMM over a member's rows (<= 256): larger
+    max_nodes is refused when the model is created, not at the first forward."""
+    from paper_2504_04104_b200.errors import ConfigError
+
+    with pytest.raises(ConfigError):
+        LlamaModel(LlamaConfig(**TINY), max_nodes=257)
+    LlamaModel(LlamaConfig(**TINY), max_nodes=256)
